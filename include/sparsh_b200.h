@@ -1,0 +1,209 @@
+/*
+ * sparsh_b200.h — C ABI of the B200-native solve phase (libsparsh_b200.so).
+ *
+ * Drop-in boundary for the reference's solve-phase API (sparsh, C++20,
+ * /root/reference/proj/include/sparsh). Each entry point cites the reference
+ * interface it replaces; INTEGRATION.md shows the binding a maintainer adds.
+ * Plain pointers and sizes only: no C++ or torch types cross this boundary.
+ *
+ * Status codes (every int-returning call):
+ *   SB_OK       0  success
+ *   SB_EINVAL   1  the reference would throw std::invalid_argument
+ *   SB_ERUNTIME 2  the reference would throw std::runtime_error
+ *                  (amg_solve divergence, singular coarse pivot)
+ *   SB_ECUDA    3  CUDA / NCCL failure (no CPU fallback exists)
+ * sb_last_error() returns the thread-local message of the last failure,
+ * phrased like the reference's exception text ("diverged", "zero diagonal
+ * entry in row i", ...).
+ *
+ * Threading: a built hierarchy (sb_hier) is immutable and shareable. A device
+ * context (sb_ctx) owns mutable device workspaces and CUDA graphs, so one
+ * context serves one solve at a time (the one deviation from the reference's
+ * "concurrent V-cycles are safe"). Termination codes equal the
+ * reference enum order (inc/convergence.hpp:15).
+ */
+#ifndef SPARSH_B200_H
+#define SPARSH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SB_OK 0
+#define SB_EINVAL 1
+#define SB_ERUNTIME 2
+#define SB_ECUDA 3
+
+/* inc/convergence.hpp:15 */
+#define SB_CONVERGED 0
+#define SB_MAX_ITERS 1
+#define SB_BREAKDOWN 2
+#define SB_DIVERGED 3
+
+/* inc/smoother.hpp:23-28 — only weighted Jacobi runs on the device; the
+ * Gauss-Seidel families are rejected with SB_EINVAL (no CPU emulation). */
+#define SB_SMOOTHER_JACOBI 0
+#define SB_SMOOTHER_GS_FORWARD 1
+#define SB_SMOOTHER_GS_BACKWARD 2
+#define SB_SMOOTHER_GS_SYMMETRIC 3
+
+/* Host CSR matrix, borrowed. Mirrors sparsh::CsrMatrix (inc/csr.hpp:44-169):
+ * int32 column indices strictly increasing per row, f64 values. Row offsets
+ * are int32 (the reference's index_t, inc/csr.hpp:22; zero-copy from a
+ * CsrMatrix) or int64 (for nnz > INT32_MAX): set exactly one of the two. */
+typedef struct {
+    int64_t nrows;
+    int64_t ncols;
+    const int32_t *row_ptr32;
+    const int64_t *row_ptr64;
+    const int32_t *col_idx;
+    const double *values;
+} sb_csr;
+
+/* inc/config.hpp:81-105 (setup subset). coarsening: 0 node_hem (1 edge_hem is
+ * rejected); coarse_solver: 0 direct (1 cg is rejected on the device path;
+ * -1 = no coarse factorization, for identity-preconditioned cg/bicgstab only). */
+typedef struct {
+    int coarsening;
+    int64_t coarse_target;
+    int max_levels;
+    int coarse_solver;
+    int threads; /* host threads for the Galerkin product (0 = all) */
+} sb_setup_opts;
+
+/* inc/cycle.hpp:24-32 (CycleParams) */
+typedef struct {
+    int pre_sweeps;
+    int post_sweeps;
+    int smoother; /* SB_SMOOTHER_* */
+    double omega; /* Jacobi weight, (0, 1] (inc/smoother.hpp:33-38) */
+} sb_cycle;
+
+/* inc/convergence.hpp:33-42 (ConvergenceReport). The caller owns the history
+ * buffers (hist_cap entries each, may be NULL); hist_len is the reference's
+ * residual_history.size() (= iterations + 1), even when > hist_cap. */
+typedef struct {
+    int iterations;
+    int termination;
+    double wall_time;
+    double true_residual;
+    int hist_len;
+    int hist_cap;
+    double *residual_history;
+    double *time_history;
+} sb_report;
+
+/* Device-context options. */
+typedef struct {
+    int device;          /* CUDA ordinal */
+    int use_graphs;      /* 1: whole-solve CUDA graph with device-side loop control (default) */
+    int64_t host_levels_from; /* hybrid mode: levels >= this index stay on the host
+                                 (paper's MI scheme); -1 = all levels device-resident */
+} sb_device_opts;
+
+typedef struct sb_hier_s *sb_hier;
+typedef struct sb_ctx_s *sb_ctx;
+
+const char *sb_last_error(void);
+const char *sb_version(void);
+
+/* ---- host setup: bit-exact with the reference ---------------------------- */
+
+/* sparsh::Hierarchy(CsrMatrix, SolverConfig) — inc/hierarchy.hpp:51-76:
+ * node-HEM (inc/coarsen.hpp:31-73) + Galerkin (inc/aggregation.hpp:92-152)
+ * until n <= coarse_target or max_levels, then the dense LU of the coarsest
+ * level (inc/coarse_solver.hpp:129-166; > 2000 rows -> SB_EINVAL, the sparse
+ * LU path is not provided). Deep-copies A. */
+int sb_setup(const sb_csr *A, const sb_setup_opts *opts, sb_hier *out);
+/* Adopt a hierarchy built elsewhere (e.g. by the reference itself): levels[k]
+ * and fine_to_coarse[k] (k < nlevels-1) exactly as sparsh::Level holds them
+ * (inc/hierarchy.hpp:24-28). The coarse LU is factorized here. */
+int sb_hier_from_levels(int nlevels, const sb_csr *levels, const int32_t *const *fine_to_coarse,
+                        sb_hier *out);
+void sb_hier_free(sb_hier h);
+int sb_hier_nlevels(sb_hier h);                        /* Hierarchy::nlevels, :78 */
+int sb_hier_stalled(sb_hier h);                        /* Hierarchy::coarsening_stalled, :82 */
+/* Borrowed views of level k (valid while h lives): A (row_ptr32 set when it fits),
+ * the aggregation (NULL on the coarsest level), n_coarse (-1 on the coarsest). */
+int sb_hier_level(sb_hier h, int k, sb_csr *A, const int32_t **fine_to_coarse, int64_t *n_coarse);
+/* Coarse factorization counters (inc/coarse_solver.hpp:75-77). */
+int sb_hier_coarse_counts(sb_hier h, long *symbolic, long *numeric, long *solves);
+
+/* ---- device context --------------------------------------------------------- */
+
+/* Upload every level (CSR, diagonal, aggregate maps) plus the coarse inverse
+ * to the device; allocate workspaces; record graphs lazily per sb_cycle. */
+int sb_create(sb_hier h, const sb_device_opts *opts, sb_ctx *out);
+void sb_destroy(sb_ctx ctx);
+/* Device bytes resident for the hierarchy (paper's memory metric). */
+int64_t sb_device_bytes(sb_ctx ctx);
+/* The CUDA stream the context launches on (cudaStream_t as void*). */
+void *sb_stream(sb_ctx ctx);
+
+/* ---- solve phase (the hot path) ------------------------------------------- */
+
+/* vcycle_in_place(h, k, f, x, p) — inc/cycle.hpp:53-75. Host vectors of level
+ * k's size; x_is_zero promises x == 0 on entry (the preconditioner case,
+ * inc/cycle.hpp:140-144). */
+int sb_vcycle(sb_ctx ctx, const sb_cycle *cp, int level, const double *f, double *x);
+/* Same on device pointers (stream-ordered on sb_stream). */
+int sb_vcycle_dev(sb_ctx ctx, const sb_cycle *cp, int level, const double *d_f, double *d_x,
+                  int x_is_zero);
+
+/* pcg(A, b, make_amg_preconditioner(h, cp), tol, max_iters) — inc/krylov.hpp:65-119
+ * with inc/cycle.hpp:137-145. A is level 0 of the context. cp == NULL selects
+ * Preconditioner::identity() (inc/krylov.hpp:33-35), i.e. cg(). tol is the
+ * reference's ABSOLUTE tolerance. x receives the solution. */
+int sb_pcg(sb_ctx ctx, const sb_cycle *cp, const double *b, double *x, double tol,
+           int max_iters, sb_report *rep);
+/* pbicgstab(...) — inc/krylov.hpp:126-211 (flexible; cp == NULL -> bicgstab()). */
+int sb_pbicgstab(sb_ctx ctx, const sb_cycle *cp, const double *b, double *x, double tol,
+                 int max_iters, sb_report *rep);
+/* amg_solve(h, b, tol, max_cycles, p) — inc/cycle.hpp:91-130. Divergence ->
+ * SB_ERUNTIME ("amg_solve: diverged ..."), report still filled. */
+int sb_amg_solve(sb_ctx ctx, const sb_cycle *cp, const double *b, double *x, double tol,
+                 int max_cycles, sb_report *rep);
+/* Device-pointer variants (inputs already resident; the bench's kernel-only number). */
+int sb_pcg_dev(sb_ctx ctx, const sb_cycle *cp, const double *d_b, double *d_x, double tol,
+               int max_iters, sb_report *rep);
+int sb_pbicgstab_dev(sb_ctx ctx, const sb_cycle *cp, const double *d_b, double *d_x,
+                     double tol, int max_iters, sb_report *rep);
+
+/* ---- single kernels on a level (unit parity; host vectors) --------------- */
+
+/* spmv(A_k, x, y) — inc/csr.hpp:174-194 */
+int sb_spmv(sb_ctx ctx, int level, const double *x, double *y);
+/* smooth_in_place(jacobi, A_k, x, f, sweeps) — inc/smoother.hpp:95-123 */
+int sb_smooth(sb_ctx ctx, int level, const sb_cycle *cp, double *x, const double *f, int sweeps);
+/* residual(A_k, x, f) — inc/csr.hpp:267-274 */
+int sb_residual(sb_ctx ctx, int level, const double *x, const double *f, double *r);
+/* spmv_transpose(P_k, r) — inc/csr.hpp:226-241, inc/cycle.hpp:69 */
+int sb_restrict(sb_ctx ctx, int level, const double *r, double *f_coarse);
+/* x += spmv(P_k, x_c) — inc/cycle.hpp:72-73 */
+int sb_prolong(sb_ctx ctx, int level, const double *x_coarse, double *x);
+/* CoarseFactorization::solve — inc/coarse_solver.hpp:63-71 */
+int sb_coarse_solve(sb_ctx ctx, const double *f, double *x);
+
+/* ---- problem generators (harness inputs) ------------------- */
+
+/* convdiff2d(nx, ny, bx, by, c) — inc/problems.hpp:28-57, bit-identical.
+ * Arrays allocated with malloc; free with sb_free_csr. */
+int sb_gen_convdiff2d(int64_t nx, int64_t ny, double bx, double by, double c, sb_csr *out);
+/* 3D 7-point: diag, and off-diagonals (x-, x+, y-, y+, z-, z+). */
+int sb_gen_stencil7(int64_t nx, int64_t ny, int64_t nz, double diag, const double off[6],
+                    sb_csr *out);
+/* 3D 7-point upwind convection-diffusion, cell-volume scaled like convdiff2d. */
+int sb_gen_convdiff3d(int64_t nx, int64_t ny, int64_t nz, double bx, double by, double bz,
+                      double c, sb_csr *out);
+/* 3D 27-point: diag, -1 to every neighbour (times off). */
+int sb_gen_stencil27(int64_t nx, int64_t ny, int64_t nz, double diag, double off, sb_csr *out);
+void sb_free_csr(sb_csr *m);
+/* rhs_random(n, seed) — inc/problems.hpp:69-75 (std::mt19937, U[0,1)), bit-identical. */
+int sb_gen_rhs_random(int64_t n, unsigned seed, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1327 @@
+// B200-native solve phase: device hierarchy, sm_100a kernels, CUDA-graph
+// Krylov drivers with device-side loop control, and the C ABI
+// (include/sparsh_b200.h). See DESIGN.md for layout, kernels and rooflines.
+//
+// Reference (paths under /root/reference/proj/include/sparsh/):
+//   spmv            csr.hpp:174-194      -> k_csr_tile<SPMV>
+//   residual        csr.hpp:267-274      -> k_csr_tile<RESID>
+//   Jacobi sweep    smoother.hpp:109-121 -> k_csr_tile<JACOBI>, k_jacobi_zero
+//   restriction     cycle.hpp:69 (+ csr.hpp:226-241)  -> k_restrict
+//   prolongation    cycle.hpp:72-73      -> k_prolong
+//   coarse solve    coarse_solver.hpp:63-71,168-182  -> k_coarse_gemv
+//   V-cycle         cycle.hpp:53-75      -> emit_vcycle
+//   pcg             krylov.hpp:65-119    -> build_pcg_graph
+//   pbicgstab       krylov.hpp:126-211   -> build_bicg_graph
+//   amg_solve       cycle.hpp:91-130     -> build_amg_graph
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "sb_internal.h"
+#include "sb_kernels.cuh"
+
+namespace sb {
+
+thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            throw sb::cuda_error(std::string(#x) + ": " + cudaGetErrorString(e_));              \
+    } while (0)
+
+// ===========================================================================
+// device helpers
+// ===========================================================================
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile("{\n"
+                 ".reg .pred P1;\n"
+                 "WAIT_%=:\n"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                 "@!P1 bra WAIT_%=;\n"
+                 "}\n" ::"r"(smem_u32(bar)),
+                 "r"(phase)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Deterministic block reduction of NV doubles (fixed shuffle tree, fixed warp
+// order); the result is valid in thread 0.
+template <int NV> __device__ __forceinline__ void block_reduce(double (&a)[NV], double *sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) a[v] += __shfl_down_sync(0xffffffffu, a[v], off);
+    if (lane == 0)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sh[v * 32 + warp] = a[v];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            a[v] = lane < nwarps ? sh[v * 32 + lane] : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) a[v] += __shfl_down_sync(0xffffffffu, a[v], off);
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void record(DevState *st, int k, double v) {
+    if (k < st->hist_cap) {
+        st->hist_r[k] = v;
+        st->hist_t[k] = static_cast<double>(globaltimer() - st->t0) * 1e-9;
+    }
+}
+
+// Krylov scalar logic; runs in ONE thread after the grid-wide reduction.
+// Each case restates the reference's scalar control flow (file:line noted).
+__device__ void epilogue(const Red &r, double a, double b) {
+    DevState *st = r.st;
+    constexpr double eps = 1e-300;  // krylov.hpp:130
+    constexpr double divf = 1e6;    // krylov.hpp:26
+    switch (r.op) {
+    case EP_STORE:
+        st->true_res = sqrt(a);
+        break;
+    case EP_INIT_NORM: {  // krylov.hpp:78-84 / 141-146, cycle.hpp:111-114
+        const double rn = sqrt(a);
+        st->rn = rn;
+        st->r0 = rn;
+        st->iter = 0;
+        st->status = 0;
+        st->half = 0;
+        st->term = SB_MAX_ITERS;
+        st->done = 0;
+        st->true_res = rn;
+        record(st, 0, rn);
+        if (rn < st->tol) {
+            st->term = SB_CONVERGED;
+            st->done = 1;
+        } else if (st->max_iters <= 0) {
+            st->done = 1;
+        }
+        break;
+    }
+    case EP_PCG_RZ0:  // krylov.hpp:87
+        st->rz = a;
+        break;
+    case EP_PCG_PAP:  // krylov.hpp:90-95
+        if (st->done) break;
+        st->pAp = a;
+        if (a <= 0.0) {
+            st->term = SB_BREAKDOWN;
+            st->done = 1;
+        } else {
+            st->alpha = st->rz / a;
+        }
+        break;
+    case EP_PCG_RN: {  // krylov.hpp:98-108
+        if (st->done) break;
+        const double rn = sqrt(a);
+        const int it = st->iter + 1;
+        st->rn = rn;
+        record(st, it, rn);
+        st->iter = it;
+        if (rn < st->tol) {
+            st->term = SB_CONVERGED;
+            st->done = 1;
+        } else if (rn > divf * st->r0) {
+            st->term = SB_DIVERGED;
+            st->done = 1;
+        } else if (it >= st->max_iters) {
+            st->done = 1;
+        }
+        break;
+    }
+    case EP_PCG_RZ:  // krylov.hpp:110-112
+        if (st->done) break;
+        st->beta = a / st->rz;
+        st->rz = a;
+        break;
+    case EP_BI_RHO0:  // krylov.hpp:150-155
+        st->rho = a;
+        if (!st->done && fabs(a) < eps) {
+            st->term = SB_BREAKDOWN;
+            st->done = 1;
+        }
+        break;
+    case EP_BI_DENOM:  // krylov.hpp:158-163
+        if (st->done) break;
+        st->denom = a;
+        if (fabs(a) < eps) {
+            st->term = SB_BREAKDOWN;
+            st->done = 1;
+        } else {
+            st->alpha = st->rho / a;
+        }
+        break;
+    case EP_BI_SN: {  // krylov.hpp:166-173
+        if (st->done) break;
+        const double sn = sqrt(a);
+        st->sn = sn;
+        if (sn < st->tol) {
+            const int it = st->iter + 1;
+            record(st, it, sn);
+            st->iter = it;
+            st->half = 1;
+            st->term = SB_CONVERGED;
+            st->done = 1;
+        }
+        break;
+    }
+    case EP_BI_AS:  // krylov.hpp:176-181
+        if (st->done) break;
+        if (a < eps) {
+            st->term = SB_BREAKDOWN;
+            st->done = 1;
+        } else {
+            st->omega = b / a;
+        }
+        break;
+    case EP_BI_RN_RHO: {  // krylov.hpp:186-203 (+ the loop-top rho test, :152)
+        if (st->done) break;
+        const double rn = sqrt(a);
+        const int it = st->iter + 1;
+        st->rn = rn;
+        record(st, it, rn);
+        st->iter = it;
+        if (rn < st->tol) {
+            st->term = SB_CONVERGED;
+            st->done = 1;
+        } else if (rn > divf * st->r0) {
+            st->term = SB_DIVERGED;
+            st->done = 1;
+        } else if (fabs(st->omega) < eps) {
+            st->term = SB_BREAKDOWN;
+            st->done = 1;
+        } else {
+            const double rho_next = b;
+            st->beta = (rho_next / st->rho) * (st->alpha / st->omega);
+            st->rho = rho_next;
+            if (it >= st->max_iters) {
+                st->done = 1;
+            } else if (fabs(st->rho) < eps) {
+                st->term = SB_BREAKDOWN;
+                st->done = 1;
+            }
+        }
+        break;
+    }
+    case EP_AMG_RN: {  // cycle.hpp:118-125
+        if (st->done) break;
+        const double rn = sqrt(a);
+        const int it = st->iter + 1;
+        st->rn = rn;
+        st->true_res = rn;
+        record(st, it, rn);
+        st->iter = it;
+        if (rn > divf * st->r0) {
+            st->status = 2;
+            st->done = 1;
+        } else if (rn < st->tol) {
+            st->term = SB_CONVERGED;
+            st->done = 1;
+        } else if (it >= st->max_iters) {
+            st->done = 1;
+        }
+        break;
+    }
+    default:
+        break;
+    }
+    for (int i = 0; i < r.cs.n; ++i)
+        cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(r.cs.h[i]),
+                                st->done ? 0u : 1u);
+}
+
+// Grid-wide deterministic reduction + epilogue. Every thread of every block
+// must call it (it contains barriers).
+template <int NV> __device__ __forceinline__ void finish_reduction(const Red &r, double (&a)[NV]) {
+    __shared__ double sh[2 * 32];
+    __shared__ int am_last;
+    block_reduce<NV>(a, sh);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) r.partials[2 * blockIdx.x + v] = a[v];
+        __threadfence();
+        const unsigned t = atomicAdd(r.counter, 1u);
+        am_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    double s[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) s[v] = 0.0;
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += blockDim.x)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) s[v] += __ldcg(&r.partials[2 * b + v]);
+    block_reduce<NV>(s, sh);
+    if (threadIdx.x == 0) {
+        *r.counter = 0u;
+        epilogue(r, s[0], NV > 1 ? s[NV > 1 ? 1 : 0] : 0.0);
+    }
+}
+
+// ===========================================================================
+// CSR tile kernel: SpMV / residual / Jacobi sweep (+ optional fused dot)
+// ===========================================================================
+
+enum CsrMode { M_SPMV = 0, M_RESID = 1, M_JACOBI = 2 };
+
+// One CTA per tile of <= 256 consecutive rows (tile_ptr from setup). The tile's
+// contiguous nnz range of values and column indices is brought into shared
+// memory by two TMA bulk copies (16-byte aligned windows), then thread t owns
+// row r0+t and walks it in CSR order. Tiles whose nnz exceed the staging
+// capacity (a single very long row) read straight from global memory.
+template <int MODE, int NV>
+__global__ void __launch_bounds__(kTileRows)
+    k_csr_tile(const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+               const double *__restrict__ val, const int32_t *__restrict__ tile_ptr,
+               const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out,
+               double omega, int cap, const int *skip, Red red) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar;
+    double acc[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
+
+    const bool active = !(skip && *skip);
+    if (active) {
+        const int r0 = tile_ptr[blockIdx.x], r1 = tile_ptr[blockIdx.x + 1];
+        const int e0 = rp[r0], e1 = rp[r1];
+        const bool staged = (e1 - e0) <= cap;
+        const int va0 = e0 & ~1, ca0 = e0 & ~3;
+        const int cap_v = (cap + 3) & ~1;  // doubles
+        double *sv = reinterpret_cast<double *>(smem);
+        int32_t *sc = reinterpret_cast<int32_t *>(smem + static_cast<size_t>(cap_v) * 8);
+        if (staged && threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            fence_mbar_init();
+            const uint32_t vbytes = static_cast<uint32_t>(((e1 + 1) & ~1) - va0) * 8u;
+            const uint32_t cbytes = static_cast<uint32_t>(((e1 + 3) & ~3) - ca0) * 4u;
+            mbar_expect_tx(&bar, vbytes + cbytes);
+            if (vbytes) bulk_g2s(sv, val + va0, vbytes, &bar);
+            if (cbytes) bulk_g2s(sc, ci + ca0, cbytes, &bar);
+            if (vbytes + cbytes == 0) mbar_expect_tx(&bar, 0);
+        }
+        const int row = r0 + static_cast<int>(threadIdx.x);
+        int rs = 0, re = 0;
+        double fi = 0.0, xi = 0.0;
+        if (row < r1) {
+            rs = rp[row];
+            re = rp[row + 1];
+            if (MODE != M_SPMV) fi = f[row];
+            if (MODE == M_JACOBI) xi = x[row];
+        }
+        __syncthreads();  // barrier init visible before anyone waits
+        if (staged) mbar_wait(&bar, 0);
+        if (row < r1) {
+            double sum = 0.0, d = 0.0;
+            const int32_t *cc = staged ? sc - ca0 : ci;
+            const double *vv = staged ? sv - va0 : val;
+            for (int k = rs; k < re; k += 8) {
+                int c[8];
+                double a[8], xv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (k + u < re) {
+                        c[u] = cc[k + u];
+                        a[u] = vv[k + u];
+                    }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (k + u < re) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (k + u < re) {
+                        sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
+                        if (MODE == M_JACOBI && c[u] == row) d = a[u];
+                    }
+            }
+            double o;
+            if (MODE == M_SPMV) o = sum;
+            else if (MODE == M_RESID) o = __dsub_rn(fi, sum);
+            else o = __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
+            out[row] = o;
+            if (NV >= 1) acc[0] = o * (red.w0 ? red.w0[row] : o);
+            if (NV >= 2) acc[NV >= 2 ? 1 : 0] = o * (red.w1 ? red.w1[row] : o);
+        }
+    }
+    if constexpr (NV > 0) finish_reduction<NV>(red, acc);
+}
+
+// First pre-smoothing sweep from x = 0: the reference computes
+// x_i = 0 + omega*(f_i - 0)/a_ii with spmv(A, 0) = +0.0 (smoother.hpp:112-119).
+__global__ void k_jacobi_zero(int64_t n, const double *__restrict__ f,
+                              const double *__restrict__ diag, double *__restrict__ x, double omega) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        x[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, f[i]), diag[i]));
+}
+
+// f_c[c] = (0.0 + r[m0]) + r[m1], members ascending (csr.hpp:232-239 with unit P).
+__global__ void k_restrict(int64_t nc, const int2 *__restrict__ mem, const double *__restrict__ r,
+                           double *__restrict__ fc) {
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < nc;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int2 m = mem[c];
+        double s = __dadd_rn(0.0, r[m.x]);
+        if (m.y >= 0) s = __dadd_rn(s, r[m.y]);
+        fc[c] = s;
+    }
+}
+
+// out_i = in_i + (0.0 + x_c[agg_i]) (cycle.hpp:72-73: spmv(P, x_c) then axpy(1.0, ...)).
+__global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const double *xin,
+                          const double *__restrict__ xc, double *xout) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        xout[i] = __dadd_rn(xin[i], __dadd_rn(0.0, xc[agg[i]]));
+}
+
+// Coarsest-level solve z = A_c^{-1} f with the precomputed inverse (one warp
+// per row, fixed shuffle tree).
+__global__ void k_coarse_gemv(int n, const double *__restrict__ inv, const double *__restrict__ f,
+                              double *__restrict__ x) {
+    const int lane = threadIdx.x & 31;
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= n) return;
+    const double *a = inv + static_cast<size_t>(row) * n;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s += a[j] * f[j];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) x[row] = s;
+}
+
+// ---- Krylov vector kernels (grid-stride, fixed grid => deterministic) -----
+
+#define GRID_LOOP(i, n)                                                                          \
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < (n);      \
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+
+// x = 0, r = b, ||b||^2 (krylov.hpp:70-79, cycle.hpp:105-111)
+__global__ void k_init(int64_t n, const double *__restrict__ b, double *__restrict__ x,
+                       double *__restrict__ r, Red red) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) red.st->t0 = globaltimer();
+    double a[1] = {0.0};
+    GRID_LOOP(i, n) {
+        const double bi = b[i];
+        x[i] = 0.0;
+        if (r) r[i] = bi;
+        a[0] += bi * bi;
+    }
+    finish_reduction<1>(red, a);
+}
+
+// dst = src; sum src*w  (PCG: p = z, rz = (r, z); BiCGStab: rbar = p = r, rho = (r, rbar))
+__global__ void k_copy_dot(int64_t n, const double *__restrict__ src, double *__restrict__ dst,
+                           double *__restrict__ dst2, const double *__restrict__ w, Red red) {
+    double a[1] = {0.0};
+    GRID_LOOP(i, n) {
+        const double s = src[i];
+        dst[i] = s;
+        if (dst2) dst2[i] = s;
+        a[0] += s * w[i];
+    }
+    finish_reduction<1>(red, a);
+}
+
+__global__ void k_dot(int64_t n, const double *__restrict__ u, const double *__restrict__ v,
+                      const int *skip, Red red) {
+    double a[1] = {0.0};
+    if (!(skip && *skip)) {
+        GRID_LOOP(i, n) a[0] += u[i] * v[i];
+    }
+    finish_reduction<1>(red, a);
+}
+
+// PCG update (krylov.hpp:96-98): x += alpha p; r += (-alpha) Ap; ||r||^2
+__global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
+                             const double *__restrict__ p, const double *__restrict__ Ap, Red red) {
+    double a[1] = {0.0};
+    const DevState *st = red.st;
+    if (!st->done) {
+        const double alpha = st->alpha, nalpha = -st->alpha;
+        GRID_LOOP(i, n) {
+            x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+            const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
+            r[i] = ri;
+            a[0] += ri * ri;
+        }
+    }
+    finish_reduction<1>(red, a);
+}
+
+// p = z + beta p (krylov.hpp:113)
+__global__ void k_xpay(int64_t n, const double *__restrict__ z, double *__restrict__ p,
+                       const DevState *__restrict__ st) {
+    const double beta = st->beta;
+    GRID_LOOP(i, n) p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+}
+
+// BiCGStab s = r + (-alpha) Ap~; ||s||^2 (krylov.hpp:164-166)
+__global__ void k_bi_s(int64_t n, const double *__restrict__ r, const double *__restrict__ Apt,
+                       double *__restrict__ s, Red red) {
+    double a[1] = {0.0};
+    const DevState *st = red.st;
+    if (!st->done) {
+        const double nalpha = -st->alpha;
+        GRID_LOOP(i, n) {
+            const double si = __dadd_rn(r[i], __dmul_rn(nalpha, Apt[i]));
+            s[i] = si;
+            a[0] += si * si;
+        }
+    }
+    finish_reduction<1>(red, a);
+}
+
+// Half-step exit: x += alpha p~ (krylov.hpp:168), only when EP_BI_SN fired.
+__global__ void k_bi_half(int64_t n, double *__restrict__ x, const double *__restrict__ pt,
+                          const DevState *__restrict__ st) {
+    if (!st->half) return;
+    const double alpha = st->alpha;
+    GRID_LOOP(i, n) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pt[i]));
+}
+
+// x += alpha p~; x += omega s~; r = s + (-omega) As~; ||r||^2, (r, rbar0)  (krylov.hpp:182-186, 201)
+__global__ void k_bi_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
+                            const double *__restrict__ pt, const double *__restrict__ st_,
+                            const double *__restrict__ s, const double *__restrict__ Ast,
+                            const double *__restrict__ rbar, Red red) {
+    double a[2] = {0.0, 0.0};
+    const DevState *st = red.st;
+    if (!st->done) {
+        const double alpha = st->alpha, omega = st->omega, nomega = -st->omega;
+        GRID_LOOP(i, n) {
+            double xi = __dadd_rn(x[i], __dmul_rn(alpha, pt[i]));
+            x[i] = __dadd_rn(xi, __dmul_rn(omega, st_[i]));
+            const double ri = __dadd_rn(s[i], __dmul_rn(nomega, Ast[i]));
+            r[i] = ri;
+            a[0] += ri * ri;
+            a[1] += ri * rbar[i];
+        }
+    }
+    finish_reduction<2>(red, a);
+}
+
+// p = r + beta (p - omega Ap~)  (krylov.hpp:204-205)
+__global__ void k_bi_p(int64_t n, const double *__restrict__ r, double *__restrict__ p,
+                       const double *__restrict__ Apt, const DevState *__restrict__ st) {
+    if (st->done) return;
+    const double beta = st->beta, omega = st->omega;
+    GRID_LOOP(i, n)
+    p[i] = __dadd_rn(r[i], __dmul_rn(beta, __dsub_rn(p[i], __dmul_rn(omega, Apt[i]))));
+}
+
+__global__ void k_set_cond(const DevState *st, CondSet cs) {
+    for (int i = 0; i < cs.n; ++i)
+        cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(cs.h[i]), st->done ? 0u : 1u);
+}
+
+// ===========================================================================
+// device hierarchy + context
+// ===========================================================================
+
+struct DevLevel {
+    int64_t n = 0, nnz = 0, nc = -1;
+    int32_t *rp = nullptr, *ci = nullptr, *agg = nullptr, *tiles = nullptr;
+    double *v = nullptr, *diag = nullptr;
+    int2 *mem = nullptr;
+    int ntiles = 0, cap = 0;
+    size_t smem = 0;
+    double *x = nullptr, *f = nullptr, *t = nullptr;
+    int64_t bad_diag = -1;
+};
+
+struct Cyc {
+    int pre = 6, post = 6;
+    double omega = 2.0 / 3.0;
+};
+
+struct GraphEntry {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+} // namespace sb
+
+struct sb_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t cap[8] = {};
+    std::vector<sb::DevLevel> L;
+    int64_t nc = 0;
+    double *inv = nullptr;
+    double *rs = nullptr;  // residual scratch (level sizes <= n0)
+    double *kv[12] = {};   // Krylov vectors
+    double *partials = nullptr;
+    unsigned *counter = nullptr;
+    sb::DevState *st = nullptr;
+    double *hist_r = nullptr, *hist_t = nullptr;
+    int hist_cap = 0;
+    int64_t bytes = 0;
+    int nvec_blocks = 1;
+    bool graphs = true;
+    std::vector<void *> allocs;
+    std::map<std::string, sb::GraphEntry> cache;
+    double *h_pinned = nullptr;  // staging for host vectors
+    int64_t h_pinned_n = 0;
+};
+
+namespace sb {
+
+enum KV { KX = 0, KR, KZ, KP, KAP, KRBAR, KPT, KAPT, KS, KST, KAST, KB };
+
+template <typename T> static T *dalloc(sb_ctx c, int64_t count, bool track = true) {
+    void *p = nullptr;
+    const size_t bytes = sizeof(T) * static_cast<size_t>(std::max<int64_t>(count, 1));
+    CK(cudaMalloc(&p, bytes));
+    CK(cudaMemset(p, 0, bytes));
+    c->allocs.push_back(p);
+    if (track) c->bytes += static_cast<int64_t>(bytes);
+    return static_cast<T *>(p);
+}
+
+static int vec_grid(int64_t n) {
+    const int64_t b = (n + kVecThreads - 1) / kVecThreads;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 8)));
+}
+
+static Red make_red(sb_ctx c, int op, int nval, const double *w0 = nullptr, const double *w1 = nullptr,
+                    CondSet cs = {{0, 0}, 0}) {
+    Red r;
+    r.partials = c->partials;
+    r.counter = c->counter;
+    r.st = c->st;
+    r.op = op;
+    r.nval = nval;
+    r.w0 = w0;
+    r.w1 = w1;
+    r.cs = cs;
+    return r;
+}
+
+static CondSet conds(std::initializer_list<cudaGraphConditionalHandle> hs) {
+    CondSet cs{{0, 0}, 0};
+    for (auto h : hs) cs.h[cs.n++] = static_cast<unsigned long long>(h);
+    return cs;
+}
+
+// ---- launchers ---------------------------------------------------------------
+
+template <int MODE, int NV>
+static void launch_csr(const DevLevel &l, cudaStream_t s, const double *x, const double *f, double *out,
+                       double omega, const int *skip, const Red &red) {
+    if (l.n == 0) return;
+    k_csr_tile<MODE, NV><<<l.ntiles, kTileRows, l.smem, s>>>(l.rp, l.ci, l.v, l.tiles, x, f, out, omega,
+                                                           l.cap, skip, red);
+    CK(cudaGetLastError());
+}
+
+static void launch_jacobi(const DevLevel &l, cudaStream_t s, const double *xin, const double *f, double *xout,
+                          double omega) {
+    launch_csr<M_JACOBI, 0>(l, s, xin, f, xout, omega, nullptr, Red{});
+}
+
+static void emit_coarse(sb_ctx c, cudaStream_t s, const double *f, double *x) {
+    const int n = static_cast<int>(c->nc);
+    k_coarse_gemv<<<(n + 7) / 8, 256, 0, s>>>(n, c->inv, f, x);
+    CK(cudaGetLastError());
+}
+
+// One V-cycle at level k (cycle.hpp:53-75), result written to X. T is the
+// level's ping-pong partner; the buffer plan makes the last post-sweep land
+// in X without copies.
+static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const double *f, double *X,
+                        bool zero) {
+    const int L = static_cast<int>(c->L.size());
+    if (k + 1 == L) {
+        emit_coarse(c, s, f, X);
+        return;
+    }
+    const DevLevel &l = c->L[static_cast<size_t>(k)];
+    double *T = l.t;
+    double *cur = X, *other = T;
+    if (zero) {
+        if (cp.pre >= 1) {
+            cur = ((cp.pre - 1) % 2 == 0) ? X : T;
+            other = (cur == X) ? T : X;
+            k_jacobi_zero<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, f, l.diag, cur, cp.omega);
+            CK(cudaGetLastError());
+            for (int i = 1; i < cp.pre; ++i) {
+                launch_jacobi(l, s, cur, f, other, cp.omega);
+                std::swap(cur, other);
+            }
+        } else {
+            CK(cudaMemsetAsync(X, 0, sizeof(double) * static_cast<size_t>(l.n), s));
+        }
+    } else {
+        for (int i = 0; i < cp.pre; ++i) {
+            launch_jacobi(l, s, cur, f, other, cp.omega);
+            std::swap(cur, other);
+        }
+    }
+    const DevLevel &lc = c->L[static_cast<size_t>(k) + 1];
+    launch_csr<M_RESID, 0>(l, s, cur, f, c->rs, 0.0, nullptr, Red{});
+    k_restrict<<<vec_grid(lc.n), kVecThreads, 0, s>>>(lc.n, l.mem, c->rs, lc.f);
+    CK(cudaGetLastError());
+    emit_vcycle(c, s, cp, k + 1, lc.f, lc.x, true);
+    double *pout = (cp.post % 2 == 0) ? X : T;
+    k_prolong<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, l.agg, cur, lc.x, pout);
+    CK(cudaGetLastError());
+    cur = pout;
+    other = (pout == X) ? T : X;
+    for (int i = 0; i < cp.post; ++i) {
+        launch_jacobi(l, s, cur, f, other, cp.omega);
+        std::swap(cur, other);
+    }
+}
+
+// ---- graph construction helpers -------------------------------------------------
+
+static cudaGraphConditionalHandle new_handle(cudaStream_t s) {
+    cudaStreamCaptureStatus status;
+    cudaGraph_t g;
+    CK(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+    return h;
+}
+
+static void add_cond(sb_ctx c, cudaStream_t s, int depth, cudaGraphConditionalHandle h,
+                     cudaGraphConditionalNodeType type,
+                     const std::function<void(cudaStream_t, int)> &body) {
+    cudaStreamCaptureStatus status;
+    cudaGraph_t g;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams p{};
+
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = type;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, deps, nd, &p));
+    CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    cudaStream_t s2 = c->cap[depth];
+    CK(cudaStreamBeginCaptureToGraph(s2, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeRelaxed));
+    body(s2, depth + 1);
+    cudaGraph_t out;
+    CK(cudaStreamEndCapture(s2, &out));
+}
+
+static cudaGraph_t begin_capture(sb_ctx c) {
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    CK(cudaStreamBeginCaptureToGraph(c->stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    return g;
+}
+
+static cudaGraph_t end_capture(sb_ctx c, cudaGraph_t g) {
+    cudaGraph_t out;
+    CK(cudaStreamEndCapture(c->stream, &out));
+    return g;
+}
+
+// PCG (krylov.hpp:65-119) as one graph: prologue IF (not converged at r0)
+// { z = M r; p = z, rz; WHILE (!done) { Ap, pAp -> alpha; x, r, ||r|| ->
+// tests; IF (!done) { z = M r; rz -> beta; p = z + beta p } } }; then the true
+// residual. cp == nullptr: identity preconditioner (z = r).
+static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x) {
+    const DevLevel &l0 = c->L[0];
+    const int64_t n = l0.n;
+    const int vb = vec_grid(n);
+    double *r = c->kv[KR], *z = c->kv[KZ], *p = c->kv[KP], *Ap = c->kv[KAP];
+    cudaStream_t s = c->stream;
+    auto precond = [c, cp, n](cudaStream_t ss, const double *in, double *out) {
+        if (cp) emit_vcycle(c, ss, *cp, 0, in, out, true);
+        else CK(cudaMemcpyAsync(out, in, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToDevice, ss));
+    };
+    cudaGraph_t g = begin_capture(c);
+    cudaGraphConditionalHandle h_pro = new_handle(s);
+    k_init<<<vb, kVecThreads, 0, s>>>(n, b, x, r, make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_pro})));
+    CK(cudaGetLastError());
+    add_cond(c, s, 0, h_pro, cudaGraphCondTypeIf, [&](cudaStream_t s1, int d1) {
+        precond(s1, r, z);
+        cudaGraphConditionalHandle h_loop = new_handle(s1);
+        k_copy_dot<<<vb, kVecThreads, 0, s1>>>(n, z, p, nullptr, r,
+                                              make_red(c, EP_PCG_RZ0, 1, nullptr, nullptr, conds({h_loop})));
+        CK(cudaGetLastError());
+        add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
+            launch_csr<M_SPMV, 1>(l0, s2, p, nullptr, Ap, 0.0, &c->st->done, make_red(c, EP_PCG_PAP, 1, p));
+            cudaGraphConditionalHandle h_vc = new_handle(s2);
+            k_pcg_update<<<vb, kVecThreads, 0, s2>>>(
+                n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})));
+            CK(cudaGetLastError());
+            add_cond(c, s2, d2, h_vc, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
+                precond(s3, r, z);
+                k_dot<<<vb, kVecThreads, 0, s3>>>(n, r, z, nullptr, make_red(c, EP_PCG_RZ, 1));
+                CK(cudaGetLastError());
+                k_xpay<<<vb, kVecThreads, 0, s3>>>(n, z, p, c->st);
+                CK(cudaGetLastError());
+            });
+        });
+    });
+    // true residual ||b - A x|| (krylov.hpp:116)
+    launch_csr<M_RESID, 1>(l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
+    return end_capture(c, g);
+}
+
+// Flexible PBiCGStab (krylov.hpp:126-211).
+static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *x) {
+    const DevLevel &l0 = c->L[0];
+    const int64_t n = l0.n;
+    const int vb = vec_grid(n);
+    double *r = c->kv[KR], *rbar = c->kv[KRBAR], *p = c->kv[KP], *pt = c->kv[KPT], *Apt = c->kv[KAPT],
+           *sv = c->kv[KS], *stv = c->kv[KST], *Ast = c->kv[KAST];
+    cudaStream_t s = c->stream;
+    auto precond = [c, cp, n](cudaStream_t ss, const double *in, double *out) {
+        if (cp) emit_vcycle(c, ss, *cp, 0, in, out, true);
+        else CK(cudaMemcpyAsync(out, in, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToDevice, ss));
+    };
+    cudaGraph_t g = begin_capture(c);
+    cudaGraphConditionalHandle h_pro = new_handle(s);
+    k_init<<<vb, kVecThreads, 0, s>>>(n, b, x, r, make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_pro})));
+    CK(cudaGetLastError());
+    add_cond(c, s, 0, h_pro, cudaGraphCondTypeIf, [&](cudaStream_t s1, int d1) {
+        cudaGraphConditionalHandle h_loop = new_handle(s1);
+        k_copy_dot<<<vb, kVecThreads, 0, s1>>>(n, r, rbar, p, r,
+                                              make_red(c, EP_BI_RHO0, 1, nullptr, nullptr, conds({h_loop})));
+        CK(cudaGetLastError());
+        add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
+            // (the loop is only entered / re-entered with done == 0)
+            precond(s2, p, pt);
+            launch_csr<M_SPMV, 1>(l0, s2, pt, nullptr, Apt, 0.0, nullptr, make_red(c, EP_BI_DENOM, 1, rbar));
+            cudaGraphConditionalHandle h_v2 = new_handle(s2);
+            k_bi_s<<<vb, kVecThreads, 0, s2>>>(n, r, Apt, sv,
+                                              make_red(c, EP_BI_SN, 1, nullptr, nullptr, conds({h_v2})));
+            CK(cudaGetLastError());
+            k_bi_half<<<vb, kVecThreads, 0, s2>>>(n, x, pt, c->st);
+            CK(cudaGetLastError());
+            add_cond(c, s2, d2, h_v2, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
+                precond(s3, sv, stv);
+                launch_csr<M_SPMV, 2>(l0, s3, stv, nullptr, Ast, 0.0, nullptr,
+                                      make_red(c, EP_BI_AS, 2, nullptr, sv));
+                k_bi_update<<<vb, kVecThreads, 0, s3>>>(n, x, r, pt, stv, sv, Ast, rbar,
+                                                       make_red(c, EP_BI_RN_RHO, 2));
+                CK(cudaGetLastError());
+                k_bi_p<<<vb, kVecThreads, 0, s3>>>(n, r, p, Apt, c->st);
+                CK(cudaGetLastError());
+            });
+            k_set_cond<<<1, 1, 0, s2>>>(c->st, conds({h_loop}));
+            CK(cudaGetLastError());
+        });
+    });
+    launch_csr<M_RESID, 1>(l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
+    return end_capture(c, g);
+}
+
+// Stationary AMG (cycle.hpp:91-130): WHILE (!done) { V-cycle(b, x); ||b - A x|| }.
+static cudaGraph_t build_amg(sb_ctx c, const Cyc &cp, const double *b, double *x) {
+    const DevLevel &l0 = c->L[0];
+    const int64_t n = l0.n;
+    const int vb = vec_grid(n);
+    cudaStream_t s = c->stream;
+    cudaGraph_t g = begin_capture(c);
+    cudaGraphConditionalHandle h_loop = new_handle(s);
+    k_init<<<vb, kVecThreads, 0, s>>>(n, b, x, nullptr,
+                                      make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_loop})));
+    CK(cudaGetLastError());
+    add_cond(c, s, 0, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s1, int) {
+        emit_vcycle(c, s1, cp, 0, b, x, false);
+        launch_csr<M_RESID, 1>(l0, s1, x, b, c->rs, 0.0, nullptr,
+                               make_red(c, EP_AMG_RN, 1, nullptr, nullptr, conds({h_loop})));
+    });
+    return end_capture(c, g);
+}
+
+// ---- context creation ----------------------------------------------------------
+
+static void make_tiles(const HostCsr &A, std::vector<int32_t> &tiles, int &cap) {
+    constexpr int64_t kCapMax = 8192;  // staged nnz per tile (96 KB of smem)
+    tiles.assign(1, 0);
+    cap = 0;
+    int64_t r = 0;
+    while (r < A.n) {
+        int64_t r1 = r, nz = 0;
+        while (r1 < A.n && r1 - r < kTileRows) {
+            const int64_t len = A.rp[r1 + 1] - A.rp[r1];
+            if (r1 > r && nz + len > kCapMax) break;
+            nz += len;
+            ++r1;
+        }
+        tiles.push_back(static_cast<int32_t>(r1));
+        if (nz <= kCapMax) cap = std::max(cap, static_cast<int>(nz));
+        r = r1;
+    }
+}
+
+static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarsest, int64_t n0) {
+    const HostCsr &A = H.A;
+    if (A.nnz() > INT32_MAX - 16 || A.n > INT32_MAX - 1)
+        throw invalid_argument("sb_create: level too large for int32 device offsets");
+    D.n = A.n;
+    D.nnz = A.nnz();
+    std::vector<int32_t> rp32(static_cast<size_t>(A.n) + 1);
+    for (int64_t i = 0; i <= A.n; ++i) rp32[i] = static_cast<int32_t>(A.rp[i]);
+    D.rp = dalloc<int32_t>(c, A.n + 1);
+    D.ci = dalloc<int32_t>(c, A.nnz() + 8);
+    D.v = dalloc<double>(c, A.nnz() + 2);
+    CK(cudaMemcpy(D.rp, rp32.data(), sizeof(int32_t) * rp32.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(D.ci, A.ci.data(), sizeof(int32_t) * A.ci.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(D.v, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice));
+    // diagonal + first bad row (smoother.hpp:55-70)
+    std::vector<double> diag(static_cast<size_t>(A.n), 0.0);
+    D.bad_diag = -1;
+    for (int64_t i = 0; i < A.n; ++i) {
+        const auto *b = A.ci.data() + A.rp[i], *e = A.ci.data() + A.rp[i + 1];
+        const auto *it = std::lower_bound(b, e, static_cast<int32_t>(i));
+        if (it == e || *it != i || A.v[static_cast<size_t>(it - A.ci.data())] == 0.0) {
+            if (D.bad_diag < 0) D.bad_diag = i;
+        } else {
+            diag[i] = A.v[static_cast<size_t>(it - A.ci.data())];
+        }
+    }
+    D.diag = dalloc<double>(c, A.n);
+    CK(cudaMemcpy(D.diag, diag.data(), sizeof(double) * diag.size(), cudaMemcpyHostToDevice));
+    std::vector<int32_t> tiles;
+    make_tiles(A, tiles, D.cap);
+    D.ntiles = static_cast<int>(tiles.size()) - 1;
+    D.tiles = dalloc<int32_t>(c, static_cast<int64_t>(tiles.size()));
+    CK(cudaMemcpy(D.tiles, tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice));
+    const size_t cap_v = static_cast<size_t>((D.cap + 3) & ~1);
+    const size_t cap_c = static_cast<size_t>((D.cap + 11) & ~3);
+    D.smem = cap_v * 8 + cap_c * 4;
+    if (!coarsest) {
+        D.nc = H.n_coarse;
+        D.agg = dalloc<int32_t>(c, A.n);
+        CK(cudaMemcpy(D.agg, H.agg.data(), sizeof(int32_t) * H.agg.size(), cudaMemcpyHostToDevice));
+        std::vector<int2> mem(static_cast<size_t>(D.nc), make_int2(-1, -1));
+        for (int64_t i = 0; i < A.n; ++i) {
+            int2 &m = mem[static_cast<size_t>(H.agg[i])];
+            if (m.x < 0) m.x = static_cast<int>(i);
+            else m.y = static_cast<int>(i);
+        }
+        D.mem = dalloc<int2>(c, D.nc);
+        CK(cudaMemcpy(D.mem, mem.data(), sizeof(int2) * mem.size(), cudaMemcpyHostToDevice));
+    }
+    D.t = dalloc<double>(c, A.n);
+    if (A.n != n0 || &D != &c->L[0]) {  // level 0 uses the caller's / Krylov vectors
+        D.x = dalloc<double>(c, A.n);
+        D.f = dalloc<double>(c, A.n);
+    }
+}
+
+template <int MODE, int NV> static void set_smem_attr(size_t smem) {
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+}
+
+static Cyc check_cycle(sb_ctx c, const sb_cycle *cp, const char *who) {
+    Cyc y;
+    if (!cp) return y;
+    if (cp->smoother != SB_SMOOTHER_JACOBI)
+        throw invalid_argument(std::string(who) +
+                               ": only the weighted Jacobi smoother runs on the device (Gauss-Seidel "
+                               "is inherently sequential and is not emulated)");
+    if (!(cp->omega > 0.0) || cp->omega > 1.0)
+        throw invalid_argument("SmootherKind: Jacobi weight " + std::to_string(cp->omega) +
+                               " outside (0, 1]");
+    if (cp->pre_sweeps < 0 || cp->post_sweeps < 0)
+        throw invalid_argument("smooth: negative sweep count");
+    y.pre = cp->pre_sweeps;
+    y.post = cp->post_sweeps;
+    y.omega = cp->omega;
+    if (y.pre + y.post > 0)
+        for (size_t k = 0; k + 1 < c->L.size(); ++k)
+            if (c->L[k].bad_diag >= 0)
+                throw invalid_argument("smooth: zero diagonal entry in row " +
+                                       std::to_string(c->L[k].bad_diag));
+    if (c->nc <= 0) throw invalid_argument(std::string(who) + ": hierarchy has no coarse factorization");
+    return y;
+}
+
+static std::string key_of(const char *kind, const Cyc *cp, const void *b, const void *x, const void *h) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "%s|%d|%d|%.17g|%p|%p|%p", kind, cp ? cp->pre : -1, cp ? cp->post : -1,
+                  cp ? cp->omega : 0.0, b, x, h);
+    return buf;
+}
+
+} // namespace sb
+
+// ===========================================================================
+// C ABI: context, solves, single kernels
+// ===========================================================================
+using namespace sb;
+
+namespace sb {
+
+static void destroy_graphs(sb_ctx c) {
+    for (auto &kv : c->cache) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.g) cudaGraphDestroy(kv.second.g);
+    }
+    c->cache.clear();
+}
+
+static void ensure_hist(sb_ctx c, int need) {
+    if (need <= c->hist_cap) return;
+    destroy_graphs(c);  // graphs embed the history pointers
+    const int cap = std::max(need, 1024);
+    if (c->hist_r) cudaFree(c->hist_r);
+    if (c->hist_t) cudaFree(c->hist_t);
+    CK(cudaMalloc(&c->hist_r, sizeof(double) * cap));
+    CK(cudaMalloc(&c->hist_t, sizeof(double) * cap));
+    c->hist_cap = cap;
+}
+
+enum SolveKind { K_PCG = 0, K_BICG = 1, K_AMG = 2 };
+
+// Runs the cached whole-solve graph (one launch, device-side loop control)
+// and fills the report. host == true: b and x are host arrays and the H2D/D2H
+// copies are part of the solve (the reference's wall_time covers its whole
+// call, krylov.hpp:68,117).
+static int run_solve(sb_ctx c, SolveKind kind, const sb_cycle *cpa, const double *b, double *x,
+                     double tol, int max_iters, sb_report *rep, bool host, const char *who) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!(tol > 0.0)) throw invalid_argument(std::string(who) + ": tol must be > 0");
+    Cyc cyc;
+    const Cyc *cp = nullptr;
+    if (cpa) {
+        cyc = check_cycle(c, cpa, who);
+        cp = &cyc;
+    }
+    if (kind == K_AMG && !cp) throw invalid_argument("amg_solve: cycle parameters required");
+    CK(cudaSetDevice(c->device));
+    const int64_t n = c->L[0].n;
+    ensure_hist(c, std::max(max_iters, 0) + 2);
+    const double *db = b;
+    double *dx = x;
+    if (host) {
+        db = c->kv[KB];
+        dx = c->kv[KX];
+        CK(cudaMemcpyAsync(c->kv[KB], b, sizeof(double) * static_cast<size_t>(n), cudaMemcpyHostToDevice,
+                           c->stream));
+    }
+    DevState hs;
+    std::memset(&hs, 0, sizeof(hs));
+    hs.tol = tol;
+    hs.max_iters = max_iters;
+    hs.hist_cap = c->hist_cap;
+    hs.hist_r = c->hist_r;
+    hs.hist_t = c->hist_t;
+    CK(cudaMemcpyAsync(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+    const char *kname = kind == K_PCG ? "pcg" : kind == K_BICG ? "bicg" : "amg";
+    const std::string key = key_of(kname, cp, db, dx, c->hist_r);
+    auto it = c->cache.find(key);
+    if (it == c->cache.end()) {
+        GraphEntry e;
+        if (kind == K_PCG) e.g = build_pcg(c, cp, db, dx);
+        else if (kind == K_BICG) e.g = build_bicg(c, cp, db, dx);
+        else e.g = build_amg(c, *cp, db, dx);
+        CK(cudaGraphInstantiate(&e.exec, e.g, 0));
+        it = c->cache.emplace(key, e).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, c->stream));
+    CK(cudaMemcpyAsync(&hs, c->st, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));
+    if (host)
+        CK(cudaMemcpyAsync(x, dx, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const int hist_len = hs.iter + 1;
+    if (rep) {
+        rep->iterations = hs.iter;
+        rep->termination = hs.term;
+        rep->true_residual = hs.true_res;
+        rep->hist_len = hist_len;
+        const int m = std::min(hist_len, std::max(rep->hist_cap, 0));
+        if (m > 0 && rep->residual_history)
+            CK(cudaMemcpy(rep->residual_history, c->hist_r, sizeof(double) * m, cudaMemcpyDeviceToHost));
+        if (m > 0 && rep->time_history)
+            CK(cudaMemcpy(rep->time_history, c->hist_t, sizeof(double) * m, cudaMemcpyDeviceToHost));
+        rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    if (kind == K_AMG && hs.status == 2) {
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "amg_solve: diverged (residual %f exceeds 1e6 x initial %f)", hs.rn,
+                      hs.r0);
+        throw runtime_error(buf);
+    }
+    return SB_OK;
+}
+
+static const DevLevel &level_of(sb_ctx c, int k) {
+    if (!c) throw invalid_argument("null context");
+    if (k < 0 || k >= static_cast<int>(c->L.size())) throw invalid_argument("level out of range");
+    return c->L[static_cast<size_t>(k)];
+}
+
+// Host-vector helper for the single-kernel entry points: copies in, runs fn
+// on device buffers (scratch vectors of the context), copies out.
+static void with_dev(sb_ctx c, const std::function<void(cudaStream_t)> &fn) {
+    CK(cudaSetDevice(c->device));
+    fn(c->stream);
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+static void h2d(sb_ctx c, double *d, const double *h, int64_t n) {
+    CK(cudaMemcpyAsync(d, h, sizeof(double) * static_cast<size_t>(n), cudaMemcpyHostToDevice, c->stream));
+}
+static void d2h(sb_ctx c, double *h, const double *d, int64_t n) {
+    CK(cudaMemcpyAsync(h, d, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, c->stream));
+}
+
+} // namespace sb
+
+extern "C" {
+
+const char *sb_last_error(void) { return sb::g_err.c_str(); }
+const char *sb_version(void) { return "sparsh_b200 0.1 (sm_100a)"; }
+
+int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
+    sb_ctx c = nullptr;
+    int rc = guard([&] {
+        Hier *h = hier_of(hh);
+        if (!h || !out) throw invalid_argument("sb_create: null argument");
+        sb_device_opts o{0, 1, -1};
+        if (opts) o = *opts;
+        if (o.host_levels_from >= 0)
+            throw invalid_argument("sb_create: hybrid host-level placement is not available in this build");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (o.device < 0 || o.device >= ndev) throw invalid_argument("sb_create: no such CUDA device");
+        CK(cudaSetDevice(o.device));
+        c = new sb_ctx_s;
+        c->device = o.device;
+        c->graphs = o.use_graphs != 0;
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        for (auto &s : c->cap) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        const int64_t n0 = h->levels[0].A.n;
+        c->L.resize(h->levels.size());
+        size_t max_smem = 0;
+        for (size_t k = 0; k < h->levels.size(); ++k) {
+            upload_level(c, h->levels[k], c->L[k], k + 1 == h->levels.size(), n0);
+            max_smem = std::max(max_smem, c->L[k].smem);
+        }
+        if (max_smem > 200 * 1024) throw invalid_argument("sb_create: tile staging exceeds shared memory");
+        set_smem_attr<M_SPMV, 0>(max_smem);
+        set_smem_attr<M_SPMV, 1>(max_smem);
+        set_smem_attr<M_SPMV, 2>(max_smem);
+        set_smem_attr<M_RESID, 0>(max_smem);
+        set_smem_attr<M_RESID, 1>(max_smem);
+        set_smem_attr<M_JACOBI, 0>(max_smem);
+        c->nc = h->nc;
+        if (h->nc > 0) {
+            c->inv = dalloc<double>(c, h->nc * h->nc);
+            CK(cudaMemcpy(c->inv, h->inv.data(), sizeof(double) * h->inv.size(), cudaMemcpyHostToDevice));
+        }
+        c->rs = dalloc<double>(c, n0);
+        for (auto &v : c->kv) v = dalloc<double>(c, n0);
+        int maxb = 148 * 8;
+        for (auto &l : c->L) maxb = std::max(maxb, l.ntiles);
+        c->partials = dalloc<double>(c, 2 * static_cast<int64_t>(maxb) + 2, false);
+        c->counter = dalloc<unsigned>(c, 4, false);
+        c->st = dalloc<DevState>(c, 1, false);
+        CK(cudaDeviceSynchronize());
+        *out = c;
+    });
+    if (rc != SB_OK && c) sb_destroy(c);
+    return rc;
+}
+
+void sb_destroy(sb_ctx c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    destroy_graphs(c);
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->hist_r) cudaFree(c->hist_r);
+    if (c->hist_t) cudaFree(c->hist_t);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    for (auto &s : c->cap)
+        if (s) cudaStreamDestroy(s);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int64_t sb_device_bytes(sb_ctx c) { return c ? c->bytes : 0; }
+void *sb_stream(sb_ctx c) { return c ? static_cast<void *>(c->stream) : nullptr; }
+
+int sb_vcycle_dev(sb_ctx c, const sb_cycle *cp, int level, const double *d_f, double *d_x, int x_is_zero) {
+    return guard([&] {
+        level_of(c, level);
+        const Cyc y = check_cycle(c, cp, "vcycle");
+        CK(cudaSetDevice(c->device));
+        emit_vcycle(c, c->stream, y, level, d_f, d_x, x_is_zero != 0);
+    });
+}
+
+int sb_vcycle(sb_ctx c, const sb_cycle *cp, int level, const double *f, double *x) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, level);
+        const Cyc y = check_cycle(c, cp, "vcycle");
+        double *df = c->kv[KB], *dx = c->kv[KX];
+        with_dev(c, [&](cudaStream_t s) {
+            h2d(c, df, f, l.n);
+            h2d(c, dx, x, l.n);
+            emit_vcycle(c, s, y, level, df, dx, false);
+            d2h(c, x, dx, l.n);
+        });
+    });
+}
+
+int sb_pcg(sb_ctx c, const sb_cycle *cp, const double *b, double *x, double tol, int max_iters,
+           sb_report *rep) {
+    return guard([&] { run_solve(c, K_PCG, cp, b, x, tol, max_iters, rep, true, "pcg"); });
+}
+int sb_pbicgstab(sb_ctx c, const sb_cycle *cp, const double *b, double *x, double tol, int max_iters,
+                 sb_report *rep) {
+    return guard([&] { run_solve(c, K_BICG, cp, b, x, tol, max_iters, rep, true, "pbicgstab"); });
+}
+int sb_amg_solve(sb_ctx c, const sb_cycle *cp, const double *b, double *x, double tol, int max_cycles,
+                 sb_report *rep) {
+    return guard([&] { run_solve(c, K_AMG, cp, b, x, tol, max_cycles, rep, true, "amg_solve"); });
+}
+int sb_pcg_dev(sb_ctx c, const sb_cycle *cp, const double *d_b, double *d_x, double tol, int max_iters,
+               sb_report *rep) {
+    return guard([&] { run_solve(c, K_PCG, cp, d_b, d_x, tol, max_iters, rep, false, "pcg"); });
+}
+int sb_pbicgstab_dev(sb_ctx c, const sb_cycle *cp, const double *d_b, double *d_x, double tol, int max_iters,
+                     sb_report *rep) {
+    return guard([&] { run_solve(c, K_BICG, cp, d_b, d_x, tol, max_iters, rep, false, "pbicgstab"); });
+}
+
+int sb_spmv(sb_ctx c, int level, const double *x, double *y) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, level);
+        with_dev(c, [&](cudaStream_t s) {
+            h2d(c, c->kv[KP], x, l.n);
+            launch_csr<M_SPMV, 0>(l, s, c->kv[KP], nullptr, c->kv[KAP], 0.0, nullptr, Red{});
+            d2h(c, y, c->kv[KAP], l.n);
+        });
+    });
+}
+
+int sb_smooth(sb_ctx c, int level, const sb_cycle *cp, double *x, const double *f, int sweeps) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, level);
+        if (sweeps < 0) throw invalid_argument("smooth: negative sweep count");
+        if (!cp || cp->smoother != SB_SMOOTHER_JACOBI)
+            throw invalid_argument("smooth: only the weighted Jacobi smoother runs on the device");
+        if (!(cp->omega > 0.0) || cp->omega > 1.0)
+            throw invalid_argument("SmootherKind: Jacobi weight " + std::to_string(cp->omega) +
+                                   " outside (0, 1]");
+        if (sweeps == 0) return;
+        if (l.bad_diag >= 0)
+            throw invalid_argument("smooth: zero diagonal entry in row " + std::to_string(l.bad_diag));
+        with_dev(c, [&](cudaStream_t s) {
+            double *a = c->kv[KX], *b = c->kv[KZ], *df = c->kv[KB];
+            h2d(c, a, x, l.n);
+            h2d(c, df, f, l.n);
+            for (int i = 0; i < sweeps; ++i) {
+                launch_jacobi(l, s, a, df, b, cp->omega);
+                std::swap(a, b);
+            }
+            d2h(c, x, a, l.n);
+        });
+    });
+}
+
+int sb_residual(sb_ctx c, int level, const double *x, const double *f, double *r) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, level);
+        with_dev(c, [&](cudaStream_t s) {
+            h2d(c, c->kv[KX], x, l.n);
+            h2d(c, c->kv[KB], f, l.n);
+            launch_csr<M_RESID, 0>(l, s, c->kv[KX], c->kv[KB], c->kv[KR], 0.0, nullptr, Red{});
+            d2h(c, r, c->kv[KR], l.n);
+        });
+    });
+}
+
+int sb_restrict(sb_ctx c, int level, const double *r, double *fc) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, level);
+        if (l.nc < 0) throw invalid_argument("restrict: coarsest level has no aggregation");
+        with_dev(c, [&](cudaStream_t s) {
+            h2d(c, c->kv[KR], r, l.n);
+            k_restrict<<<vec_grid(l.nc), kVecThreads, 0, s>>>(l.nc, l.mem, c->kv[KR], c->kv[KZ]);
+            CK(cudaGetLastError());
+            d2h(c, fc, c->kv[KZ], l.nc);
+        });
+    });
+}
+
+int sb_prolong(sb_ctx c, int level, const double *xc, double *x) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, level);
+        if (l.nc < 0) throw invalid_argument("prolong: coarsest level has no aggregation");
+        with_dev(c, [&](cudaStream_t s) {
+            h2d(c, c->kv[KZ], xc, l.nc);
+            h2d(c, c->kv[KX], x, l.n);
+            k_prolong<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, l.agg, c->kv[KX], c->kv[KZ], c->kv[KX]);
+            CK(cudaGetLastError());
+            d2h(c, x, c->kv[KX], l.n);
+        });
+    });
+}
+
+int sb_coarse_solve(sb_ctx c, const double *f, double *x) {
+    return guard([&] {
+        if (!c || c->nc <= 0) throw invalid_argument("coarse_solve: no coarse factorization");
+        with_dev(c, [&](cudaStream_t s) {
+            h2d(c, c->kv[KB], f, c->nc);
+            emit_coarse(c, s, c->kv[KB], c->kv[KX]);
+            d2h(c, x, c->kv[KX], c->nc);
+        });
+    });
+}
+
+} // extern "C"

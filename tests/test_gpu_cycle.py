@@ -1,0 +1,81 @@
+"""V-cycle parity on the GPU (cycle.hpp:53-75): every level operation is
+bitwise the reference's except the coarsest solve (inverse GEMV), so one
+V-cycle agrees to ~1e-15; the contract is 1e-12 relative."""
+import numpy as np
+import pytest
+
+from helpers import random_spd, rel
+
+pytestmark = pytest.mark.gpu
+
+JAC = None
+
+
+def _cp(sp, pre=6, post=6, omega=2.0 / 3.0):
+    return sp.CycleParams(pre, post, sp.SmootherKind.weighted_jacobi(omega))
+
+
+@pytest.mark.parametrize("mk", [
+    lambda sp: sp.poisson3d(32), lambda sp: sp.aniso3d(24), lambda sp: sp.poisson2d(96, 80),
+    lambda sp: sp.convdiff3d(16, 16, 16, 1.0, 100.0, 1.0, 1.0), lambda sp: sp.poisson3d_27(12),
+    lambda sp: random_spd(sp, 300, 7, 0.05)])
+@pytest.mark.parametrize("sweeps", [(6, 6), (1, 2), (0, 3), (2, 0)])
+def test_vcycle_matches_oracle(sp, port, mk, sweeps):
+    A = mk(sp)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40, coarse_target=min(500, A.nrows() // 4)))
+    o = port.hierarchy(A, min(500, A.nrows() // 4), 40)
+    o.set_cycle(sweeps[0], sweeps[1], 2.0 / 3.0)
+    cp = _cp(sp, *sweeps)
+    f = sp.rhs_random(A.nrows(), 42)
+    got = sp.vcycle(h, 0, f, np.zeros(A.nrows()), cp)
+    assert rel(got, o.vcycle(f, np.zeros(A.nrows()))) < 1e-12
+    x0 = np.random.default_rng(1).uniform(-1, 1, A.nrows())  # general initial guess
+    assert rel(sp.vcycle(h, 0, f, x0, cp), o.vcycle(f, x0)) < 1e-12
+
+
+def test_vcycle_linear_symmetric_zero(sp):
+    # test_cycle.cpp:32-56, 188-199
+    h = sp.Hierarchy(sp.poisson2d(16, 16), sp.SolverConfig(coarse_target=60))
+    cp = _cp(sp)
+    rng = np.random.default_rng(83)
+    f, g = rng.uniform(-1, 1, 256), rng.uniform(-1, 1, 256)
+    Bf, Bg = sp.vcycle(h, 0, f, np.zeros(256), cp), sp.vcycle(h, 0, g, np.zeros(256), cp)
+    Bc = sp.vcycle(h, 0, 2 * f - 3 * g, np.zeros(256), cp)
+    assert np.max(np.abs(Bc - (2 * Bf - 3 * Bg))) <= 1e-10 * np.max(np.abs(Bc))
+    M = sp.make_amg_preconditioner(h, cp)
+    for _ in range(10):
+        u, v = rng.uniform(-1, 1, 256), rng.uniform(-1, 1, 256)
+        a, b = M.apply(u) @ v, u @ M.apply(v)
+        assert abs(a - b) <= 1e-9 * max(1.0, abs(a))
+    assert not sp.vcycle(h, 0, np.zeros(256), np.zeros(256), cp).any()
+    assert np.array_equal(M.apply(f), sp.vcycle(h, 0, f, np.zeros(256), cp))
+
+
+def test_residual_drops_every_cycle(sp):
+    # test_cycle.cpp:58-72 (Jacobi variant)
+    A = sp.poisson2d(64, 64)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40))
+    b = sp.rhs_ones(4096)
+    x = np.zeros(4096)
+    prev = np.linalg.norm(b)
+    for _ in range(5):
+        sp.vcycle_in_place(h, 0, b, x, _cp(sp))
+        rn = np.linalg.norm(sp.residual(A, x, b))
+        assert rn < prev
+        prev = rn
+
+
+def test_single_level_is_direct_solve(sp):
+    A = sp.CsrMatrix.from_dense([[4, -1, 0], [-1, 4, -1], [0, -1, 4]])
+    h = sp.Hierarchy(A, sp.SolverConfig(coarse_target=100))
+    assert h.nlevels() == 1
+    f = np.ones(3)
+    assert rel(sp.vcycle(h, 0, f, np.zeros(3), _cp(sp)), np.linalg.solve(A.to_dense(), f)) < 1e-14
+
+
+def test_vcycle_rejects(sp):
+    h = sp.Hierarchy(sp.poisson2d(16, 16), sp.SolverConfig(coarse_target=60))
+    with pytest.raises(sp.InvalidArgument):
+        sp.vcycle(h, 0, np.ones(255), np.zeros(256), _cp(sp))
+    with pytest.raises(sp.InvalidArgument, match="Jacobi"):
+        sp.vcycle(h, 0, np.ones(256), np.zeros(256), sp.CycleParams())  # GS default: rejected

@@ -1,0 +1,110 @@
+"""Single-kernel parity on the GPU through the C ABI: SpMV, residual, Jacobi
+sweeps, restriction and prolongation are bit-identical to the reference
+(thread-per-row CSR-order sums, no FMA); the coarse solve uses a precomputed
+inverse and matches to 1e-12 relative."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden_path
+from helpers import from_npz, random_sparse, random_spd, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _mats(sp):
+    long_row = np.zeros((40, 40))
+    np.fill_diagonal(long_row, 50.0)
+    long_row[3, :] = 1.0
+    long_row[3, 3] = 60.0
+    return [sp.poisson2d(33, 17), sp.poisson3d(20), sp.aniso3d(16), sp.poisson3d_27(9),
+            sp.convdiff3d(11, 12, 13, 1.0, 100.0, 1.0, 1.0), random_sparse(sp, 70, 3, 0.3, False),
+            random_spd(sp, 50, 4), sp.CsrMatrix.from_dense(long_row)]
+
+
+def test_spmv_residual_bitexact(sp, oracle_best):
+    for A in _mats(sp):
+        x = np.random.default_rng(1).uniform(-1, 1, A.ncols())
+        f = np.random.default_rng(2).uniform(-1, 1, A.nrows())
+        assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x))
+        assert np.array_equal(sp.residual(A, x, f), oracle_best.residual(A, x, f))
+
+
+def test_spmv_long_rows_unstaged_path(sp, oracle_best):
+    # a row with > 8192 entries exceeds the per-tile staging capacity
+    n = 9000
+    ent = [(i, i, 4.0) for i in range(n)] + [(7, j, 0.5 + (j % 3)) for j in range(n) if j != 7]
+    A = sp.CsrMatrix.from_triplets(n, n, ent)
+    x = np.random.default_rng(5).uniform(-1, 1, n)
+    assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x))
+
+
+@pytest.mark.parametrize("sweeps", [1, 2, 3, 6])
+def test_jacobi_bitexact(sp, oracle_best, sweeps):
+    jac = sp.SmootherKind.weighted_jacobi()
+    for A in _mats(sp):
+        x = np.random.default_rng(3).uniform(-1, 1, A.nrows())
+        f = np.random.default_rng(4).uniform(-1, 1, A.nrows())
+        got = sp.smooth(jac, A, x, f, sweeps)
+        assert np.array_equal(got, oracle_best.jacobi(A, 2.0 / 3.0, x, f, sweeps))
+
+
+def test_jacobi_hand_values(sp):
+    # test_smoother.cpp:33-51
+    D = sp.CsrMatrix.from_dense([[2, 0, 0], [0, 4, 0], [0, 0, 8]])
+    x = sp.smooth(sp.SmootherKind.weighted_jacobi(1.0), D, np.zeros(3), [2.0, 2.0, 2.0], 1)
+    assert x.tolist() == [1.0, 0.5, 0.25]
+    A = sp.CsrMatrix.from_dense([[2, 1], [1, 3]])
+    x = sp.smooth(sp.SmootherKind.weighted_jacobi(0.5), A, [1.0, -1.0], [3.0, 2.0], 1)
+    assert x[0] == 1.5 and x[1] == -1.0 + 2.0 / 3.0
+
+
+def test_jacobi_fixed_point_and_errors(sp):
+    # test_smoother.cpp:114-125: integer data, exact solution is a fixed point
+    A = sp.poisson2d(4, 4)
+    x = np.array([float(i % 5 - 2) for i in range(16)])
+    f = sp.spmv(A, x)
+    assert np.array_equal(sp.smooth(sp.SmootherKind.weighted_jacobi(), A, x, f, 4), x)
+    # test_smoother.cpp:170-186: zero / missing diagonal reported with the row
+    Z = sp.CsrMatrix.from_triplets(2, 2, [(0, 0, 1.0), (0, 1, 1.0), (1, 0, 1.0), (1, 1, 0.0)])
+    with pytest.raises(sp.InvalidArgument, match="row 1"):
+        sp.smooth(sp.SmootherKind.weighted_jacobi(), Z, np.zeros(2), [1.0, 1.0], 1)
+    with pytest.raises(sp.InvalidArgument, match="Jacobi"):
+        sp.smooth(sp.SmootherKind.gauss_seidel_forward(), A, np.zeros(16), np.ones(16), 1)
+    assert np.array_equal(sp.smooth(sp.SmootherKind.weighted_jacobi(), A, x, f, 0), x)
+
+
+def test_restrict_prolong_bitexact(sp):
+    # test_cycle.cpp:76-100: restriction == aggregate sums (ascending), prolongation scatters
+    A = sp.poisson3d(16)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40))
+    for k in range(h.nlevels() - 1):
+        lv = h.level(k)
+        r = np.random.default_rng(k).uniform(-1, 1, lv.A.nrows())
+        man = np.zeros(lv.agg.n_coarse)
+        for i, c in enumerate(lv.agg.fine_to_coarse):
+            man[c] += 1.0 * r[i]
+        assert np.array_equal(h.restrict(k, r), man)
+        xc = np.random.default_rng(100 + k).uniform(-1, 1, lv.agg.n_coarse)
+        x = np.random.default_rng(200 + k).uniform(-1, 1, lv.A.nrows())
+        want = x + (0.0 + xc[lv.agg.fine_to_coarse])
+        assert np.array_equal(h.prolong_add(k, xc, x), want)
+
+
+def test_coarse_solve(sp, oracle_best):
+    A = sp.poisson3d(24)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40))
+    o = oracle_best.hierarchy(A, 500, 40)
+    f = np.random.default_rng(9).uniform(-1, 1, h.coarsest().nrows())
+    assert rel(h.coarse_solve(f), o.coarse_solve(f)) < 1e-12
+
+
+@pytest.mark.parametrize("path", sorted(p for p in glob.glob(golden_path("*.npz"))
+                                        if not p.endswith("example_6x6.npz")))
+def test_golden_kernels(sp, path):
+    d = np.load(path)
+    A = from_npz(sp, d)
+    assert np.array_equal(sp.spmv(A, d["f"]), d["spmv_f"])
+    assert np.array_equal(sp.smooth(sp.SmootherKind.weighted_jacobi(), A, d["f"], d["b"], 3), d["jacobi3"])
