@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark: AMG-PCG solve of BASELINE.json configs[1] (C2: 3D 7-point Poisson
+128^3, 2.1M DOFs, Jacobi 6/6, node-HEM, coarse_target 500, max_levels 40,
+rhs = ones, tol = 1e-8 * ||b||) on N GPUs of one node. One "step" = one full
+PCG solve to tolerance.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload C2|C1|C3|C4]
+
+`value`  = device time of one solve (CUDA events on the solve stream, inputs
+           resident in HBM; L2 flushed before every step), max over ranks.
+`e2e`    = the same solve through the public C ABI with host (pinned) b and x:
+           H2D of b, solve, D2H of x inside the timed region.
+`roofline` = the L0 Jacobi sweep kernel (dominant: ~80% of solve bytes),
+           algorithmic bytes / CUDA-event duration vs MEASURED_PEAKS.json.
+`cpu_baseline` = the reference's own CPU code (oracle/_ref) on this host.
+N > 1: replicas (each rank solves its own C2; row partitioning is future work,
+see DESIGN.md §6) — `scaling: weak`.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AMG-PCG solve s to 1e-8 rel. residual; SpMV/V-cycle HBM GB/s vs peak, 1–8 GPU"
+
+WORKLOADS = {
+    "C2": dict(desc="C2: 3D 7-pt Poisson 128^3 (2.1M DOFs) AMG-PCG, full hierarchy device-resident",
+               solver="pcg", gen=lambda sp: sp.poisson3d(128)),
+    "C1": dict(desc="C1: 2D 5-pt Poisson 1024^2 (1M DOFs) AMG-PCG",
+               solver="pcg", gen=lambda sp: sp.poisson2d(1024, 1024)),
+    "C3": dict(desc="C3: 3D anisotropic (eps=1e-3 in z) 7-pt 256^3 (16.8M DOFs) AMG-PCG",
+               solver="pcg", gen=lambda sp: sp.aniso3d(256, 1e-3)),
+    "C4": dict(desc="C4: 3D convection-diffusion 256^3, b=(1,100,1), c=1 AMG-PBiCGStab",
+               solver="pbicgstab", gen=lambda sp: sp.convdiff3d(256, 256, 256, 1.0, 100.0, 1.0, 1.0)),
+}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(s[0]) for s in self.samples if num(s[0])]
+        busy = [num(s[0]) for s in self.samples if num(s[0]) and (num(s[6]) or 0) > 0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(num(s[1]) or 0 for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def bytes_model(h, pre=6, post=6):
+    """Algorithmic bytes: matrix once per pass (12 B/nnz + 4 B/row
+    offsets), each distinct vector once."""
+    lv = [(l.A.nrows(), l.A.nnz()) for l in h.levels()]
+    L = len(lv)
+
+    def jac(n, z):
+        return 12 * z + 4 * (n + 1) + 24 * n
+
+    vc = 0
+    for k in range(L - 1):
+        n, z = lv[k]
+        nc = lv[k + 1][0]
+        vc += (pre + post - 1) * jac(n, z) + 24 * n                # sweeps + zero-guess sweep
+        vc += 12 * z + 4 * (n + 1) + 16 * n + 4 * n + 8 * nc       # residual + restriction
+        vc += 16 * n + 4 * n + 8 * nc                              # prolongation
+    ncs = lv[-1][0]
+    vc += 8 * ncs * ncs + 16 * ncs
+    n0, z0 = lv[0]
+    spmv = 12 * z0 + 4 * (n0 + 1) + 16 * n0
+    pcg_it = vc + spmv + 40 * n0 + 16 * n0 + 24 * n0
+    return dict(vcycle=vc, pcg_iter=pcg_it, l0_jacobi=jac(n0, z0), l0_spmv=spmv)
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("jacobi_l0_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference's own CPU code (oracle/_ref: the unmodified
+    sparsh headers compiled by oracle/Makefile) on this host's cores."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    from paper_2007_00056_b200 import sparsh as sp  # generator only (same matrix as our arm)
+    try:
+        R = orc.Ref()
+        kind = "reference"
+    except Exception:
+        R = orc.Port()
+        kind = "port"
+    cores = os.cpu_count() or 1
+    if kind == "reference":
+        R.set_threads(cores)
+    A = WORKLOADS[wl]["gen"](sp)
+    b = sp.rhs_ones(A.nrows())
+    tol = 1e-8 * float(np.linalg.norm(b))
+    h = R.hierarchy(A, 500, 40)
+    solver = WORKLOADS[wl]["solver"]
+    k_full = REF_ITERS.get(wl)
+    m = args.ref_sample_iters
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        out = getattr(h, solver)(b, tol, m)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = statistics.median(times)
+    # full solve with k iterations ~ (k + 1) preconditioner applications; the
+    # m-iteration sample performs m + 1 (krylov.hpp:85,109) -> scale by (k+1)/(m+1)
+    scale = (k_full + 1) / (m + 1) if solver == "pcg" else k_full / m
+    value = t * scale
+    line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOADS[wl]["desc"], "n": A.nrows(), "nnz": A.nnz(),
+                       "tol": "1e-8*||b||", "rhs": "ones", "parallelism": "cpu-threads"},
+            "cpu_baseline": {"value": value, "unit": "s", "cores": cores if kind == "reference" else 1,
+                             "kind": kind,
+                             "sample": f"{solver} max_iters={m} on the full {wl} system per step "
+                                       f"(median {t:.3f} s), scaled x{scale:.2f} to the {k_full}-iteration "
+                                       f"solve"},
+            "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# iteration counts of the reference at these configs (re-checked by tests)
+REF_ITERS = {"C1": 60, "C2": 22, "C3": 43, "C4": 20}
+
+
+def cpu_baseline_sample(A, b, tol, wl, sample_iters):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    try:
+        R = orc.Ref()
+        kind = "reference"
+    except Exception:
+        R = orc.Port()
+        kind = "port"
+    cores = os.cpu_count() or 1
+    if kind == "reference":
+        R.set_threads(cores)
+    h = R.hierarchy(A, 500, 40)
+    solver = WORKLOADS[wl]["solver"]
+    t0 = time.perf_counter()
+    getattr(h, solver)(b, tol, sample_iters)
+    dt = time.perf_counter() - t0
+    k = REF_ITERS[wl]
+    scale = (k + 1) / (sample_iters + 1) if solver == "pcg" else k / sample_iters
+    return {"value": dt * scale, "unit": "s", "cores": cores if kind == "reference" else 1, "kind": kind,
+            "sample": f"{solver} max_iters={sample_iters} on the full {wl} system ({dt:.2f} s), "
+                      f"scaled x{scale:.2f} to the {k}-iteration solve"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--ref-sample-iters", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = args.workload
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from paper_2007_00056_b200 import sparsh as sp, _lib
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    L = _lib.lib()
+
+    A = WORKLOADS[wl]["gen"](sp)
+    n = A.nrows()
+    cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40, coarse_target=500)
+    t0 = time.perf_counter()
+    h = sp.Hierarchy(A, cfg, device=local)
+    ctx = h.ctx()
+    setup_s = time.perf_counter() - t0
+    cp = sp.CycleParams.from_config(cfg)._abi()
+    solver = WORKLOADS[wl]["solver"]
+    b_host = sp.rhs_ones(n)
+    tol = 1e-8 * float(np.linalg.norm(b_host))
+    max_iters = 1000
+
+    stream = torch.cuda.ExternalStream(L.sb_stream(ctx), device=torch.device("cuda", local))
+    b_dev = torch.ones(n, dtype=torch.float64, device=f"cuda:{local}")
+    x_dev = torch.zeros(n, dtype=torch.float64, device=f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    fn_dev = L.sb_pcg_dev if solver == "pcg" else L.sb_pbicgstab_dev
+    fn_host = L.sb_pcg if solver == "pcg" else L.sb_pbicgstab
+    torch.cuda.synchronize()
+
+    def solve_dev():
+        rep = _lib.sb_report()
+        _lib.check(fn_dev(ctx, C.byref(cp), C.c_void_p(b_dev.data_ptr()), C.c_void_p(x_dev.data_ptr()),
+                          tol, max_iters, C.byref(rep)))
+        return rep
+
+    # warm-up (also builds + instantiates the solve graph)
+    for _ in range(max(args.warmup, 3)):
+        rep = solve_dev()
+    iters = rep.iterations
+    assert rep.termination == 0, f"solve did not converge: termination {rep.termination}"
+
+    # ---- timed region: device-resident solves -------------------------------
+    per_step = []
+    with ClockSampler(local) as clk:
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush (256 MB > 126 MB L2), outside the event window
+            torch.cuda.synchronize()
+            rep = solve_dev()
+            per_step.append(L.sb_last_solve_ms(ctx))
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+    ms_local = statistics.mean(per_step)
+    ms = ms_local
+    if ws > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ms / 1e3
+
+    # ---- e2e: public C ABI with pinned host buffers ---------------------------
+    b_pin = torch.ones(n, dtype=torch.float64).pin_memory()
+    x_pin = torch.zeros(n, dtype=torch.float64).pin_memory()
+    bp = C.cast(C.c_void_p(b_pin.data_ptr()), C.POINTER(C.c_double))
+    xp = C.cast(C.c_void_p(x_pin.data_ptr()), C.POINTER(C.c_double))
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        rep2 = _lib.sb_report()
+        t1 = time.perf_counter()
+        _lib.check(fn_host(ctx, C.byref(cp), bp, xp, tol, max_iters, C.byref(rep2)))
+        dt = time.perf_counter() - t1
+        if i >= args.warmup:
+            e2e.append(dt)
+    e2e_s = statistics.mean(e2e)
+    if ws > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    x_np = x_pin.numpy()
+    true_rel = float(np.linalg.norm(sp.residual(A, x_np, b_host)) / np.linalg.norm(b_host)) if rank == 0 else None
+
+    # ---- roofline: L0 Jacobi sweep, CUDA events on the solve stream ----------------
+    bm = bytes_model(h, cfg.pre_sweeps, cfg.post_sweeps)
+    avg = C.c_double()
+    cnt = C.c_int()
+    _lib.check(L.sb_time_kernel(ctx, 0, 0, C.byref(cp), 20, C.byref(avg), C.byref(cnt)))
+    jac_ms = avg.value
+    vc_ms = C.c_double()
+    _lib.check(L.sb_time_kernel(ctx, 3, 0, C.byref(cp), 5, C.byref(vc_ms), C.byref(cnt)))
+    vc_launches = cnt.value
+    spmv_ms = C.c_double()
+    _lib.check(L.sb_time_kernel(ctx, 1, 0, C.byref(cp), 20, C.byref(spmv_ms), C.byref(cnt)))
+    peak, peak_kind = peaks()
+    achieved = bm["l0_jacobi"] / (jac_ms * 1e-3) / 1e9
+    vcycle_gbs = bm["vcycle"] / (vc_ms.value * 1e-3) / 1e9
+    solve_gbs = (bm["pcg_iter"] * iters) / value / 1e9
+
+    # kernels per solve: init + [V-cycle + rz/p] + iters x (SpMV+dot, update) + (iters-1) x
+    # (V-cycle, rz, xpay) + true residual
+    launches = 1 + (vc_launches + 1) + iters * 2 + (iters - 1) * (vc_launches + 2) + 1
+    if solver != "pcg":
+        launches = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[wl]["desc"], "n": n, "nnz": A.nnz(), "levels": h.nlevels(),
+                       "iterations": iters, "rhs": "ones", "tol": "1e-8*||b|| (absolute, as the reference)",
+                       "smoother": "weighted Jacobi 2/3, 6 pre / 6 post", "coarsening": "node-HEM",
+                       "coarse_target": 500, "max_levels": 40,
+                       "l2": "hierarchy (%.0f MB) > 126 MB L2 and L2 flushed (256 MB write) before every step"
+                             % (h.device_bytes() / 1e6),
+                       "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
+                       "setup_s": round(setup_s, 3), "true_rel_residual": true_rel},
+            "roofline": {"bound": "hbm", "kernel": "k_csr_tile<JACOBI> (L0 Jacobi sweep)",
+                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": load_traffic(),
+                         "algorithmic_bytes_per_launch": bm["l0_jacobi"], "launch_ms": jac_ms,
+                         "l0_spmv_gbs": (bm["l0_spmv"] / (spmv_ms.value * 1e-3) / 1e9),
+                         "vcycle_gbs": vcycle_gbs, "vcycle_ms": vc_ms.value,
+                         "solve_gbs": solve_gbs, "solve_frac": solve_gbs / peak},
+            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": launches * args.steps if launches else None,
+        }
+        if not args.no_cpu_baseline and ws == 1:
+            try:
+                line["cpu_baseline"] = cpu_baseline_sample(A, b_host, tol, wl, args.ref_sample_iters)
+            except Exception as e:  # never silently: record why
+                line["cpu_baseline"] = {"value": None, "error": str(e)}
+        line["clocks"] = clk.summary()
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

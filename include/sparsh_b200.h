@@ -101,6 +101,9 @@ typedef struct {
     int use_graphs;      /* 1: whole-solve CUDA graph with device-side loop control (default) */
     int64_t host_levels_from; /* hybrid mode: levels >= this index stay on the host
                                  (paper's MI scheme); -1 = all levels device-resident */
+    int coarse_exact;    /* 0: coarsest solve = GEMV with the precomputed inverse (fast);
+                            1: the reference's permuted forward/backward substitution in
+                               its exact operation order (bit-identical, slow; parity mode) */
 } sb_device_opts;
 
 typedef struct sb_hier_s *sb_hier;
@@ -170,6 +173,19 @@ int sb_pcg_dev(sb_ctx ctx, const sb_cycle *cp, const double *d_b, double *d_x, d
                int max_iters, sb_report *rep);
 int sb_pbicgstab_dev(sb_ctx ctx, const sb_cycle *cp, const double *d_b, double *d_x,
                      double tol, int max_iters, sb_report *rep);
+
+/* ---- measurement --------------------------------------------------------- */
+
+/* CUDA-event time (ms) of the last whole-solve graph launch on sb_stream. */
+double sb_last_solve_ms(sb_ctx ctx);
+/* Times `reps` back-to-back launches of one kernel on level `level` with CUDA
+ * events on sb_stream; *avg_ms = mean per launch. kind: 0 Jacobi sweep,
+ * 1 SpMV, 2 residual, 3 one V-cycle from x = 0 (cp required for 0 and 3).
+ * *launches = kernels launched per repetition. */
+int sb_time_kernel(sb_ctx ctx, int kind, int level, const sb_cycle *cp, int reps, double *avg_ms,
+                   int *launches);
+/* Kernels launched by one V-cycle from level 0 (graph node count). */
+int sb_vcycle_launches(sb_ctx ctx, const sb_cycle *cp);
 
 /* ---- single kernels on a level (unit parity; host vectors) --------------- */
 

@@ -66,6 +66,7 @@ class sb_device_opts(C.Structure):
         ("device", C.c_int),
         ("use_graphs", C.c_int),
         ("host_levels_from", C.c_int64),
+        ("coarse_exact", C.c_int),
     ]
 
 
@@ -77,7 +78,7 @@ EXPORTS = [
     "sb_pcg", "sb_pbicgstab", "sb_amg_solve", "sb_pcg_dev", "sb_pbicgstab_dev", "sb_spmv",
     "sb_smooth", "sb_residual", "sb_restrict", "sb_prolong", "sb_coarse_solve",
     "sb_gen_convdiff2d", "sb_gen_stencil7", "sb_gen_convdiff3d", "sb_gen_stencil27",
-    "sb_free_csr", "sb_gen_rhs_random",
+    "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_time_kernel", "sb_vcycle_launches",
 ]
 
 _P = C.c_void_p
@@ -115,6 +116,9 @@ _SIGS = {
     "sb_gen_stencil27": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.POINTER(sb_csr)]),
     "sb_free_csr": (None, [C.POINTER(sb_csr)]),
     "sb_gen_rhs_random": (C.c_int, [C.c_int64, C.c_uint, _D]),
+    "sb_last_solve_ms": (C.c_double, [_P]),
+    "sb_time_kernel": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(sb_cycle), C.c_int, _D, C.POINTER(C.c_int)]),
+    "sb_vcycle_launches": (C.c_int, [_P, C.POINTER(sb_cycle)]),
 }
 
 

@@ -436,6 +436,34 @@ __global__ void k_coarse_gemv(int n, const double *__restrict__ inv, const doubl
     if (lane == 0) x[row] = s;
 }
 
+// Bit-exact coarsest solve (parity mode): the reference's permuted forward
+// substitution (column sweep keeps each row's ascending-j order) and its
+// backward substitution, row by row in ascending-j order, in one thread.
+// lu is the reference's row-major LU (coarse_solver.hpp:168-182).
+__global__ void k_coarse_lu_exact(int n, const double *__restrict__ lu, const int32_t *__restrict__ perm,
+                                  const double *__restrict__ f, double *__restrict__ x) {
+    extern __shared__ double y[];
+    const int lane = threadIdx.x;
+    for (int i = lane; i < n; i += 32) y[i] = f[perm[i]];
+    __syncwarp();
+    for (int j = 0; j < n; ++j) {
+        const double yj = y[j];
+        for (int i = j + 1 + lane; i < n; i += 32)
+            y[i] = __dsub_rn(y[i], __dmul_rn(lu[static_cast<size_t>(i) * n + j], yj));
+        __syncwarp();
+    }
+    if (lane == 0) {
+        for (int i = n - 1; i >= 0; --i) {
+            double s = y[i];
+            const double *row = lu + static_cast<size_t>(i) * n;
+            for (int j = i + 1; j < n; ++j) s = __dsub_rn(s, __dmul_rn(row[j], y[j]));
+            y[i] = __ddiv_rn(s, row[i]);
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) x[i] = y[i];
+}
+
 // ---- Krylov vector kernels (grid-stride, fixed grid => deterministic) -----
 
 #define GRID_LOOP(i, n)                                                                          \
@@ -556,6 +584,10 @@ __global__ void k_bi_p(int64_t n, const double *__restrict__ r, double *__restri
     p[i] = __dadd_rn(r[i], __dmul_rn(beta, __dsub_rn(p[i], __dmul_rn(omega, Apt[i]))));
 }
 
+__global__ void k_fill(int64_t n, double *x, double v) {
+    GRID_LOOP(i, n) x[i] = v;
+}
+
 __global__ void k_set_cond(const DevState *st, CondSet cs) {
     for (int i = 0; i < cs.n; ++i)
         cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(cs.h[i]), st->done ? 0u : 1u);
@@ -595,6 +627,9 @@ struct sb_ctx_s {
     std::vector<sb::DevLevel> L;
     int64_t nc = 0;
     double *inv = nullptr;
+    double *lu = nullptr;
+    int32_t *perm = nullptr;
+    bool coarse_exact = false;
     double *rs = nullptr;  // residual scratch (level sizes <= n0)
     double *kv[12] = {};   // Krylov vectors
     double *partials = nullptr;
@@ -609,6 +644,9 @@ struct sb_ctx_s {
     std::map<std::string, sb::GraphEntry> cache;
     double *h_pinned = nullptr;  // staging for host vectors
     int64_t h_pinned_n = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_solve_ms = 0.0;
+    int launch_count = 0;  // kernels emitted by the last emit_* sequence
 };
 
 namespace sb {
@@ -667,8 +705,12 @@ static void launch_jacobi(const DevLevel &l, cudaStream_t s, const double *xin, 
 }
 
 static void emit_coarse(sb_ctx c, cudaStream_t s, const double *f, double *x) {
+    ++c->launch_count;
     const int n = static_cast<int>(c->nc);
-    k_coarse_gemv<<<(n + 7) / 8, 256, 0, s>>>(n, c->inv, f, x);
+    if (c->coarse_exact)
+        k_coarse_lu_exact<<<1, 32, sizeof(double) * n, s>>>(n, c->lu, c->perm, f, x);
+    else
+        k_coarse_gemv<<<(n + 7) / 8, 256, 0, s>>>(n, c->inv, f, x);
     CK(cudaGetLastError());
 }
 
@@ -691,6 +733,7 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
             other = (cur == X) ? T : X;
             k_jacobi_zero<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, f, l.diag, cur, cp.omega);
             CK(cudaGetLastError());
+            c->launch_count += cp.pre;
             for (int i = 1; i < cp.pre; ++i) {
                 launch_jacobi(l, s, cur, f, other, cp.omega);
                 std::swap(cur, other);
@@ -699,11 +742,13 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
             CK(cudaMemsetAsync(X, 0, sizeof(double) * static_cast<size_t>(l.n), s));
         }
     } else {
+        c->launch_count += cp.pre;
         for (int i = 0; i < cp.pre; ++i) {
             launch_jacobi(l, s, cur, f, other, cp.omega);
             std::swap(cur, other);
         }
     }
+    c->launch_count += 3 + cp.post;  // residual, restriction, prolongation, post sweeps
     const DevLevel &lc = c->L[static_cast<size_t>(k) + 1];
     launch_csr<M_RESID, 0>(l, s, cur, f, c->rs, 0.0, nullptr, Red{});
     k_restrict<<<vec_grid(lc.n), kVecThreads, 0, s>>>(lc.n, l.mem, c->rs, lc.f);
@@ -1070,11 +1115,16 @@ static int run_solve(sb_ctx c, SolveKind kind, const sb_cycle *cpa, const double
         CK(cudaGraphInstantiate(&e.exec, e.g, 0));
         it = c->cache.emplace(key, e).first;
     }
+    CK(cudaEventRecord(c->ev0, c->stream));
     CK(cudaGraphLaunch(it->second.exec, c->stream));
+    CK(cudaEventRecord(c->ev1, c->stream));
     CK(cudaMemcpyAsync(&hs, c->st, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));
     if (host)
         CK(cudaMemcpyAsync(x, dx, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->last_solve_ms = ms;
     const int hist_len = hs.iter + 1;
     if (rep) {
         rep->iterations = hs.iter;
@@ -1130,7 +1180,7 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
     int rc = guard([&] {
         Hier *h = hier_of(hh);
         if (!h || !out) throw invalid_argument("sb_create: null argument");
-        sb_device_opts o{0, 1, -1};
+        sb_device_opts o{0, 1, -1, 0};
         if (opts) o = *opts;
         if (o.host_levels_from >= 0)
             throw invalid_argument("sb_create: hybrid host-level placement is not available in this build");
@@ -1142,6 +1192,8 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
         c->device = o.device;
         c->graphs = o.use_graphs != 0;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&c->ev0));
+        CK(cudaEventCreate(&c->ev1));
         for (auto &s : c->cap) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         const int64_t n0 = h->levels[0].A.n;
         c->L.resize(h->levels.size());
@@ -1161,6 +1213,13 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
         if (h->nc > 0) {
             c->inv = dalloc<double>(c, h->nc * h->nc);
             CK(cudaMemcpy(c->inv, h->inv.data(), sizeof(double) * h->inv.size(), cudaMemcpyHostToDevice));
+            c->coarse_exact = o.coarse_exact != 0;
+            if (c->coarse_exact) {
+                c->lu = dalloc<double>(c, h->nc * h->nc);
+                c->perm = dalloc<int32_t>(c, h->nc);
+                CK(cudaMemcpy(c->lu, h->lu.data(), sizeof(double) * h->lu.size(), cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(c->perm, h->perm.data(), sizeof(int32_t) * h->perm.size(), cudaMemcpyHostToDevice));
+            }
         }
         c->rs = dalloc<double>(c, n0);
         for (auto &v : c->kv) v = dalloc<double>(c, n0);
@@ -1185,6 +1244,8 @@ void sb_destroy(sb_ctx c) {
     if (c->hist_r) cudaFree(c->hist_r);
     if (c->hist_t) cudaFree(c->hist_t);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
     for (auto &s : c->cap)
         if (s) cudaStreamDestroy(s);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -1236,6 +1297,66 @@ int sb_pcg_dev(sb_ctx c, const sb_cycle *cp, const double *d_b, double *d_x, dou
 int sb_pbicgstab_dev(sb_ctx c, const sb_cycle *cp, const double *d_b, double *d_x, double tol, int max_iters,
                      sb_report *rep) {
     return guard([&] { run_solve(c, K_BICG, cp, d_b, d_x, tol, max_iters, rep, false, "pbicgstab"); });
+}
+
+double sb_last_solve_ms(sb_ctx c) { return c ? c->last_solve_ms : 0.0; }
+
+int sb_vcycle_launches(sb_ctx c, const sb_cycle *cp) {
+    int out = 0;
+    const int rc = guard([&] {
+        const Cyc y = check_cycle(c, cp, "vcycle");
+        // count by a dry emission into a throw-away capture
+        cudaGraph_t g = begin_capture(c);
+        c->launch_count = 0;
+        emit_vcycle(c, c->stream, y, 0, c->kv[KB], c->kv[KX], true);
+        out = c->launch_count;
+        end_capture(c, g);
+        cudaGraphDestroy(g);
+    });
+    return rc == SB_OK ? out : -1;
+}
+
+int sb_time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int reps, double *avg_ms, int *launches) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, level);
+        if (reps < 1) throw invalid_argument("sb_time_kernel: reps must be >= 1");
+        Cyc y;
+        if (kind == 0 || kind == 3) y = check_cycle(c, cp, "sb_time_kernel");
+        CK(cudaSetDevice(c->device));
+        cudaStream_t s = c->stream;
+        double *x = c->kv[KX], *t = c->kv[KZ], *f = c->kv[KB];
+        k_fill<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, f, 1.0);
+        k_fill<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, x, 0.5);
+        k_fill<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, t, 0.5);
+        CK(cudaGetLastError());
+        auto once = [&]() {
+            c->launch_count = 0;
+            if (kind == 0) {
+                launch_jacobi(l, s, x, f, t, y.omega);
+                std::swap(x, t);
+                c->launch_count = 1;
+            } else if (kind == 1) {
+                launch_csr<M_SPMV, 0>(l, s, x, nullptr, t, 0.0, nullptr, Red{});
+                c->launch_count = 1;
+            } else if (kind == 2) {
+                launch_csr<M_RESID, 0>(l, s, x, f, t, 0.0, nullptr, Red{});
+                c->launch_count = 1;
+            } else if (kind == 3) {
+                emit_vcycle(c, s, y, level, f, t, true);
+            } else {
+                throw invalid_argument("sb_time_kernel: unknown kind");
+            }
+        };
+        once();  // warm-up
+        CK(cudaEventRecord(c->ev0, s));
+        for (int i = 0; i < reps; ++i) once();
+        CK(cudaEventRecord(c->ev1, s));
+        CK(cudaEventSynchronize(c->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        if (avg_ms) *avg_ms = ms / reps;
+        if (launches) *launches = c->launch_count;
+    });
 }
 
 int sb_spmv(sb_ctx c, int level, const double *x, double *y) {

@@ -312,7 +312,8 @@ class HierarchyStats:
 # Hierarchy (inc/hierarchy.hpp:49-93) — host setup + lazily created device context
 # --------------------------------------------------------------------------
 class Hierarchy:
-    def __init__(self, A: CsrMatrix, cfg: SolverConfig = None, device: int = 0, *, _coarse_solver=None):
+    def __init__(self, A: CsrMatrix, cfg: SolverConfig = None, device: int = 0, *, _coarse_solver=None,
+                 coarse_exact: bool = False):
         cfg = cfg or SolverConfig()
         if not A.is_square():
             raise InvalidArgument("Hierarchy: matrix must be square")
@@ -330,6 +331,7 @@ class Hierarchy:
         self._h = h
         self._ctx = None
         self._device = device
+        self._coarse_exact = bool(coarse_exact)
         self._levels = None
         self._A0 = A
         self.config = cfg
@@ -385,7 +387,7 @@ class Hierarchy:
     def ctx(self):
         if self._ctx is None:
             c = C.c_void_p()
-            opts = _lib.sb_device_opts(self._device, 1, -1)
+            opts = _lib.sb_device_opts(self._device, 1, -1, int(self._coarse_exact))
             check(_lib.lib().sb_create(self._h, C.byref(opts), C.byref(c)))
             self._ctx = c
         return self._ctx
