@@ -19,6 +19,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "_build", "libsparsh_oracle.so")
+PORT_FMA_SO = os.path.join(HERE, "_build", "libsparsh_oracle_fma.so")
 REF_SO = os.path.join(HERE, "_ref", "libsparsh_ref.so")
 _D = C.POINTER(C.c_double)
 _I = C.POINTER(C.c_int32)
@@ -70,12 +71,14 @@ class OcCsr(C.Structure):
 
 
 class Port:
+    """The restatement; fma=True loads the FMA-contracted build (noise-floor probe)."""
     kind = "port"
 
-    def __init__(self):
-        if not os.path.exists(PORT_SO):
+    def __init__(self, fma: bool = False):
+        so = PORT_FMA_SO if fma else PORT_SO
+        if not os.path.exists(so):
             build(ref=False)
-        L = C.CDLL(PORT_SO)
+        L = C.CDLL(so)
         L.oc_hier_build.restype = C.c_void_p
         L.oc_hier_build.argtypes = [C.POINTER(OcCsr), C.c_int32, C.c_int, C.POINTER(C.c_int)]
         L.oc_hier_free.argtypes = [C.c_void_p]

@@ -310,83 +310,113 @@ template <int NV> __device__ __forceinline__ void finish_reduction(const Red &r,
 
 enum CsrMode { M_SPMV = 0, M_RESID = 1, M_JACOBI = 2 };
 
-// One CTA per tile of <= 256 consecutive rows (tile_ptr from setup). The tile's
-// contiguous nnz range of values and column indices is brought into shared
-// memory by two TMA bulk copies (16-byte aligned windows), then thread t owns
-// row r0+t and walks it in CSR order. Tiles whose nnz exceed the staging
-// capacity (a single very long row) read straight from global memory.
+// Persistent, double-buffered CSR tile pipeline. Tiles of <= 256 consecutive
+// rows (tile_ptr, built at setup) are dealt round-robin to a grid sized to the
+// SM count; for each tile one elected thread issues two TMA bulk copies
+// (values + column indices, 16-byte aligned windows of the tile's contiguous
+// nnz range) into the NEXT stage while the CTA computes the current one, so
+// HBM streaming overlaps the x-gathers and arithmetic. Thread t owns row
+// r0 + t and walks it in CSR order from shared memory. A tile whose nnz exceed
+// the stage capacity (a single very long row) reads straight from global.
 template <int MODE, int NV>
-__global__ void __launch_bounds__(kTileRows)
+__global__ void __launch_bounds__(kTileRows, 3)
     k_csr_tile(const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-               const double *__restrict__ val, const int32_t *__restrict__ tile_ptr,
+               const double *__restrict__ val, const int32_t *__restrict__ tile_ptr, int ntiles,
                const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out,
                double omega, int cap, const int *skip, Red red) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int4 hdr[2];
     double acc[NV > 0 ? NV : 1];
 #pragma unroll
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
 
+    const int cap_v = (cap + 3) & ~1;   // doubles per stage
+    const int cap_c = (cap + 11) & ~3;  // ints per stage
+    const size_t stage_bytes = static_cast<size_t>(cap_v) * 8 + static_cast<size_t>(cap_c) * 4;
     const bool active = !(skip && *skip);
-    if (active) {
-        const int r0 = tile_ptr[blockIdx.x], r1 = tile_ptr[blockIdx.x + 1];
+
+    // thread 0: stage tile t into buffer s
+    auto issue = [&](int t, int s) {
+        const int r0 = tile_ptr[t], r1 = tile_ptr[t + 1];
         const int e0 = rp[r0], e1 = rp[r1];
-        const bool staged = (e1 - e0) <= cap;
-        const int va0 = e0 & ~1, ca0 = e0 & ~3;
-        const int cap_v = (cap + 3) & ~1;  // doubles
-        double *sv = reinterpret_cast<double *>(smem);
-        int32_t *sc = reinterpret_cast<int32_t *>(smem + static_cast<size_t>(cap_v) * 8);
-        if (staged && threadIdx.x == 0) {
-            mbar_init(&bar, 1);
-            fence_mbar_init();
+        hdr[s] = make_int4(r0, r1, e0, e1);
+        double *sv = reinterpret_cast<double *>(smem + s * stage_bytes);
+        int32_t *sc = reinterpret_cast<int32_t *>(smem + s * stage_bytes + static_cast<size_t>(cap_v) * 8);
+        if (e1 - e0 <= cap && e1 > e0) {
+            const int va0 = e0 & ~1, ca0 = e0 & ~3;
             const uint32_t vbytes = static_cast<uint32_t>(((e1 + 1) & ~1) - va0) * 8u;
             const uint32_t cbytes = static_cast<uint32_t>(((e1 + 3) & ~3) - ca0) * 4u;
-            mbar_expect_tx(&bar, vbytes + cbytes);
-            if (vbytes) bulk_g2s(sv, val + va0, vbytes, &bar);
-            if (cbytes) bulk_g2s(sc, ci + ca0, cbytes, &bar);
-            if (vbytes + cbytes == 0) mbar_expect_tx(&bar, 0);
+            mbar_expect_tx(&bar[s], vbytes + cbytes);
+            bulk_g2s(sv, val + va0, vbytes, &bar[s]);
+            bulk_g2s(sc, ci + ca0, cbytes, &bar[s]);
+        } else {
+            mbar_expect_tx(&bar[s], 0);  // plain arrive: nothing staged
         }
-        const int row = r0 + static_cast<int>(threadIdx.x);
-        int rs = 0, re = 0;
-        double fi = 0.0, xi = 0.0;
-        if (row < r1) {
-            rs = rp[row];
-            re = rp[row + 1];
-            if (MODE != M_SPMV) fi = f[row];
-            if (MODE == M_JACOBI) xi = x[row];
+    };
+
+    if (active) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+            fence_mbar_init();
         }
-        __syncthreads();  // barrier init visible before anyone waits
-        if (staged) mbar_wait(&bar, 0);
-        if (row < r1) {
-            double sum = 0.0, d = 0.0;
-            const int32_t *cc = staged ? sc - ca0 : ci;
-            const double *vv = staged ? sv - va0 : val;
-            for (int k = rs; k < re; k += 8) {
-                int c[8];
-                double a[8], xv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (k + u < re) {
-                        c[u] = cc[k + u];
-                        a[u] = vv[k + u];
-                    }
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (k + u < re) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (k + u < re) {
-                        sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
-                        if (MODE == M_JACOBI && c[u] == row) d = a[u];
-                    }
+        __syncthreads();
+        int t = blockIdx.x;
+        if (threadIdx.x == 0 && t < ntiles) issue(t, 0);
+        uint32_t phases = 0u;  // bit s = parity of stage s
+        for (int s = 0; t < ntiles; t += gridDim.x, s ^= 1) {
+            const int tn = t + gridDim.x;
+            if (threadIdx.x == 0 && tn < ntiles) issue(tn, s ^ 1);
+            // per-row operands, loaded before waiting on the stage
+            const int r0g = tile_ptr[t], r1g = tile_ptr[t + 1];
+            const int row = r0g + static_cast<int>(threadIdx.x);
+            int rs = 0, re = 0;
+            double fi = 0.0, xi = 0.0;
+            if (row < r1g) {
+                rs = rp[row];
+                re = rp[row + 1];
+                if (MODE != M_SPMV) fi = f[row];
+                if (MODE == M_JACOBI) xi = x[row];
             }
-            double o;
-            if (MODE == M_SPMV) o = sum;
-            else if (MODE == M_RESID) o = __dsub_rn(fi, sum);
-            else o = __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
-            out[row] = o;
-            if (NV >= 1) acc[0] = o * (red.w0 ? red.w0[row] : o);
-            if (NV >= 2) acc[NV >= 2 ? 1 : 0] = o * (red.w1 ? red.w1[row] : o);
+            mbar_wait(&bar[s], (phases >> s) & 1u);
+            phases ^= 1u << s;
+            const int4 h = hdr[s];
+            const bool staged = (h.w - h.z) <= cap;
+            if (row < r1g) {
+                const int32_t *cc = staged
+                    ? reinterpret_cast<const int32_t *>(smem + s * stage_bytes + static_cast<size_t>(cap_v) * 8) - (h.z & ~3)
+                    : ci;
+                const double *vv = staged ? reinterpret_cast<const double *>(smem + s * stage_bytes) - (h.z & ~1) : val;
+                double sum = 0.0, d = 0.0;
+                for (int k = rs; k < re; k += 8) {
+                    int c[8];
+                    double a[8], xv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (k + u < re) {
+                            c[u] = cc[k + u];
+                            a[u] = vv[k + u];
+                        }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (k + u < re) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (k + u < re) {
+                            sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
+                            if (MODE == M_JACOBI && c[u] == row) d = a[u];
+                        }
+                }
+                double o;
+                if (MODE == M_SPMV) o = sum;
+                else if (MODE == M_RESID) o = __dsub_rn(fi, sum);
+                else o = __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
+                out[row] = o;
+                if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row] : o);
+                if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
+            }
+            __syncthreads();  // stage s fully consumed before it is refilled
         }
     }
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
@@ -602,7 +632,7 @@ struct DevLevel {
     int32_t *rp = nullptr, *ci = nullptr, *agg = nullptr, *tiles = nullptr;
     double *v = nullptr, *diag = nullptr;
     int2 *mem = nullptr;
-    int ntiles = 0, cap = 0;
+    int ntiles = 0, cap = 0, grid = 0;
     size_t smem = 0;
     double *x = nullptr, *f = nullptr, *t = nullptr;
     int64_t bad_diag = -1;
@@ -694,8 +724,8 @@ template <int MODE, int NV>
 static void launch_csr(const DevLevel &l, cudaStream_t s, const double *x, const double *f, double *out,
                        double omega, const int *skip, const Red &red) {
     if (l.n == 0) return;
-    k_csr_tile<MODE, NV><<<l.ntiles, kTileRows, l.smem, s>>>(l.rp, l.ci, l.v, l.tiles, x, f, out, omega,
-                                                           l.cap, skip, red);
+    k_csr_tile<MODE, NV><<<std::min(l.ntiles, l.grid), kTileRows, l.smem, s>>>(
+        l.rp, l.ci, l.v, l.tiles, l.ntiles, x, f, out, omega, l.cap, skip, red);
     CK(cudaGetLastError());
 }
 
@@ -982,7 +1012,7 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
     CK(cudaMemcpy(D.tiles, tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice));
     const size_t cap_v = static_cast<size_t>((D.cap + 3) & ~1);
     const size_t cap_c = static_cast<size_t>((D.cap + 11) & ~3);
-    D.smem = cap_v * 8 + cap_c * 4;
+    D.smem = 2 * (cap_v * 8 + cap_c * 4);  // two pipeline stages
     if (!coarsest) {
         D.nc = H.n_coarse;
         D.agg = dalloc<int32_t>(c, A.n);
@@ -1209,6 +1239,13 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
         set_smem_attr<M_RESID, 0>(max_smem);
         set_smem_attr<M_RESID, 1>(max_smem);
         set_smem_attr<M_JACOBI, 0>(max_smem);
+        int nsm = 0;
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
+        for (auto &l : c->L) {
+            int occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tile<M_JACOBI, 0>, kTileRows, l.smem));
+            l.grid = std::max(1, nsm * std::max(occ, 1));
+        }
         c->nc = h->nc;
         if (h->nc > 0) {
             c->inv = dalloc<double>(c, h->nc * h->nc);
