@@ -180,10 +180,15 @@ int sb_pbicgstab_dev(sb_ctx ctx, const sb_cycle *cp, const double *d_b, double *
 double sb_last_solve_ms(sb_ctx ctx);
 /* Times `reps` back-to-back launches of one kernel on level `level` with CUDA
  * events on sb_stream; *avg_ms = mean per launch. kind: 0 Jacobi sweep,
- * 1 SpMV, 2 residual, 3 one V-cycle from x = 0 (cp required for 0 and 3).
+ * 1 SpMV, 2 residual, 3 one V-cycle from x = 0 launched eagerly, 4 the same
+ * V-cycle captured once as a CUDA graph and replayed (cp required for 0, 3, 4).
  * *launches = kernels launched per repetition. */
 int sb_time_kernel(sb_ctx ctx, int kind, int level, const sb_cycle *cp, int reps, double *avg_ms,
                    int *launches);
+/* Diagnostics: tail-kernel phase timestamps (needs SB_TAIL_TRACE=1 at
+ * sb_create) and the tail placement (first tail level, cluster CTAs, smem). */
+int sb_tail_trace(sb_ctx ctx, unsigned long long *out, int cap);
+int sb_tail_info(sb_ctx ctx, int *tail_from, int *ctas, int *smem_bytes);
 /* Kernels launched by one V-cycle from level 0 (graph node count). */
 int sb_vcycle_launches(sb_ctx ctx, const sb_cycle *cp);
 

@@ -78,7 +78,8 @@ EXPORTS = [
     "sb_pcg", "sb_pbicgstab", "sb_amg_solve", "sb_pcg_dev", "sb_pbicgstab_dev", "sb_spmv",
     "sb_smooth", "sb_residual", "sb_restrict", "sb_prolong", "sb_coarse_solve",
     "sb_gen_convdiff2d", "sb_gen_stencil7", "sb_gen_convdiff3d", "sb_gen_stencil27",
-    "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_time_kernel", "sb_vcycle_launches",
+    "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_time_kernel", "sb_vcycle_launches", "sb_tail_trace",
+    "sb_tail_info",
 ]
 
 _P = C.c_void_p
@@ -119,6 +120,8 @@ _SIGS = {
     "sb_last_solve_ms": (C.c_double, [_P]),
     "sb_time_kernel": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(sb_cycle), C.c_int, _D, C.POINTER(C.c_int)]),
     "sb_vcycle_launches": (C.c_int, [_P, C.POINTER(sb_cycle)]),
+    "sb_tail_trace": (C.c_int, [_P, C.POINTER(C.c_ulonglong), C.c_int]),
+    "sb_tail_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
 }
 
 

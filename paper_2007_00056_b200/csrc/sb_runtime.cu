@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -77,6 +78,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
                  "r"(phase)
                  : "memory");
 }
+// Programmatic dependent launch: wait for the predecessor grid's completion
+// (no-op when launched without the attribute) / allow the successor to launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -308,7 +314,73 @@ template <int NV> __device__ __forceinline__ void finish_reduction(const Red &r,
 // CSR tile kernel: SpMV / residual / Jacobi sweep (+ optional fused dot)
 // ===========================================================================
 
-enum CsrMode { M_SPMV = 0, M_RESID = 1, M_JACOBI = 2 };
+enum CsrMode {
+    M_SPMV = 0,          // y = A x                          (csr.hpp:174-194)
+    M_RESID = 1,         // r = f - A x                      (csr.hpp:267-274)
+    M_JACOBI = 2,        // x' = x + w (f - A x) / a_ii      (smoother.hpp:113-120)
+    M_JACOBI_ZERO = 3,   // first two sweeps from x = 0 fused: neighbours' x0_j = 0 + w f_j / a_jj
+    M_JACOBI_PROLONG = 4 // prolongation + first post-sweep fused: x_j + (0 + x_c[agg_j])
+};
+
+// Operands of the fused modes.
+struct Aux {
+    const double *diag;   // a_ii (M_JACOBI_ZERO)
+    const int32_t *agg;   // fine_to_coarse (M_JACOBI_PROLONG)
+    const double *xc;     // coarse correction (M_JACOBI_PROLONG)
+};
+
+// Mutable vectors inside the cluster tail kernel are read with ld.global.cg
+// (L2; another CTA of the cluster may have rewritten them since the last
+// phase); everywhere else with the read-only path.
+template <bool CG> __device__ __forceinline__ double ldv(const double *p) {
+    if constexpr (CG) return __ldcg(p);
+    else return __ldg(p);
+}
+
+// The value the reference's sweep sees for x_j (bitwise).
+template <int MODE, bool CG>
+__device__ __forceinline__ double xval(int j, const double *x, const double *f, const Aux &a, double omega) {
+    if constexpr (MODE == M_JACOBI_ZERO)
+        return __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, ldv<CG>(f + j)), __ldg(a.diag + j)));
+    else if constexpr (MODE == M_JACOBI_PROLONG)
+        return __dadd_rn(ldv<CG>(x + j), __dadd_rn(0.0, ldv<CG>(a.xc + __ldg(a.agg + j))));
+    else
+        return ldv<CG>(x + j);
+}
+
+// One row in the reference's order: sum = 0.0; sum += a_k * x_{c_k} for k in
+// CSR order (no FMA), then the mode's epilogue. cc / vv index the row's entries.
+template <int MODE, bool CG, int U = 8>
+__device__ __forceinline__ double row_eval(int row, int rs, int re, const int32_t *cc, const double *vv,
+                                           const double *x, const double *f, double fi, const Aux &aux,
+                                           double omega) {
+    double sum = 0.0, d = 0.0;
+    for (int k = rs; k < re; k += U) {
+        int c[U];
+        double a[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k + u < re) {
+                c[u] = cc[k + u];
+                a[u] = vv[k + u];
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k + u < re) xv[u] = xval<MODE, CG>(c[u], x, f, aux, omega);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k + u < re) {
+                sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
+                if (MODE >= M_JACOBI && c[u] == row) d = a[u];
+            }
+    }
+    if constexpr (MODE == M_SPMV) return sum;
+    else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
+    else {
+        const double xi = xval<MODE, CG>(row, x, f, aux, omega);
+        return __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
+    }
+}
 
 // Persistent, double-buffered CSR tile pipeline. Tiles of <= 256 consecutive
 // rows (tile_ptr, built at setup) are dealt round-robin to a grid sized to the
@@ -318,15 +390,17 @@ enum CsrMode { M_SPMV = 0, M_RESID = 1, M_JACOBI = 2 };
 // HBM streaming overlaps the x-gathers and arithmetic. Thread t owns row
 // r0 + t and walks it in CSR order from shared memory. A tile whose nnz exceed
 // the stage capacity (a single very long row) reads straight from global.
+constexpr int kStages = 3;  // TMA pipeline depth (tiles in flight per CTA)
+
 template <int MODE, int NV>
 __global__ void __launch_bounds__(kTileRows, 3)
     k_csr_tile(const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                const double *__restrict__ val, const int32_t *__restrict__ tile_ptr, int ntiles,
                const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out,
-               double omega, int cap, const int *skip, Red red) {
+               double omega, int cap, const int *skip, Aux aux, Red red) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ int4 hdr[2];
+    __shared__ __align__(8) uint64_t bar[kStages];
+    __shared__ int4 hdr[kStages];
     double acc[NV > 0 ? NV : 1];
 #pragma unroll
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
@@ -334,9 +408,9 @@ __global__ void __launch_bounds__(kTileRows, 3)
     const int cap_v = (cap + 3) & ~1;   // doubles per stage
     const int cap_c = (cap + 11) & ~3;  // ints per stage
     const size_t stage_bytes = static_cast<size_t>(cap_v) * 8 + static_cast<size_t>(cap_c) * 4;
-    const bool active = !(skip && *skip);
 
-    // thread 0: stage tile t into buffer s
+    // thread 0: stage tile t into buffer s (matrix data only: constant, so it
+    // may be issued before the programmatic-dependency wait)
     auto issue = [&](int t, int s) {
         const int r0 = tile_ptr[t], r1 = tile_ptr[t + 1];
         const int e0 = rp[r0], e1 = rp[r1];
@@ -355,29 +429,43 @@ __global__ void __launch_bounds__(kTileRows, 3)
         }
     };
 
-    if (active) {
-        if (threadIdx.x == 0) {
-            mbar_init(&bar[0], 1);
-            mbar_init(&bar[1], 1);
-            fence_mbar_init();
-        }
-        __syncthreads();
-        int t = blockIdx.x;
-        if (threadIdx.x == 0 && t < ntiles) issue(t, 0);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < kStages; ++q) mbar_init(&bar[q], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int G = static_cast<int>(gridDim.x);
+    int issued = 0;
+    if (threadIdx.x == 0)
+        for (int q = 0; q < kStages - 1; ++q)
+            if (static_cast<int>(blockIdx.x) + q * G < ntiles) {
+                issue(static_cast<int>(blockIdx.x) + q * G, q);
+                ++issued;
+            }
+    pdl_wait();  // predecessor kernel complete: x, f (and skip) are final
+    const bool active = !(skip && *skip);
+    if (!active) {  // skipped (solve already finished): drain the prologue's copies
+        for (int q = 0; q < kStages - 1; ++q)
+            if (static_cast<int>(blockIdx.x) + q * G < ntiles) mbar_wait(&bar[q], 0u);
+        pdl_trigger();
+    } else {
         uint32_t phases = 0u;  // bit s = parity of stage s
-        for (int s = 0; t < ntiles; t += gridDim.x, s ^= 1) {
-            const int tn = t + gridDim.x;
-            if (threadIdx.x == 0 && tn < ntiles) issue(tn, s ^ 1);
+        int s = 0;
+        for (int t = blockIdx.x; t < ntiles; t += G, s = (s + 1 == kStages) ? 0 : s + 1) {
+            if (t + G >= ntiles) pdl_trigger();  // last tile of this CTA: let the next kernel launch
+            const int tn = t + (kStages - 1) * G;
+            const int sn = (s + kStages - 1) % kStages;
+            if (threadIdx.x == 0 && tn < ntiles) issue(tn, sn);
             // per-row operands, loaded before waiting on the stage
             const int r0g = tile_ptr[t], r1g = tile_ptr[t + 1];
             const int row = r0g + static_cast<int>(threadIdx.x);
             int rs = 0, re = 0;
-            double fi = 0.0, xi = 0.0;
+            double fi = 0.0;
             if (row < r1g) {
                 rs = rp[row];
                 re = rp[row + 1];
                 if (MODE != M_SPMV) fi = f[row];
-                if (MODE == M_JACOBI) xi = x[row];
             }
             mbar_wait(&bar[s], (phases >> s) & 1u);
             phases ^= 1u << s;
@@ -388,30 +476,7 @@ __global__ void __launch_bounds__(kTileRows, 3)
                     ? reinterpret_cast<const int32_t *>(smem + s * stage_bytes + static_cast<size_t>(cap_v) * 8) - (h.z & ~3)
                     : ci;
                 const double *vv = staged ? reinterpret_cast<const double *>(smem + s * stage_bytes) - (h.z & ~1) : val;
-                double sum = 0.0, d = 0.0;
-                for (int k = rs; k < re; k += 8) {
-                    int c[8];
-                    double a[8], xv[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (k + u < re) {
-                            c[u] = cc[k + u];
-                            a[u] = vv[k + u];
-                        }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (k + u < re) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (k + u < re) {
-                            sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
-                            if (MODE == M_JACOBI && c[u] == row) d = a[u];
-                        }
-                }
-                double o;
-                if (MODE == M_SPMV) o = sum;
-                else if (MODE == M_RESID) o = __dsub_rn(fi, sum);
-                else o = __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
+                const double o = row_eval<MODE, false>(row, rs, re, cc, vv, x, f, fi, aux, omega);
                 out[row] = o;
                 if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row] : o);
                 if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
@@ -419,13 +484,278 @@ __global__ void __launch_bounds__(kTileRows, 3)
             __syncthreads();  // stage s fully consumed before it is refilled
         }
     }
+    (void)issued;
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
+}
+
+// ===========================================================================
+// Cluster-resident tail: the deepest levels (each CTA's slice of every tail
+// level fits in its shared memory), down to the coarsest solve and back up, in
+// ONE launch of a thread-block cluster (16 CTAs where schedulable). CTA r owns
+// the contiguous row block [r*rows_per, (r+1)*rows_per) of every level and
+// keeps that block's CSR rows, diagonal, aggregate map, members and all level
+// vectors in its shared memory; neighbour values come over DSMEM
+// (ld.shared::cluster). Phases are separated by hardware cluster barriers
+// (~0.2 us) instead of kernel boundaries (~2-5 us each), which is what these
+// latency-bound levels pay. Arithmetic is the same bitwise row order as the
+// big levels (sum = 0; sum += a*x in CSR order, no FMA).
+// ===========================================================================
+
+constexpr int kTailMaxLevels = 24;
+constexpr int kTailThreads = 512;
+
+struct TailLevel {
+    int n, nc;        // rows; coarse rows (-1 on the coarsest)
+    int rows_per;     // rows owned per CTA (last CTA may own fewer)
+    int nnz_cap;      // max local nnz over CTAs
+    const int32_t *rp, *ci, *agg;
+    const double *v, *diag;
+    const int2 *mem;  // members of coarse rows (next level)
+    // shared-memory offsets (bytes) of this level's block
+    int o_rp, o_ci, o_v, o_diag, o_agg, o_mem, o_x, o_t, o_f, o_r;
+};
+
+struct TailDesc {
+    int nlev;          // including the coarsest
+    int ncoarse;
+    int o_inv, o_fc;   // coarsest: owned inverse rows, full f_c copy
+    int smem_bytes;
+    const double *inv;
+    TailLevel L[kTailMaxLevels];
+};
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_ncta() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+// f64 at the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ double dsmem_ld(const double *local, unsigned cta) {
+    uint32_t a = smem_u32(local), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(cta));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+    return v;
+}
+
+template <typename T> __device__ __forceinline__ T *sm(unsigned char *base, int off) {
+    return reinterpret_cast<T *>(base + off);
+}
+
+// value of global row j of a level vector stored block-wise at offset `off`
+__device__ __forceinline__ double tget(unsigned char *base, int off, int j, int rows_per, unsigned me) {
+    const unsigned o = static_cast<unsigned>(j / rows_per);
+    const double *p = sm<double>(base, off) + (j - static_cast<int>(o) * rows_per);
+    return o == me ? *p : dsmem_ld(p, o);
+}
+
+// one Jacobi sweep (or residual when RESID) over the CTA's own rows:
+// out_i = x_i + w (f_i - sum_k a_k x_{c_k}) / a_ii, sum in CSR order
+template <bool RESID>
+__device__ __forceinline__ void tail_sweep(unsigned char *sb, const TailLevel &l, int o_in, int o_out,
+                                           double omega, unsigned me, int r0, int m) {
+    const int32_t *rp = sm<int32_t>(sb, l.o_rp);
+    const int32_t *ci = sm<int32_t>(sb, l.o_ci);
+    const double *v = sm<double>(sb, l.o_v);
+    const double *f = sm<double>(sb, l.o_f);
+    const double *xin = sm<double>(sb, o_in);
+    double *out = sm<double>(sb, o_out);
+    for (int li = threadIdx.x; li < m; li += blockDim.x) {
+        const int row = r0 + li;
+        const int rs = rp[li], re = rp[li + 1];
+        double sum = 0.0, d = 0.0;
+        for (int k = rs; k < re; k += 4) {
+            int c[4];
+            double a[4], xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k + u < re) {
+                    c[u] = ci[k + u];
+                    a[u] = v[k + u];
+                }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k + u < re) xv[u] = tget(sb, o_in, c[u], l.rows_per, me);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k + u < re) {
+                    sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
+                    if (c[u] == row) d = a[u];
+                }
+        }
+        if constexpr (RESID) out[li] = __dsub_rn(f[li], sum);
+        else out[li] = __dadd_rn(xin[li], __ddiv_rn(__dmul_rn(omega, __dsub_rn(f[li], sum)), d));
+    }
+}
+
+__global__ void __launch_bounds__(kTailThreads, 1)
+    k_tail(const TailDesc *__restrict__ Dg, const double *f0, double *X0, double omega, int pre, int post,
+           unsigned long long *trace) {
+    extern __shared__ __align__(16) unsigned char sb[];
+    int ntr = 0;
+    auto mark = [&]() {
+        if (trace && threadIdx.x == 0 && cluster_rank() == 0 && ntr < 255) trace[1 + ntr++] = globaltimer();
+    };
+    mark();
+    __shared__ TailDesc D;
+    // descriptor into shared memory (uniform reads below)
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(TailDesc) / 4); i += blockDim.x)
+        reinterpret_cast<int *>(&D)[i] = reinterpret_cast<const int *>(Dg)[i];
+    __syncthreads();
+    const unsigned me = cluster_rank();
+    const int nlev = D.nlev;
+
+    // ---- load this CTA's block of every level into shared memory --------------
+    for (int q = 0; q + 1 < nlev; ++q) {
+        const TailLevel &l = D.L[q];
+        const int r0 = static_cast<int>(me) * l.rows_per;
+        const int m = max(0, min(l.rows_per, l.n - r0));
+        const int e0 = m > 0 ? __ldg(l.rp + r0) : 0;
+        const int e1 = m > 0 ? __ldg(l.rp + r0 + m) : 0;
+        int32_t *rp = sm<int32_t>(sb, l.o_rp);
+        for (int i = threadIdx.x; i <= m; i += blockDim.x) rp[i] = (m > 0 ? __ldg(l.rp + r0 + i) : 0) - e0;
+        for (int k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
+            sm<int32_t>(sb, l.o_ci)[k] = __ldg(l.ci + e0 + k);
+            sm<double>(sb, l.o_v)[k] = __ldg(l.v + e0 + k);
+        }
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            sm<double>(sb, l.o_diag)[i] = __ldg(l.diag + r0 + i);
+            sm<int32_t>(sb, l.o_agg)[i] = __ldg(l.agg + r0 + i);
+        }
+        const TailLevel &lc = D.L[q + 1];
+        const int c0 = static_cast<int>(me) * lc.rows_per;
+        const int mc = max(0, min(lc.rows_per, lc.n - c0));
+        for (int c = threadIdx.x; c < mc; c += blockDim.x) sm<int2>(sb, l.o_mem)[c] = __ldg(l.mem + c0 + c);
+    }
+    pdl_wait();  // the predecessor (restriction) has produced f0
+    {
+        const TailLevel &l = D.L[0];
+        const int r0 = static_cast<int>(me) * l.rows_per;
+        const int m = max(0, min(l.rows_per, l.n - r0));
+        for (int i = threadIdx.x; i < m; i += blockDim.x) sm<double>(sb, l.o_f)[i] = __ldcg(f0 + r0 + i);
+    }
+    if (nlev >= 1) {  // coarsest: own rows of the inverse
+        const TailLevel &l = D.L[nlev - 1];
+        const int r0 = static_cast<int>(me) * l.rows_per;
+        const int m = max(0, min(l.rows_per, l.n - r0));
+        double *inv = sm<double>(sb, D.o_inv);
+        for (int k = threadIdx.x; k < m * D.ncoarse; k += blockDim.x)
+            inv[k] = __ldg(D.inv + static_cast<size_t>(r0) * D.ncoarse + k);
+    }
+    cluster_sync_all();
+    mark();
+
+    uint32_t cur_is_x = 0u;  // per level: pre-smoothed iterate in x (1) or t (0)
+    // ---- down -----------------------------------------------------------------
+    for (int q = 0; q < nlev; ++q) {
+        const TailLevel &l = D.L[q];
+        const int r0 = static_cast<int>(me) * l.rows_per;
+        const int m = max(0, min(l.rows_per, l.n - r0));
+        if (q + 1 == nlev) {  // coarsest: gather f_c, then own rows of A_c^{-1} f_c
+            double *fc = sm<double>(sb, D.o_fc);
+            for (int j = threadIdx.x; j < D.ncoarse; j += blockDim.x) fc[j] = tget(sb, l.o_f, j, l.rows_per, me);
+            __syncthreads();
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+            const double *inv = sm<double>(sb, D.o_inv);
+            for (int li = warp; li < m; li += nw) {
+                double acc = 0.0;
+                for (int j = lane; j < D.ncoarse; j += 32) acc += inv[static_cast<size_t>(li) * D.ncoarse + j] * fc[j];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+                if (lane == 0) sm<double>(sb, l.o_x)[li] = acc;
+            }
+            cluster_sync_all();
+    mark();
+            break;
+        }
+        // plan: the prolongation runs in place on the pre-smoothed iterate and
+        // the post-sweeps must end in x
+        const int pre_end = (post % 2 == 0) ? l.o_x : l.o_t;
+        int cur = pre_end;
+        if (pre == 0) {
+            for (int i = threadIdx.x; i < m; i += blockDim.x) sm<double>(sb, pre_end)[i] = 0.0;
+        } else {
+            const int first = (pre % 2 == 1) ? pre_end : (pre_end == l.o_x ? l.o_t : l.o_x);
+            const double *f = sm<double>(sb, l.o_f);
+            const double *dg = sm<double>(sb, l.o_diag);
+            for (int i = threadIdx.x; i < m; i += blockDim.x)  // sweep 1 from x = 0
+                sm<double>(sb, first)[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, f[i]), dg[i]));
+            cur = first;
+            for (int sw = 1; sw < pre; ++sw) {
+                cluster_sync_all();
+    mark();
+                const int nxt = cur == l.o_x ? l.o_t : l.o_x;
+                tail_sweep<false>(sb, l, cur, nxt, omega, me, r0, m);
+                cur = nxt;
+            }
+        }
+        if (cur == l.o_x) cur_is_x |= 1u << q;
+        cluster_sync_all();
+    mark();
+        tail_sweep<true>(sb, l, cur, l.o_r, omega, me, r0, m);  // r = f - A x
+        cluster_sync_all();
+    mark();
+        // restriction: f_c[c] = (0.0 + r[m0]) + r[m1] (ascending members)
+        const TailLevel &lc = D.L[q + 1];
+        const int c0 = static_cast<int>(me) * lc.rows_per;
+        const int mc = max(0, min(lc.rows_per, lc.n - c0));
+        for (int c = threadIdx.x; c < mc; c += blockDim.x) {
+            const int2 mm = sm<int2>(sb, l.o_mem)[c];
+            double acc = __dadd_rn(0.0, tget(sb, l.o_r, mm.x, l.rows_per, me));
+            if (mm.y >= 0) acc = __dadd_rn(acc, tget(sb, l.o_r, mm.y, l.rows_per, me));
+            sm<double>(sb, lc.o_f)[c] = acc;
+        }
+        cluster_sync_all();
+    mark();
+    }
+    // ---- up -----------------------------------------------------------------------
+    for (int q = nlev - 2; q >= 0; --q) {
+        const TailLevel &l = D.L[q];
+        const TailLevel &lc = D.L[q + 1];
+        const int r0 = static_cast<int>(me) * l.rows_per;
+        const int m = max(0, min(l.rows_per, l.n - r0));
+        int cur = (cur_is_x >> q) & 1u ? l.o_x : l.o_t;
+        // x += P x_c: x_i + (0.0 + x_c[agg_i]) (cycle.hpp:72-73), in place
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            double *xi = sm<double>(sb, cur) + i;
+            *xi = __dadd_rn(*xi, __dadd_rn(0.0, tget(sb, lc.o_x, sm<int32_t>(sb, l.o_agg)[i], lc.rows_per, me)));
+        }
+        for (int sw = 0; sw < post; ++sw) {
+            cluster_sync_all();
+    mark();
+            const int nxt = cur == l.o_x ? l.o_t : l.o_x;
+            tail_sweep<false>(sb, l, cur, nxt, omega, me, r0, m);
+            cur = nxt;
+        }
+        cluster_sync_all();
+    mark();
+    }
+    // ---- result of tail level 0 -> X0 --------------------------------------------
+    {
+        const TailLevel &l = D.L[0];
+        const int r0 = static_cast<int>(me) * l.rows_per;
+        const int m = max(0, min(l.rows_per, l.n - r0));
+        for (int i = threadIdx.x; i < m; i += blockDim.x) X0[r0 + i] = sm<double>(sb, l.o_x)[i];
+    }
+    cluster_sync_all();  // no CTA exits while others may still read its shared memory
+    mark();
+    if (trace && threadIdx.x == 0 && cluster_rank() == 0) trace[0] = ntr;
 }
 
 // First pre-smoothing sweep from x = 0: the reference computes
 // x_i = 0 + omega*(f_i - 0)/a_ii with spmv(A, 0) = +0.0 (smoother.hpp:112-119).
 __global__ void k_jacobi_zero(int64_t n, const double *__restrict__ f,
                               const double *__restrict__ diag, double *__restrict__ x, double omega) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         x[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, f[i]), diag[i]));
@@ -434,6 +764,7 @@ __global__ void k_jacobi_zero(int64_t n, const double *__restrict__ f,
 // f_c[c] = (0.0 + r[m0]) + r[m1], members ascending (csr.hpp:232-239 with unit P).
 __global__ void k_restrict(int64_t nc, const int2 *__restrict__ mem, const double *__restrict__ r,
                            double *__restrict__ fc) {
+    pdl_wait();
     for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < nc;
          c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int2 m = mem[c];
@@ -446,6 +777,7 @@ __global__ void k_restrict(int64_t nc, const int2 *__restrict__ mem, const doubl
 // out_i = in_i + (0.0 + x_c[agg_i]) (cycle.hpp:72-73: spmv(P, x_c) then axpy(1.0, ...)).
 __global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const double *xin,
                           const double *__restrict__ xc, double *xout) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         xout[i] = __dadd_rn(xin[i], __dadd_rn(0.0, xc[agg[i]]));
@@ -455,6 +787,7 @@ __global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const doub
 // per row, fixed shuffle tree).
 __global__ void k_coarse_gemv(int n, const double *__restrict__ inv, const double *__restrict__ f,
                               double *__restrict__ x) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (row >= n) return;
@@ -473,6 +806,7 @@ __global__ void k_coarse_gemv(int n, const double *__restrict__ inv, const doubl
 __global__ void k_coarse_lu_exact(int n, const double *__restrict__ lu, const int32_t *__restrict__ perm,
                                   const double *__restrict__ f, double *__restrict__ x) {
     extern __shared__ double y[];
+    pdl_wait();
     const int lane = threadIdx.x;
     for (int i = lane; i < n; i += 32) y[i] = f[perm[i]];
     __syncwarp();
@@ -676,6 +1010,12 @@ struct sb_ctx_s {
     int64_t h_pinned_n = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_solve_ms = 0.0;
+    int tail_from = 1 << 30;  // first level run inside the cluster tail kernel
+    int tail_ctas = 0;
+    int tail_smem = 0;
+    unsigned long long *trace = nullptr;  // SB_TAIL_TRACE=1: per-phase timestamps of the tail
+    bool pdl = true;                      // programmatic dependent launch in the V-cycle (SB_PDL=0 off)
+    sb::TailDesc *tail = nullptr;
     int launch_count = 0;  // kernels emitted by the last emit_* sequence
 };
 
@@ -718,80 +1058,143 @@ static CondSet conds(std::initializer_list<cudaGraphConditionalHandle> hs) {
     return cs;
 }
 
-// ---- launchers ---------------------------------------------------------------
+// ---- launchers (each counts the kernels it emits) -------------------------------
 
-template <int MODE, int NV>
-static void launch_csr(const DevLevel &l, cudaStream_t s, const double *x, const double *f, double *out,
-                       double omega, const int *skip, const Red &red) {
-    if (l.n == 0) return;
-    k_csr_tile<MODE, NV><<<std::min(l.ntiles, l.grid), kTileRows, l.smem, s>>>(
-        l.rp, l.ci, l.v, l.tiles, l.ntiles, x, f, out, omega, l.cap, skip, red);
-    CK(cudaGetLastError());
+// Launch with programmatic dependent launch (the kernel calls pdl_wait()
+// before touching its predecessor's outputs) when the context enables it.
+template <typename... KArgs, typename... Args>
+static void launch_k(sb_ctx c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args &&...args) {
+    ++c->launch_count;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = c->pdl ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
 
-static void launch_jacobi(const DevLevel &l, cudaStream_t s, const double *xin, const double *f, double *xout,
-                          double omega) {
-    launch_csr<M_JACOBI, 0>(l, s, xin, f, xout, omega, nullptr, Red{});
+template <int MODE, int NV>
+static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
+                       double *out, double omega, const int *skip, const Red &red, Aux aux = Aux{}) {
+    if (l.n == 0) return;
+    launch_k(c, k_csr_tile<MODE, NV>, dim3(std::min(l.ntiles, l.grid)), dim3(kTileRows), l.smem, s, l.rp, l.ci,
+             l.v, l.tiles, l.ntiles, x, f, out, omega, l.cap, skip, aux, red);
+}
+
+static void launch_jacobi(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *xin, const double *f,
+                          double *xout, double omega) {
+    launch_csr<M_JACOBI, 0>(c, l, s, xin, f, xout, omega, nullptr, Red{});
 }
 
 static void emit_coarse(sb_ctx c, cudaStream_t s, const double *f, double *x) {
-    ++c->launch_count;
     const int n = static_cast<int>(c->nc);
     if (c->coarse_exact)
-        k_coarse_lu_exact<<<1, 32, sizeof(double) * n, s>>>(n, c->lu, c->perm, f, x);
+        launch_k(c, k_coarse_lu_exact, dim3(1), dim3(32), sizeof(double) * n, s, n,
+                 static_cast<const double *>(c->lu), static_cast<const int32_t *>(c->perm), f, x);
     else
-        k_coarse_gemv<<<(n + 7) / 8, 256, 0, s>>>(n, c->inv, f, x);
-    CK(cudaGetLastError());
+        launch_k(c, k_coarse_gemv, dim3((n + 7) / 8), dim3(256), 0, s, n, static_cast<const double *>(c->inv), f,
+                 x);
+}
+
+static void emit_tail(sb_ctx c, cudaStream_t s, const Cyc &cp, const double *f, double *X) {
+    ++c->launch_count;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->tail_ctas, 1, 1);
+    cfg.blockDim = dim3(kTailThreads, 1, 1);
+    cfg.dynamicSmemBytes = static_cast<size_t>(c->tail_smem);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c->tail_ctas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = c->pdl ? 2 : 1;
+    CK(cudaLaunchKernelEx(&cfg, k_tail, static_cast<const TailDesc *>(c->tail), f, X, cp.omega, cp.pre, cp.post,
+                          c->trace));
 }
 
 // One V-cycle at level k (cycle.hpp:53-75), result written to X. T is the
 // level's ping-pong partner; the buffer plan makes the last post-sweep land
-// in X without copies.
+// in X without copies, and lets the first two pre-sweeps (from x = 0) and the
+// prolongation + first post-sweep run fused. Levels from
+// c->tail_from down run inside one cluster-resident kernel.
 static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const double *f, double *X,
                         bool zero) {
     const int L = static_cast<int>(c->L.size());
-    if (k + 1 == L) {
+    if (k + 1 == L && !(zero && k == c->tail_from)) {
         emit_coarse(c, s, f, X);
+        return;
+    }
+    if (zero && k == c->tail_from) {
+        emit_tail(c, s, cp, f, X);
         return;
     }
     const DevLevel &l = c->L[static_cast<size_t>(k)];
     double *T = l.t;
+    double *post_first = (cp.post >= 1) ? (((cp.post - 1) % 2 == 0) ? X : T) : X;
     double *cur = X, *other = T;
     if (zero) {
-        if (cp.pre >= 1) {
-            cur = ((cp.pre - 1) % 2 == 0) ? X : T;
+        double *pre_end = (cp.post >= 1) ? (post_first == X ? T : X) : X;
+        if (cp.pre == 0) {
+            CK(cudaMemsetAsync(pre_end, 0, sizeof(double) * static_cast<size_t>(l.n), s));
+            cur = pre_end;
+        } else {
+            const int writes = cp.pre >= 2 ? cp.pre - 1 : 1;
+            cur = (writes % 2 == 1) ? pre_end : (pre_end == X ? T : X);
             other = (cur == X) ? T : X;
-            k_jacobi_zero<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, f, l.diag, cur, cp.omega);
-            CK(cudaGetLastError());
-            c->launch_count += cp.pre;
-            for (int i = 1; i < cp.pre; ++i) {
-                launch_jacobi(l, s, cur, f, other, cp.omega);
+            if (cp.pre == 1) {
+                launch_k(c, k_jacobi_zero, dim3(vec_grid(l.n)), dim3(kVecThreads), 0, s, l.n, f,
+                         static_cast<const double *>(l.diag), cur, cp.omega);
+            } else {
+                launch_csr<M_JACOBI_ZERO, 0>(c, l, s, nullptr, f, cur, cp.omega, nullptr, Red{},
+                                             Aux{l.diag, nullptr, nullptr});
+            }
+            for (int i = 2; i < cp.pre; ++i) {
+                launch_jacobi(c, l, s, cur, f, other, cp.omega);
                 std::swap(cur, other);
             }
-        } else {
-            CK(cudaMemsetAsync(X, 0, sizeof(double) * static_cast<size_t>(l.n), s));
         }
     } else {
-        c->launch_count += cp.pre;
         for (int i = 0; i < cp.pre; ++i) {
-            launch_jacobi(l, s, cur, f, other, cp.omega);
+            launch_jacobi(c, l, s, cur, f, other, cp.omega);
             std::swap(cur, other);
         }
     }
-    c->launch_count += 3 + cp.post;  // residual, restriction, prolongation, post sweeps
     const DevLevel &lc = c->L[static_cast<size_t>(k) + 1];
-    launch_csr<M_RESID, 0>(l, s, cur, f, c->rs, 0.0, nullptr, Red{});
-    k_restrict<<<vec_grid(lc.n), kVecThreads, 0, s>>>(lc.n, l.mem, c->rs, lc.f);
-    CK(cudaGetLastError());
+    launch_csr<M_RESID, 0>(c, l, s, cur, f, c->rs, 0.0, nullptr, Red{});
+    launch_k(c, k_restrict, dim3(vec_grid(lc.n)), dim3(kVecThreads), 0, s, lc.n,
+             static_cast<const int2 *>(l.mem), static_cast<const double *>(c->rs), lc.f);
     emit_vcycle(c, s, cp, k + 1, lc.f, lc.x, true);
-    double *pout = (cp.post % 2 == 0) ? X : T;
-    k_prolong<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, l.agg, cur, lc.x, pout);
-    CK(cudaGetLastError());
-    cur = pout;
-    other = (pout == X) ? T : X;
-    for (int i = 0; i < cp.post; ++i) {
-        launch_jacobi(l, s, cur, f, other, cp.omega);
-        std::swap(cur, other);
+    if (cp.post >= 1 && cur != post_first) {
+        // x' = cur + P x_c folded into the first post-sweep's gathers
+        launch_csr<M_JACOBI_PROLONG, 0>(c, l, s, cur, f, post_first, cp.omega, nullptr, Red{},
+                                        Aux{l.diag, l.agg, lc.x});
+        cur = post_first;
+        other = (cur == X) ? T : X;
+        for (int i = 1; i < cp.post; ++i) {
+            launch_jacobi(c, l, s, cur, f, other, cp.omega);
+            std::swap(cur, other);
+        }
+    } else {
+        double *pout = (cp.post % 2 == 0) ? X : T;
+        launch_k(c, k_prolong, dim3(vec_grid(l.n)), dim3(kVecThreads), 0, s, l.n,
+                 static_cast<const int32_t *>(l.agg), static_cast<const double *>(cur),
+                 static_cast<const double *>(lc.x), pout);
+        cur = pout;
+        other = (pout == X) ? T : X;
+        for (int i = 0; i < cp.post; ++i) {
+            launch_jacobi(c, l, s, cur, f, other, cp.omega);
+            std::swap(cur, other);
+        }
     }
 }
 
@@ -869,7 +1272,7 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
                                               make_red(c, EP_PCG_RZ0, 1, nullptr, nullptr, conds({h_loop})));
         CK(cudaGetLastError());
         add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
-            launch_csr<M_SPMV, 1>(l0, s2, p, nullptr, Ap, 0.0, &c->st->done, make_red(c, EP_PCG_PAP, 1, p));
+            launch_csr<M_SPMV, 1>(c, l0, s2, p, nullptr, Ap, 0.0, &c->st->done, make_red(c, EP_PCG_PAP, 1, p));
             cudaGraphConditionalHandle h_vc = new_handle(s2);
             k_pcg_update<<<vb, kVecThreads, 0, s2>>>(
                 n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})));
@@ -884,7 +1287,7 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
         });
     });
     // true residual ||b - A x|| (krylov.hpp:116)
-    launch_csr<M_RESID, 1>(l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
+    launch_csr<M_RESID, 1>(c, l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
     return end_capture(c, g);
 }
 
@@ -912,7 +1315,7 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
         add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
             // (the loop is only entered / re-entered with done == 0)
             precond(s2, p, pt);
-            launch_csr<M_SPMV, 1>(l0, s2, pt, nullptr, Apt, 0.0, nullptr, make_red(c, EP_BI_DENOM, 1, rbar));
+            launch_csr<M_SPMV, 1>(c, l0, s2, pt, nullptr, Apt, 0.0, nullptr, make_red(c, EP_BI_DENOM, 1, rbar));
             cudaGraphConditionalHandle h_v2 = new_handle(s2);
             k_bi_s<<<vb, kVecThreads, 0, s2>>>(n, r, Apt, sv,
                                               make_red(c, EP_BI_SN, 1, nullptr, nullptr, conds({h_v2})));
@@ -921,7 +1324,7 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
             CK(cudaGetLastError());
             add_cond(c, s2, d2, h_v2, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
                 precond(s3, sv, stv);
-                launch_csr<M_SPMV, 2>(l0, s3, stv, nullptr, Ast, 0.0, nullptr,
+                launch_csr<M_SPMV, 2>(c, l0, s3, stv, nullptr, Ast, 0.0, nullptr,
                                       make_red(c, EP_BI_AS, 2, nullptr, sv));
                 k_bi_update<<<vb, kVecThreads, 0, s3>>>(n, x, r, pt, stv, sv, Ast, rbar,
                                                        make_red(c, EP_BI_RN_RHO, 2));
@@ -933,7 +1336,7 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
             CK(cudaGetLastError());
         });
     });
-    launch_csr<M_RESID, 1>(l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
+    launch_csr<M_RESID, 1>(c, l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
     return end_capture(c, g);
 }
 
@@ -950,7 +1353,7 @@ static cudaGraph_t build_amg(sb_ctx c, const Cyc &cp, const double *b, double *x
     CK(cudaGetLastError());
     add_cond(c, s, 0, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s1, int) {
         emit_vcycle(c, s1, cp, 0, b, x, false);
-        launch_csr<M_RESID, 1>(l0, s1, x, b, c->rs, 0.0, nullptr,
+        launch_csr<M_RESID, 1>(c, l0, s1, x, b, c->rs, 0.0, nullptr,
                                make_red(c, EP_AMG_RN, 1, nullptr, nullptr, conds({h_loop})));
     });
     return end_capture(c, g);
@@ -959,7 +1362,7 @@ static cudaGraph_t build_amg(sb_ctx c, const Cyc &cp, const double *b, double *x
 // ---- context creation ----------------------------------------------------------
 
 static void make_tiles(const HostCsr &A, std::vector<int32_t> &tiles, int &cap) {
-    constexpr int64_t kCapMax = 8192;  // staged nnz per tile (96 KB of smem)
+    constexpr int64_t kCapMax = 4096;  // staged nnz per tile (49 KB per pipeline stage)
     tiles.assign(1, 0);
     cap = 0;
     int64_t r = 0;
@@ -1012,7 +1415,7 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
     CK(cudaMemcpy(D.tiles, tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice));
     const size_t cap_v = static_cast<size_t>((D.cap + 3) & ~1);
     const size_t cap_c = static_cast<size_t>((D.cap + 11) & ~3);
-    D.smem = 2 * (cap_v * 8 + cap_c * 4);  // two pipeline stages
+    D.smem = kStages * (cap_v * 8 + cap_c * 4);  // pipeline stages
     if (!coarsest) {
         D.nc = H.n_coarse;
         D.agg = dalloc<int32_t>(c, A.n);
@@ -1061,6 +1464,123 @@ static Cyc check_cycle(sb_ctx c, const sb_cycle *cp, const char *who) {
                                        std::to_string(c->L[k].bad_diag));
     if (c->nc <= 0) throw invalid_argument(std::string(who) + ": hierarchy has no coarse factorization");
     return y;
+}
+
+// Chooses the cluster-resident tail: starting from the coarsest level, adds
+// finer levels while each CTA's block of every tail level (CSR slice, diag,
+// aggregates, members, 4 vectors) plus its rows of the coarse inverse fit in
+// shared memory. SB_TAIL_ROWS caps the finest tail level (0 disables; default
+// 1<<20). Disabled in the bit-exact coarse mode.
+static void setup_tail(sb_ctx c, const Hier &H) {
+    const int L = static_cast<int>(c->L.size());
+    c->tail_from = 1 << 30;
+    const char *env = std::getenv("SB_TAIL_ROWS");
+    const long long tail_rows = env ? std::atoll(env) : (1ll << 20);
+    if (tail_rows <= 0 || c->nc <= 0 || c->coarse_exact) return;
+    CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    int dev_smem = 0;
+    CK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    const int budget = dev_smem - static_cast<int>(sizeof(TailDesc)) - 1024;
+    int ctas = 0;
+    for (int want : {16, 8}) {
+        CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(want, 1, 1);
+        cfg.blockDim = dim3(kTailThreads, 1, 1);
+        cfg.dynamicSmemBytes = budget;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = want;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, k_tail, &cfg) == cudaSuccess && nclusters > 0) {
+            ctas = want;
+            break;
+        }
+        cudaGetLastError();
+    }
+    if (ctas == 0) return;
+    auto align16 = [](int x) { return (x + 15) & ~15; };
+    // per-level block sizes (bytes) for a given start level
+    auto level_bytes = [&](int k, int &rows_per, int &nnz_cap) {
+        const HostLevel &hl = H.levels[static_cast<size_t>(k)];
+        rows_per = static_cast<int>((hl.A.n + ctas - 1) / ctas);
+        nnz_cap = 0;
+        for (int r = 0; r < ctas; ++r) {
+            const int64_t a = std::min<int64_t>(hl.A.n, static_cast<int64_t>(r) * rows_per);
+            const int64_t b = std::min<int64_t>(hl.A.n, static_cast<int64_t>(r + 1) * rows_per);
+            nnz_cap = std::max<int>(nnz_cap, static_cast<int>(hl.A.rp[b] - hl.A.rp[a]));
+        }
+        return align16(4 * (rows_per + 1)) + align16(4 * nnz_cap) + align16(8 * nnz_cap) +
+               align16(8 * rows_per) * 6 /* diag x t f r + agg(4) mem(8/2) */;
+    };
+    const int nc = static_cast<int>(c->nc);
+    const int rows_c = (nc + ctas - 1) / ctas;
+    int total = align16(8 * rows_c * nc) + align16(8 * nc) + align16(8 * rows_c) * 2;
+    int k0 = L - 1;
+    while (k0 > 0) {
+        int rp_, nz_;
+        const int add = level_bytes(k0 - 1, rp_, nz_);
+        if (total + add > budget || c->L[static_cast<size_t>(k0) - 1].n > tail_rows ||
+            L - (k0 - 1) > kTailMaxLevels)
+            break;
+        total += add;
+        --k0;
+    }
+    TailDesc d;
+    std::memset(&d, 0, sizeof(d));
+    d.nlev = L - k0;
+    d.ncoarse = nc;
+    d.inv = c->inv;
+    int off = 0;
+    auto take = [&](int bytes) {
+        const int o = off;
+        off += align16(bytes);
+        return o;
+    };
+    for (int q = 0; q < d.nlev; ++q) {
+        const int k = k0 + q;
+        const DevLevel &l = c->L[static_cast<size_t>(k)];
+        TailLevel &t = d.L[q];
+        t.n = static_cast<int>(l.n);
+        t.nc = static_cast<int>(l.nc);
+        t.rp = l.rp;
+        t.ci = l.ci;
+        t.agg = l.agg;
+        t.v = l.v;
+        t.diag = l.diag;
+        t.mem = l.mem;
+        if (q + 1 < d.nlev) {
+            level_bytes(k, t.rows_per, t.nnz_cap);
+            t.o_rp = take(4 * (t.rows_per + 1));
+            t.o_ci = take(4 * t.nnz_cap);
+            t.o_v = take(8 * t.nnz_cap);
+            t.o_diag = take(8 * t.rows_per);
+            t.o_agg = take(4 * t.rows_per);
+            t.o_x = take(8 * t.rows_per);
+            t.o_t = take(8 * t.rows_per);
+            t.o_f = take(8 * t.rows_per);
+            t.o_r = take(8 * t.rows_per);
+        } else {
+            t.rows_per = rows_c;
+            t.o_x = take(8 * rows_c);
+            t.o_f = take(8 * rows_c);
+        }
+    }
+    for (int q = 0; q + 1 < d.nlev; ++q) d.L[q].o_mem = take(8 * d.L[q + 1].rows_per);
+    d.o_inv = take(8 * rows_c * nc);
+    d.o_fc = take(8 * nc);
+    d.smem_bytes = off;
+    if (off > budget) return;  // (should not happen: sized above)
+    c->tail = dalloc<TailDesc>(c, 1, false);
+    CK(cudaMemcpy(c->tail, &d, sizeof(d), cudaMemcpyHostToDevice));
+    c->tail_ctas = ctas;
+    c->tail_from = k0;
+    c->tail_smem = off;
+    if (std::getenv("SB_TAIL_TRACE")) c->trace = dalloc<unsigned long long>(c, 256, false);
 }
 
 static std::string key_of(const char *kind, const Cyc *cp, const void *b, const void *x, const void *h) {
@@ -1221,6 +1741,7 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
         c = new sb_ctx_s;
         c->device = o.device;
         c->graphs = o.use_graphs != 0;
+        if (const char *e = std::getenv("SB_PDL")) c->pdl = std::atoi(e) != 0;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         CK(cudaEventCreate(&c->ev0));
         CK(cudaEventCreate(&c->ev1));
@@ -1239,6 +1760,8 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
         set_smem_attr<M_RESID, 0>(max_smem);
         set_smem_attr<M_RESID, 1>(max_smem);
         set_smem_attr<M_JACOBI, 0>(max_smem);
+        set_smem_attr<M_JACOBI_ZERO, 0>(max_smem);
+        set_smem_attr<M_JACOBI_PROLONG, 0>(max_smem);
         int nsm = 0;
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
         for (auto &l : c->L) {
@@ -1259,6 +1782,7 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
             }
         }
         c->rs = dalloc<double>(c, n0);
+        setup_tail(c, *h);
         for (auto &v : c->kv) v = dalloc<double>(c, n0);
         int maxb = 148 * 8;
         for (auto &l : c->L) maxb = std::max(maxb, l.ntiles);
@@ -1306,10 +1830,12 @@ int sb_vcycle(sb_ctx c, const sb_cycle *cp, int level, const double *f, double *
         const DevLevel &l = level_of(c, level);
         const Cyc y = check_cycle(c, cp, "vcycle");
         double *df = c->kv[KB], *dx = c->kv[KX];
+        bool zero = true;  // an all-zero initial guess takes the preconditioner path
+        for (int64_t i = 0; i < l.n && zero; ++i) zero = (x[i] == 0.0 && !std::signbit(x[i]));
         with_dev(c, [&](cudaStream_t s) {
             h2d(c, df, f, l.n);
             h2d(c, dx, x, l.n);
-            emit_vcycle(c, s, y, level, df, dx, false);
+            emit_vcycle(c, s, y, level, df, dx, zero);
             d2h(c, x, dx, l.n);
         });
     });
@@ -1337,6 +1863,24 @@ int sb_pbicgstab_dev(sb_ctx c, const sb_cycle *cp, const double *d_b, double *d_
 }
 
 double sb_last_solve_ms(sb_ctx c) { return c ? c->last_solve_ms : 0.0; }
+
+// Diagnostics: copies the tail kernel's phase timestamps (SB_TAIL_TRACE=1) into
+// out (count first); returns the number of entries, or -1 if tracing is off.
+int sb_tail_trace(sb_ctx c, unsigned long long *out, int cap) {
+    if (!c || !c->trace) return -1;
+    unsigned long long buf[256];
+    if (cudaMemcpy(buf, c->trace, sizeof(buf), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    const int n = static_cast<int>(std::min<unsigned long long>(buf[0], 255));
+    for (int i = 0; i < n && i < cap; ++i) out[i] = buf[1 + i];
+    return n;
+}
+int sb_tail_info(sb_ctx c, int *tail_from, int *ctas, int *smem) {
+    if (!c) return SB_EINVAL;
+    *tail_from = c->tail_from;
+    *ctas = c->tail_ctas;
+    *smem = c->tail_smem;
+    return SB_OK;
+}
 
 int sb_vcycle_launches(sb_ctx c, const sb_cycle *cp) {
     int out = 0;
@@ -1366,20 +1910,31 @@ int sb_time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int reps, 
         k_fill<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, x, 0.5);
         k_fill<<<vec_grid(l.n), kVecThreads, 0, s>>>(l.n, t, 0.5);
         CK(cudaGetLastError());
+        cudaGraphExec_t vgraph = nullptr;
+        int vlaunch = 0;
         auto once = [&]() {
             c->launch_count = 0;
             if (kind == 0) {
-                launch_jacobi(l, s, x, f, t, y.omega);
+                launch_jacobi(c, l, s, x, f, t, y.omega);
                 std::swap(x, t);
-                c->launch_count = 1;
             } else if (kind == 1) {
-                launch_csr<M_SPMV, 0>(l, s, x, nullptr, t, 0.0, nullptr, Red{});
-                c->launch_count = 1;
+                launch_csr<M_SPMV, 0>(c, l, s, x, nullptr, t, 0.0, nullptr, Red{});
             } else if (kind == 2) {
-                launch_csr<M_RESID, 0>(l, s, x, f, t, 0.0, nullptr, Red{});
-                c->launch_count = 1;
+                launch_csr<M_RESID, 0>(c, l, s, x, f, t, 0.0, nullptr, Red{});
             } else if (kind == 3) {
                 emit_vcycle(c, s, y, level, f, t, true);
+            } else if (kind == 4) {
+                if (!vgraph) {
+                    cudaGraph_t g = begin_capture(c);
+                    c->launch_count = 0;
+                    emit_vcycle(c, s, y, level, f, t, true);
+                    vlaunch = c->launch_count;
+                    end_capture(c, g);
+                    CK(cudaGraphInstantiate(&vgraph, g, 0));
+                    cudaGraphDestroy(g);
+                }
+                CK(cudaGraphLaunch(vgraph, s));
+                c->launch_count = vlaunch;
             } else {
                 throw invalid_argument("sb_time_kernel: unknown kind");
             }
@@ -1393,6 +1948,7 @@ int sb_time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int reps, 
         CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
         if (avg_ms) *avg_ms = ms / reps;
         if (launches) *launches = c->launch_count;
+        if (vgraph) cudaGraphExecDestroy(vgraph);
     });
 }
 
@@ -1401,7 +1957,7 @@ int sb_spmv(sb_ctx c, int level, const double *x, double *y) {
         const DevLevel &l = level_of(c, level);
         with_dev(c, [&](cudaStream_t s) {
             h2d(c, c->kv[KP], x, l.n);
-            launch_csr<M_SPMV, 0>(l, s, c->kv[KP], nullptr, c->kv[KAP], 0.0, nullptr, Red{});
+            launch_csr<M_SPMV, 0>(c, l, s, c->kv[KP], nullptr, c->kv[KAP], 0.0, nullptr, Red{});
             d2h(c, y, c->kv[KAP], l.n);
         });
     });
@@ -1424,7 +1980,7 @@ int sb_smooth(sb_ctx c, int level, const sb_cycle *cp, double *x, const double *
             h2d(c, a, x, l.n);
             h2d(c, df, f, l.n);
             for (int i = 0; i < sweeps; ++i) {
-                launch_jacobi(l, s, a, df, b, cp->omega);
+                launch_jacobi(c, l, s, a, df, b, cp->omega);
                 std::swap(a, b);
             }
             d2h(c, x, a, l.n);
@@ -1438,7 +1994,7 @@ int sb_residual(sb_ctx c, int level, const double *x, const double *f, double *r
         with_dev(c, [&](cudaStream_t s) {
             h2d(c, c->kv[KX], x, l.n);
             h2d(c, c->kv[KB], f, l.n);
-            launch_csr<M_RESID, 0>(l, s, c->kv[KX], c->kv[KB], c->kv[KR], 0.0, nullptr, Red{});
+            launch_csr<M_RESID, 0>(c, l, s, c->kv[KX], c->kv[KB], c->kv[KR], 0.0, nullptr, Red{});
             d2h(c, r, c->kv[KR], l.n);
         });
     });

@@ -19,8 +19,12 @@ def _cp(sp, pre=6, post=6, omega=2.0 / 3.0):
     lambda sp: sp.poisson3d(32), lambda sp: sp.aniso3d(24), lambda sp: sp.poisson2d(96, 80),
     lambda sp: sp.convdiff3d(16, 16, 16, 1.0, 100.0, 1.0, 1.0), lambda sp: sp.poisson3d_27(12),
     lambda sp: random_spd(sp, 300, 7, 0.05)])
-@pytest.mark.parametrize("sweeps", [(6, 6), (1, 2), (0, 3), (2, 0)])
-def test_vcycle_matches_oracle(sp, port, mk, sweeps):
+@pytest.mark.parametrize("sweeps", [(6, 6), (1, 2), (0, 3), (2, 0), (3, 5)])
+@pytest.mark.parametrize("tail_rows", ["0", "2000", "32768"])
+def test_vcycle_matches_oracle(sp, port, mk, sweeps, tail_rows, monkeypatch):
+    # SB_TAIL_ROWS=0: every level as separate kernels; otherwise the small
+    # levels run inside the cluster-resident tail kernel
+    monkeypatch.setenv("SB_TAIL_ROWS", tail_rows)
     A = mk(sp)
     h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40, coarse_target=min(500, A.nrows() // 4)))
     o = port.hierarchy(A, min(500, A.nrows() // 4), 40)
@@ -29,6 +33,8 @@ def test_vcycle_matches_oracle(sp, port, mk, sweeps):
     f = sp.rhs_random(A.nrows(), 42)
     got = sp.vcycle(h, 0, f, np.zeros(A.nrows()), cp)
     assert rel(got, o.vcycle(f, np.zeros(A.nrows()))) < 1e-12
+    # the preconditioner path (x = 0 promise, fused first sweeps, tail)
+    assert rel(sp.make_amg_preconditioner(h, cp).apply(f), o.vcycle(f, np.zeros(A.nrows()))) < 1e-12
     x0 = np.random.default_rng(1).uniform(-1, 1, A.nrows())  # general initial guess
     assert rel(sp.vcycle(h, 0, f, x0, cp), o.vcycle(f, x0)) < 1e-12
 
@@ -79,3 +85,15 @@ def test_vcycle_rejects(sp):
         sp.vcycle(h, 0, np.ones(255), np.zeros(256), _cp(sp))
     with pytest.raises(sp.InvalidArgument, match="Jacobi"):
         sp.vcycle(h, 0, np.ones(256), np.zeros(256), sp.CycleParams())  # GS default: rejected
+
+
+@pytest.mark.parametrize("tail_rows", ["0", "32768"])
+def test_vcycle_bitexact_with_exact_coarse(sp, port, tail_rows, monkeypatch):
+    # with the reference-order coarse substitution every level is bitwise the
+    # reference's (the tail is disabled in that mode)
+    monkeypatch.setenv("SB_TAIL_ROWS", tail_rows)
+    A = sp.poisson3d(24)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40), coarse_exact=True)
+    o = port.hierarchy(A, 500, 40)
+    f = sp.rhs_random(A.nrows(), 3)
+    assert np.array_equal(sp.vcycle(h, 0, f, np.zeros(A.nrows()), _cp(sp)), o.vcycle(f, np.zeros(A.nrows())))
