@@ -355,6 +355,8 @@ __device__ __forceinline__ double row_eval(int row, int rs, int re, const int32_
                                            const double *x, const double *f, double fi, const Aux &aux,
                                            double omega) {
     double sum = 0.0, d = 0.0;
+    double xi = 0.0;  // own iterate, loaded up front so its latency overlaps the row
+    if constexpr (MODE >= M_JACOBI) xi = xval<MODE, CG>(row, x, f, aux, omega);
     for (int k = rs; k < re; k += U) {
         int c[U];
         double a[U], xv[U];
@@ -376,10 +378,7 @@ __device__ __forceinline__ double row_eval(int row, int rs, int re, const int32_
     }
     if constexpr (MODE == M_SPMV) return sum;
     else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
-    else {
-        const double xi = xval<MODE, CG>(row, x, f, aux, omega);
-        return __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
-    }
+    else return __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
 }
 
 // Persistent, double-buffered CSR tile pipeline. Tiles of <= 256 consecutive
@@ -390,7 +389,19 @@ __device__ __forceinline__ double row_eval(int row, int rs, int re, const int32_
 // HBM streaming overlaps the x-gathers and arithmetic. Thread t owns row
 // r0 + t and walks it in CSR order from shared memory. A tile whose nnz exceed
 // the stage capacity (a single very long row) reads straight from global.
-constexpr int kStages = 3;  // TMA pipeline depth (tiles in flight per CTA)
+constexpr int kStages = 3;      // TMA pipeline depth (tiles in flight per CTA)
+constexpr int kRpWin = 264;     // staged row-pointer window (ints): 256 + 1 + alignment
+constexpr int kFWin = 258;      // staged f window (doubles): 256 + alignment
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Stage layout: [values cap_v f64][cols cap_c i32][rp kRpWin i32][f kFWin f64]
+__host__ __device__ __forceinline__ size_t stage_bytes_of(int cap) {
+    return static_cast<size_t>((cap + 3) & ~1) * 8 + static_cast<size_t>((cap + 11) & ~3) * 4 +
+           static_cast<size_t>(kRpWin) * 4 + static_cast<size_t>(kFWin) * 8;
+}
 
 template <int MODE, int NV>
 __global__ void __launch_bounds__(kTileRows, 3)
@@ -399,7 +410,8 @@ __global__ void __launch_bounds__(kTileRows, 3)
                const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out,
                double omega, int cap, const int *skip, Aux aux, Red red) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar[kStages];
+    __shared__ __align__(8) uint64_t full[kStages];
+    __shared__ __align__(8) uint64_t empty[kStages];
     __shared__ int4 hdr[kStages];
     double acc[NV > 0 ? NV : 1];
 #pragma unroll
@@ -407,84 +419,98 @@ __global__ void __launch_bounds__(kTileRows, 3)
 
     const int cap_v = (cap + 3) & ~1;   // doubles per stage
     const int cap_c = (cap + 11) & ~3;  // ints per stage
-    const size_t stage_bytes = static_cast<size_t>(cap_v) * 8 + static_cast<size_t>(cap_c) * 4;
+    const size_t sb = stage_bytes_of(cap);
+    const size_t o_c = static_cast<size_t>(cap_v) * 8;
+    const size_t o_rp = o_c + static_cast<size_t>(cap_c) * 4;
+    const size_t o_f = o_rp + static_cast<size_t>(kRpWin) * 4;
+    constexpr int kWarps = kTileRows / 32;
 
-    // thread 0: stage tile t into buffer s (matrix data only: constant, so it
-    // may be issued before the programmatic-dependency wait)
-    auto issue = [&](int t, int s) {
+    // thread 0: stage tile t into buffer s. Matrix data (values, columns, row
+    // pointers) is constant and may be issued before the dependency wait;
+    // with_f adds the rhs window (a predecessor output) once that wait is done.
+    auto issue = [&](int t, int s, bool with_f) {
         const int r0 = tile_ptr[t], r1 = tile_ptr[t + 1];
         const int e0 = rp[r0], e1 = rp[r1];
         hdr[s] = make_int4(r0, r1, e0, e1);
-        double *sv = reinterpret_cast<double *>(smem + s * stage_bytes);
-        int32_t *sc = reinterpret_cast<int32_t *>(smem + s * stage_bytes + static_cast<size_t>(cap_v) * 8);
-        if (e1 - e0 <= cap && e1 > e0) {
-            const int va0 = e0 & ~1, ca0 = e0 & ~3;
-            const uint32_t vbytes = static_cast<uint32_t>(((e1 + 1) & ~1) - va0) * 8u;
-            const uint32_t cbytes = static_cast<uint32_t>(((e1 + 3) & ~3) - ca0) * 4u;
-            mbar_expect_tx(&bar[s], vbytes + cbytes);
-            bulk_g2s(sv, val + va0, vbytes, &bar[s]);
-            bulk_g2s(sc, ci + ca0, cbytes, &bar[s]);
-        } else {
-            mbar_expect_tx(&bar[s], 0);  // plain arrive: nothing staged
-        }
+        unsigned char *st = smem + s * sb;
+        uint32_t bytes = 0;
+        const bool staged = e1 - e0 <= cap && e1 > e0;
+        const int va0 = e0 & ~1, ca0 = e0 & ~3, ra0 = r0 & ~3, fa0 = r0 & ~1;
+        const uint32_t vbytes = staged ? static_cast<uint32_t>(((e1 + 1) & ~1) - va0) * 8u : 0u;
+        const uint32_t cbytes = staged ? static_cast<uint32_t>(((e1 + 3) & ~3) - ca0) * 4u : 0u;
+        const uint32_t rbytes = static_cast<uint32_t>(((r1 + 1 + 3) & ~3) - ra0) * 4u;
+        const uint32_t fbytes = (MODE != M_SPMV && with_f) ? static_cast<uint32_t>((r1 & ~1) - fa0) * 8u : 0u;
+        bytes = vbytes + cbytes + rbytes + fbytes;
+        mbar_expect_tx(&full[s], bytes);
+        if (vbytes) bulk_g2s(st, val + va0, vbytes, &full[s]);
+        if (cbytes) bulk_g2s(st + o_c, ci + ca0, cbytes, &full[s]);
+        bulk_g2s(st + o_rp, rp + ra0, rbytes, &full[s]);
+        if (fbytes) bulk_g2s(st + o_f, f + fa0, fbytes, &full[s]);
     };
 
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int q = 0; q < kStages; ++q) mbar_init(&bar[q], 1);
+        for (int q = 0; q < kStages; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], kWarps);
+        }
         fence_mbar_init();
     }
     __syncthreads();
     const int G = static_cast<int>(gridDim.x);
-    int issued = 0;
+    const int b = static_cast<int>(blockIdx.x);
+    // prologue tiles go out before the dependency wait WITHOUT f; their f rows
+    // are read from global after the wait (flag below)
     if (threadIdx.x == 0)
         for (int q = 0; q < kStages - 1; ++q)
-            if (static_cast<int>(blockIdx.x) + q * G < ntiles) {
-                issue(static_cast<int>(blockIdx.x) + q * G, q);
-                ++issued;
-            }
-    pdl_wait();  // predecessor kernel complete: x, f (and skip) are final
+            if (b + q * G < ntiles) issue(b + q * G, q, false);
+    pdl_wait();  // predecessor complete: x, f (and skip) are final
     const bool active = !(skip && *skip);
     if (!active) {  // skipped (solve already finished): drain the prologue's copies
         for (int q = 0; q < kStages - 1; ++q)
-            if (static_cast<int>(blockIdx.x) + q * G < ntiles) mbar_wait(&bar[q], 0u);
+            if (b + q * G < ntiles) mbar_wait(&full[q], 0u);
         pdl_trigger();
     } else {
-        uint32_t phases = 0u;  // bit s = parity of stage s
-        int s = 0;
-        for (int t = blockIdx.x; t < ntiles; t += G, s = (s + 1 == kStages) ? 0 : s + 1) {
+        uint32_t fph = 0u, eph = 0u;  // parities of full[] (all threads) / empty[] (thread 0)
+        int s = 0, it = 0;
+        const int lane = threadIdx.x & 31;
+        for (int t = b; t < ntiles; t += G, ++it, s = (s + 1 == kStages) ? 0 : s + 1) {
             if (t + G >= ntiles) pdl_trigger();  // last tile of this CTA: let the next kernel launch
             const int tn = t + (kStages - 1) * G;
             const int sn = (s + kStages - 1) % kStages;
-            if (threadIdx.x == 0 && tn < ntiles) issue(tn, sn);
-            // per-row operands, loaded before waiting on the stage
-            const int r0g = tile_ptr[t], r1g = tile_ptr[t + 1];
-            const int row = r0g + static_cast<int>(threadIdx.x);
-            int rs = 0, re = 0;
-            double fi = 0.0;
-            if (row < r1g) {
-                rs = rp[row];
-                re = rp[row + 1];
-                if (MODE != M_SPMV) fi = f[row];
+            if (threadIdx.x == 0 && tn < ntiles) {
+                if (it >= 1) {  // stage sn was consumed in iteration it-1
+                    mbar_wait(&empty[sn], (eph >> sn) & 1u);
+                    eph ^= 1u << sn;
+                }
+                issue(tn, sn, true);
             }
-            mbar_wait(&bar[s], (phases >> s) & 1u);
-            phases ^= 1u << s;
+            mbar_wait(&full[s], (fph >> s) & 1u);
+            fph ^= 1u << s;
             const int4 h = hdr[s];
-            const bool staged = (h.w - h.z) <= cap;
-            if (row < r1g) {
-                const int32_t *cc = staged
-                    ? reinterpret_cast<const int32_t *>(smem + s * stage_bytes + static_cast<size_t>(cap_v) * 8) - (h.z & ~3)
-                    : ci;
-                const double *vv = staged ? reinterpret_cast<const double *>(smem + s * stage_bytes) - (h.z & ~1) : val;
+            const int r0 = h.x, r1 = h.y;
+            const int row = r0 + static_cast<int>(threadIdx.x);
+            const unsigned char *st = smem + s * sb;
+            if (row < r1) {
+                const int32_t *srp = reinterpret_cast<const int32_t *>(st + o_rp) - (r0 & ~3);
+                const int rs = srp[row], re = srp[row + 1];
+                double fi = 0.0;
+                if (MODE != M_SPMV) {
+                    const bool f_staged = it >= kStages - 1 && row < (r1 & ~1);
+                    fi = f_staged ? reinterpret_cast<const double *>(st + o_f)[row - (r0 & ~1)] : f[row];
+                }
+                const bool staged = (h.w - h.z) <= cap;
+                const int32_t *cc = staged ? reinterpret_cast<const int32_t *>(st + o_c) - (h.z & ~3) : ci;
+                const double *vv = staged ? reinterpret_cast<const double *>(st) - (h.z & ~1) : val;
                 const double o = row_eval<MODE, false>(row, rs, re, cc, vv, x, f, fi, aux, omega);
                 out[row] = o;
                 if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row] : o);
                 if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
             }
-            __syncthreads();  // stage s fully consumed before it is refilled
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
         }
     }
-    (void)issued;
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
 }
 
@@ -1388,7 +1414,7 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
     D.nnz = A.nnz();
     std::vector<int32_t> rp32(static_cast<size_t>(A.n) + 1);
     for (int64_t i = 0; i <= A.n; ++i) rp32[i] = static_cast<int32_t>(A.rp[i]);
-    D.rp = dalloc<int32_t>(c, A.n + 1);
+    D.rp = dalloc<int32_t>(c, A.n + 1 + 8);  // + slack for 16-byte TMA windows
     D.ci = dalloc<int32_t>(c, A.nnz() + 8);
     D.v = dalloc<double>(c, A.nnz() + 2);
     CK(cudaMemcpy(D.rp, rp32.data(), sizeof(int32_t) * rp32.size(), cudaMemcpyHostToDevice));
@@ -1413,9 +1439,7 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
     D.ntiles = static_cast<int>(tiles.size()) - 1;
     D.tiles = dalloc<int32_t>(c, static_cast<int64_t>(tiles.size()));
     CK(cudaMemcpy(D.tiles, tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice));
-    const size_t cap_v = static_cast<size_t>((D.cap + 3) & ~1);
-    const size_t cap_c = static_cast<size_t>((D.cap + 11) & ~3);
-    D.smem = kStages * (cap_v * 8 + cap_c * 4);  // pipeline stages
+    D.smem = kStages * stage_bytes_of(D.cap);  // pipeline stages
     if (!coarsest) {
         D.nc = H.n_coarse;
         D.agg = dalloc<int32_t>(c, A.n);
