@@ -348,12 +348,29 @@ __device__ __forceinline__ double xval(int j, const double *x, const double *f, 
         return ldv<CG>(x + j);
 }
 
+// Matrix entry storage formats (per level, chosen at upload):
+//   VF 0: f64 values; 1: uint8 index into a <=256-entry dictionary of the
+//         level's distinct values (exact doubles: lossless)
+//   CF 0: int32 columns; 1: int16 column - row deltas (when every |delta| fits)
+template <int VF, int CF> struct Ent {
+    const void *vals;
+    const void *cols;
+    const double *dict;
+    __device__ __forceinline__ int col(int k, int row) const {
+        if constexpr (CF == 1) return row + static_cast<int>(static_cast<const int16_t *>(cols)[k]);
+        else return static_cast<const int32_t *>(cols)[k];
+    }
+    __device__ __forceinline__ double val(int k) const {
+        if constexpr (VF == 1) return dict[static_cast<const uint8_t *>(vals)[k]];
+        else return static_cast<const double *>(vals)[k];
+    }
+};
+
 // One row in the reference's order: sum = 0.0; sum += a_k * x_{c_k} for k in
-// CSR order (no FMA), then the mode's epilogue. cc / vv index the row's entries.
-template <int MODE, bool CG, int U = 8>
-__device__ __forceinline__ double row_eval(int row, int rs, int re, const int32_t *cc, const double *vv,
-                                           const double *x, const double *f, double fi, const Aux &aux,
-                                           double omega) {
+// CSR order (no FMA), then the mode's epilogue.
+template <int MODE, bool CG, int U = 8, typename E>
+__device__ __forceinline__ double row_eval(int row, int rs, int re, const E &e, const double *x,
+                                           const double *f, double fi, const Aux &aux, double omega) {
     double sum = 0.0, d = 0.0;
     double xi = 0.0;  // own iterate, loaded up front so its latency overlaps the row
     if constexpr (MODE >= M_JACOBI) xi = xval<MODE, CG>(row, x, f, aux, omega);
@@ -363,8 +380,8 @@ __device__ __forceinline__ double row_eval(int row, int rs, int re, const int32_
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (k + u < re) {
-                c[u] = cc[k + u];
-                a[u] = vv[k + u];
+                c[u] = e.col(k + u, row);
+                a[u] = e.val(k + u);
             }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -397,33 +414,44 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Stage layout: [values cap_v f64][cols cap_c i32][rp kRpWin i32][f kFWin f64]
-__host__ __device__ __forceinline__ size_t stage_bytes_of(int cap) {
-    return static_cast<size_t>((cap + 3) & ~1) * 8 + static_cast<size_t>((cap + 11) & ~3) * 4 +
-           static_cast<size_t>(kRpWin) * 4 + static_cast<size_t>(kFWin) * 8;
+// Stage layout: [values][cols][rp kRpWin i32][f kFWin f64], each a 16-byte
+// aligned window; sizes depend on the level's storage format.
+__host__ __device__ __forceinline__ size_t stage_vbytes(int cap, int vf) {
+    return vf ? static_cast<size_t>((cap + 31) & ~15) : static_cast<size_t>((cap + 3) & ~1) * 8;
+}
+__host__ __device__ __forceinline__ size_t stage_cbytes(int cap, int cf) {
+    return cf ? static_cast<size_t>((cap + 15) & ~7) * 2 : static_cast<size_t>((cap + 11) & ~3) * 4;
+}
+__host__ __device__ __forceinline__ size_t stage_bytes_of(int cap, int vf, int cf) {
+    return stage_vbytes(cap, vf) + stage_cbytes(cap, cf) + static_cast<size_t>(kRpWin) * 4 +
+           static_cast<size_t>(kFWin) * 8;
 }
 
-template <int MODE, int NV>
+template <int MODE, int NV, int VF, int CF>
 __global__ void __launch_bounds__(kTileRows, 3)
-    k_csr_tile(const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-               const double *__restrict__ val, const int32_t *__restrict__ tile_ptr, int ntiles,
+    k_csr_tile(const int32_t *__restrict__ rp, const void *__restrict__ cols, const void *__restrict__ vals,
+               const double *__restrict__ dict, int ndict, const int32_t *__restrict__ tile_ptr, int ntiles,
                const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out,
                double omega, int cap, const int *skip, Aux aux, Red red) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) uint64_t full[kStages];
     __shared__ __align__(8) uint64_t empty[kStages];
     __shared__ int4 hdr[kStages];
+    __shared__ double sdict[VF ? 256 : 1];
     double acc[NV > 0 ? NV : 1];
 #pragma unroll
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
 
-    const int cap_v = (cap + 3) & ~1;   // doubles per stage
-    const int cap_c = (cap + 11) & ~3;  // ints per stage
-    const size_t sb = stage_bytes_of(cap);
-    const size_t o_c = static_cast<size_t>(cap_v) * 8;
-    const size_t o_rp = o_c + static_cast<size_t>(cap_c) * 4;
+    constexpr int VB = VF ? 1 : 8;  // bytes per value / column entry
+    constexpr int CB = CF ? 2 : 4;
+    constexpr int VA = 16 / VB, CA = 16 / CB;  // entries per 16-byte granule
+    const size_t sb = stage_bytes_of(cap, VF, CF);
+    const size_t o_c = stage_vbytes(cap, VF);
+    const size_t o_rp = o_c + stage_cbytes(cap, CF);
     const size_t o_f = o_rp + static_cast<size_t>(kRpWin) * 4;
     constexpr int kWarps = kTileRows / 32;
+    const unsigned char *vbase = static_cast<const unsigned char *>(vals);
+    const unsigned char *cbase = static_cast<const unsigned char *>(cols);
 
     // thread 0: stage tile t into buffer s. Matrix data (values, columns, row
     // pointers) is constant and may be issued before the dependency wait;
@@ -433,17 +461,15 @@ __global__ void __launch_bounds__(kTileRows, 3)
         const int e0 = rp[r0], e1 = rp[r1];
         hdr[s] = make_int4(r0, r1, e0, e1);
         unsigned char *st = smem + s * sb;
-        uint32_t bytes = 0;
         const bool staged = e1 - e0 <= cap && e1 > e0;
-        const int va0 = e0 & ~1, ca0 = e0 & ~3, ra0 = r0 & ~3, fa0 = r0 & ~1;
-        const uint32_t vbytes = staged ? static_cast<uint32_t>(((e1 + 1) & ~1) - va0) * 8u : 0u;
-        const uint32_t cbytes = staged ? static_cast<uint32_t>(((e1 + 3) & ~3) - ca0) * 4u : 0u;
+        const int va0 = e0 & ~(VA - 1), ca0 = e0 & ~(CA - 1), ra0 = r0 & ~3, fa0 = r0 & ~1;
+        const uint32_t vbytes = staged ? static_cast<uint32_t>(((e1 + VA - 1) & ~(VA - 1)) - va0) * VB : 0u;
+        const uint32_t cbytes = staged ? static_cast<uint32_t>(((e1 + CA - 1) & ~(CA - 1)) - ca0) * CB : 0u;
         const uint32_t rbytes = static_cast<uint32_t>(((r1 + 1 + 3) & ~3) - ra0) * 4u;
         const uint32_t fbytes = (MODE != M_SPMV && with_f) ? static_cast<uint32_t>((r1 & ~1) - fa0) * 8u : 0u;
-        bytes = vbytes + cbytes + rbytes + fbytes;
-        mbar_expect_tx(&full[s], bytes);
-        if (vbytes) bulk_g2s(st, val + va0, vbytes, &full[s]);
-        if (cbytes) bulk_g2s(st + o_c, ci + ca0, cbytes, &full[s]);
+        mbar_expect_tx(&full[s], vbytes + cbytes + rbytes + fbytes);
+        if (vbytes) bulk_g2s(st, vbase + static_cast<size_t>(va0) * VB, vbytes, &full[s]);
+        if (cbytes) bulk_g2s(st + o_c, cbase + static_cast<size_t>(ca0) * CB, cbytes, &full[s]);
         bulk_g2s(st + o_rp, rp + ra0, rbytes, &full[s]);
         if (fbytes) bulk_g2s(st + o_f, f + fa0, fbytes, &full[s]);
     };
@@ -456,11 +482,13 @@ __global__ void __launch_bounds__(kTileRows, 3)
         }
         fence_mbar_init();
     }
+    if constexpr (VF == 1)
+        for (int i = threadIdx.x; i < ndict; i += blockDim.x) sdict[i] = dict[i];
     __syncthreads();
     const int G = static_cast<int>(gridDim.x);
     const int b = static_cast<int>(blockIdx.x);
     // prologue tiles go out before the dependency wait WITHOUT f; their f rows
-    // are read from global after the wait (flag below)
+    // are read from global after the wait
     if (threadIdx.x == 0)
         for (int q = 0; q < kStages - 1; ++q)
             if (b + q * G < ntiles) issue(b + q * G, q, false);
@@ -500,9 +528,13 @@ __global__ void __launch_bounds__(kTileRows, 3)
                     fi = f_staged ? reinterpret_cast<const double *>(st + o_f)[row - (r0 & ~1)] : f[row];
                 }
                 const bool staged = (h.w - h.z) <= cap;
-                const int32_t *cc = staged ? reinterpret_cast<const int32_t *>(st + o_c) - (h.z & ~3) : ci;
-                const double *vv = staged ? reinterpret_cast<const double *>(st) - (h.z & ~1) : val;
-                const double o = row_eval<MODE, false>(row, rs, re, cc, vv, x, f, fi, aux, omega);
+                Ent<VF, CF> e;
+                e.vals = staged ? static_cast<const void *>(st - static_cast<size_t>(h.z & ~(VA - 1)) * VB)
+                                : vals;
+                e.cols = staged ? static_cast<const void *>(st + o_c - static_cast<size_t>(h.z & ~(CA - 1)) * CB)
+                                : cols;
+                e.dict = sdict;
+                const double o = row_eval<MODE, false>(row, rs, re, e, x, f, fi, aux, omega);
                 out[row] = o;
                 if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row] : o);
                 if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
@@ -991,6 +1023,11 @@ struct DevLevel {
     int64_t n = 0, nnz = 0, nc = -1;
     int32_t *rp = nullptr, *ci = nullptr, *agg = nullptr, *tiles = nullptr;
     double *v = nullptr, *diag = nullptr;
+    // streamed storage format (see Ent<>): vf 1 = uint8 dictionary values,
+    // cf 1 = int16 column deltas; the raw ci / v stay for the cluster tail
+    int vf = 0, cf = 0, ndict = 0;
+    const void *sv = nullptr, *sc = nullptr;
+    double *dict = nullptr;
     int2 *mem = nullptr;
     int ntiles = 0, cap = 0, grid = 0;
     size_t smem = 0;
@@ -1105,12 +1142,23 @@ static void launch_k(sb_ctx c, void (*k)(KArgs...), dim3 grid, dim3 block, size_
     CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
 
+template <int MODE, int NV, int VF, int CF>
+static void launch_csr_f(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
+                         double *out, double omega, const int *skip, const Red &red, Aux aux) {
+    launch_k(c, k_csr_tile<MODE, NV, VF, CF>, dim3(std::min(l.ntiles, l.grid)), dim3(kTileRows), l.smem, s,
+             static_cast<const int32_t *>(l.rp), l.sc, l.sv, static_cast<const double *>(l.dict), l.ndict,
+             static_cast<const int32_t *>(l.tiles), static_cast<int>(l.ntiles), x, f, out, omega, l.cap, skip, aux,
+             red);
+}
+
 template <int MODE, int NV>
 static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
                        double *out, double omega, const int *skip, const Red &red, Aux aux = Aux{}) {
     if (l.n == 0) return;
-    launch_k(c, k_csr_tile<MODE, NV>, dim3(std::min(l.ntiles, l.grid)), dim3(kTileRows), l.smem, s, l.rp, l.ci,
-             l.v, l.tiles, l.ntiles, x, f, out, omega, l.cap, skip, aux, red);
+    if (l.vf && l.cf) launch_csr_f<MODE, NV, 1, 1>(c, l, s, x, f, out, omega, skip, red, aux);
+    else if (l.vf) launch_csr_f<MODE, NV, 1, 0>(c, l, s, x, f, out, omega, skip, red, aux);
+    else if (l.cf) launch_csr_f<MODE, NV, 0, 1>(c, l, s, x, f, out, omega, skip, red, aux);
+    else launch_csr_f<MODE, NV, 0, 0>(c, l, s, x, f, out, omega, skip, red, aux);
 }
 
 static void launch_jacobi(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *xin, const double *f,
@@ -1439,7 +1487,61 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
     D.ntiles = static_cast<int>(tiles.size()) - 1;
     D.tiles = dalloc<int32_t>(c, static_cast<int64_t>(tiles.size()));
     CK(cudaMemcpy(D.tiles, tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice));
-    D.smem = kStages * stage_bytes_of(D.cap);  // pipeline stages
+    // lossless streamed format: dictionary values / int16 column deltas
+    const char *cz = std::getenv("SB_COMPRESS");
+    const bool compress = !cz || std::atoi(cz) != 0;
+    D.sv = D.v;
+    D.sc = D.ci;
+    if (compress && A.nnz() > 0) {
+        std::map<uint64_t, int> ids;
+        std::vector<double> dict;
+        bool ok = true;
+        for (int64_t k = 0; k < A.nnz() && ok; ++k) {
+            uint64_t bits;
+            std::memcpy(&bits, &A.v[k], 8);
+            if (ids.find(bits) == ids.end()) {
+                if (dict.size() == 256) ok = false;
+                else {
+                    ids[bits] = static_cast<int>(dict.size());
+                    dict.push_back(A.v[k]);
+                }
+            }
+        }
+        if (ok) {
+            std::vector<uint8_t> vi(static_cast<size_t>(A.nnz()));
+            for (int64_t k = 0; k < A.nnz(); ++k) {
+                uint64_t bits;
+                std::memcpy(&bits, &A.v[k], 8);
+                vi[k] = static_cast<uint8_t>(ids[bits]);
+            }
+            auto *dvi = dalloc<uint8_t>(c, A.nnz() + 32);
+            CK(cudaMemcpy(dvi, vi.data(), vi.size(), cudaMemcpyHostToDevice));
+            D.dict = dalloc<double>(c, 256);
+            CK(cudaMemcpy(D.dict, dict.data(), sizeof(double) * dict.size(), cudaMemcpyHostToDevice));
+            D.sv = dvi;
+            D.vf = 1;
+            D.ndict = static_cast<int>(dict.size());
+        }
+        bool fits = true;
+        for (int64_t i = 0; i < A.n && fits; ++i)
+            for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+                const int64_t dlt = static_cast<int64_t>(A.ci[k]) - i;
+                if (dlt < -32768 || dlt > 32767) {
+                    fits = false;
+                    break;
+                }
+            }
+        if (fits) {
+            std::vector<int16_t> cd(static_cast<size_t>(A.nnz()));
+            for (int64_t i = 0; i < A.n; ++i)
+                for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) cd[k] = static_cast<int16_t>(A.ci[k] - i);
+            auto *dcd = dalloc<int16_t>(c, A.nnz() + 16);
+            CK(cudaMemcpy(dcd, cd.data(), sizeof(int16_t) * cd.size(), cudaMemcpyHostToDevice));
+            D.sc = dcd;
+            D.cf = 1;
+        }
+    }
+    D.smem = kStages * stage_bytes_of(D.cap, D.vf, D.cf);  // pipeline stages
     if (!coarsest) {
         D.nc = H.n_coarse;
         D.agg = dalloc<int32_t>(c, A.n);
@@ -1461,9 +1563,12 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
 }
 
 template <int MODE, int NV> static void set_smem_attr(size_t smem) {
-    if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
+    if (smem <= 48 * 1024) return;
+    const int b = static_cast<int>(smem);
+    CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
 }
 
 static Cyc check_cycle(sb_ctx c, const sb_cycle *cp, const char *who) {
@@ -1790,7 +1895,7 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
         for (auto &l : c->L) {
             int occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tile<M_JACOBI, 0>, kTileRows, l.smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tile<M_JACOBI, 0, 0, 0>, kTileRows, l.smem));
             l.grid = std::max(1, nsm * std::max(occ, 1));
         }
         c->nc = h->nc;

@@ -24,8 +24,13 @@ def _mats(sp):
             random_spd(sp, 50, 4), sp.CsrMatrix.from_dense(long_row)]
 
 
-def test_spmv_residual_bitexact(sp, oracle_best):
-    for A in _mats(sp):
+@pytest.mark.parametrize("compress", ["0", "1"])
+def test_spmv_residual_bitexact(sp, oracle_best, compress, monkeypatch):
+    # SB_COMPRESS=1 (default): dictionary values + int16 column deltas where
+    # they fit; 0: raw CSR. Both must give the reference's bits.
+    monkeypatch.setenv("SB_COMPRESS", compress)
+    mats = _mats(sp) + [sp.stencil7(200, 200, 2, 6.0, [-1.0] * 6)]  # |delta| 40000: int32 columns
+    for A in mats:
         x = np.random.default_rng(1).uniform(-1, 1, A.ncols())
         f = np.random.default_rng(2).uniform(-1, 1, A.nrows())
         assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x))
@@ -42,7 +47,9 @@ def test_spmv_long_rows_unstaged_path(sp, oracle_best):
 
 
 @pytest.mark.parametrize("sweeps", [1, 2, 3, 6])
-def test_jacobi_bitexact(sp, oracle_best, sweeps):
+@pytest.mark.parametrize("compress", ["0", "1"])
+def test_jacobi_bitexact(sp, oracle_best, sweeps, compress, monkeypatch):
+    monkeypatch.setenv("SB_COMPRESS", compress)
     jac = sp.SmootherKind.weighted_jacobi()
     for A in _mats(sp):
         x = np.random.default_rng(3).uniform(-1, 1, A.nrows())
