@@ -547,6 +547,157 @@ __global__ void __launch_bounds__(kTileRows, 3)
 }
 
 // ===========================================================================
+// Sliced-ELL tile pipeline (the default streamed format of every level whose
+// 256-row slices pad by <= 50%). Slice t holds rows [256t, 256t+256); entry k
+// of all its rows is contiguous (vals[k*256 + lane], cols[k*256 + lane]), so
+// the thread of row r0+t reads conflict-free shared memory at constant
+// strides with a uniform trip count (the slice width w); its own row length
+// (1 byte) predicates the tail. Entry order within a row is the CSR order:
+// sums are bitwise the reference's. Every TMA window is naturally 16-byte
+// aligned (slices start at multiples of 256 entries / rows).
+// ===========================================================================
+
+__host__ __device__ __forceinline__ size_t sell_stage_bytes(int wmax, int vf, int cf) {
+    return static_cast<size_t>(wmax) * kTileRows * ((vf ? 1 : 8) + (cf ? 2 : 4)) + kTileRows /* len */ +
+           static_cast<size_t>(kTileRows) * 8 /* f */;
+}
+
+template <int MODE, int NV, int VF, int CF>
+__global__ void __launch_bounds__(kTileRows, 3)
+    k_sell_tile(int n, const int64_t *__restrict__ soff, const uint8_t *__restrict__ slen,
+                const void *__restrict__ cols, const void *__restrict__ vals, const double *__restrict__ dict,
+                int ndict, int ntiles, int wmax, const double *__restrict__ x, const double *__restrict__ f,
+                double *__restrict__ out, double omega, const int *skip, Aux aux, Red red) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full[kStages];
+    __shared__ __align__(8) uint64_t empty[kStages];
+    __shared__ int2 hdr[kStages];
+    __shared__ double sdict[VF ? 256 : 1];
+    double acc[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
+
+    constexpr int VB = VF ? 1 : 8;
+    constexpr int CB = CF ? 2 : 4;
+    constexpr int R = kTileRows;
+    const size_t sb = sell_stage_bytes(wmax, VF, CF);
+    const size_t o_c = static_cast<size_t>(wmax) * R * VB;
+    const size_t o_len = o_c + static_cast<size_t>(wmax) * R * CB;
+    const size_t o_f = o_len + R;
+    constexpr int kWarps = R / 32;
+    const unsigned char *vbase = static_cast<const unsigned char *>(vals);
+    const unsigned char *cbase = static_cast<const unsigned char *>(cols);
+
+    auto issue = [&](int t, int s, bool with_f) {
+        const int64_t e0 = soff[t], e1 = soff[t + 1];
+        const int w = static_cast<int>((e1 - e0) / R);
+        const int r0 = t * R;
+        hdr[s] = make_int2(r0, w);
+        unsigned char *st = smem + s * sb;
+        const uint32_t vbytes = static_cast<uint32_t>(w) * R * VB;
+        const uint32_t cbytes = static_cast<uint32_t>(w) * R * CB;
+        const int rows_here = min(R, n - r0);
+        const uint32_t fbytes = (MODE != M_SPMV && with_f) ? static_cast<uint32_t>(rows_here & ~1) * 8u : 0u;
+        mbar_expect_tx(&full[s], vbytes + cbytes + R + fbytes);
+        if (vbytes) bulk_g2s(st, vbase + e0 * VB, vbytes, &full[s]);
+        if (cbytes) bulk_g2s(st + o_c, cbase + e0 * CB, cbytes, &full[s]);
+        bulk_g2s(st + o_len, slen + static_cast<size_t>(r0), R, &full[s]);
+        if (fbytes) bulk_g2s(st + o_f, f + r0, fbytes, &full[s]);
+    };
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < kStages; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], kWarps);
+        }
+        fence_mbar_init();
+    }
+    if constexpr (VF == 1)
+        for (int i = threadIdx.x; i < ndict; i += blockDim.x) sdict[i] = dict[i];
+    __syncthreads();
+    const int G = static_cast<int>(gridDim.x);
+    const int b = static_cast<int>(blockIdx.x);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < kStages - 1; ++q)
+            if (b + q * G < ntiles) issue(b + q * G, q, false);
+    pdl_wait();
+    const bool active = !(skip && *skip);
+    if (!active) {
+        for (int q = 0; q < kStages - 1; ++q)
+            if (b + q * G < ntiles) mbar_wait(&full[q], 0u);
+        pdl_trigger();
+    } else {
+        uint32_t fph = 0u, eph = 0u;
+        int s = 0, it = 0;
+        const int lane = threadIdx.x & 31;
+        const int tid = threadIdx.x;
+        for (int t = b; t < ntiles; t += G, ++it, s = (s + 1 == kStages) ? 0 : s + 1) {
+            if (t + G >= ntiles) pdl_trigger();
+            const int tn = t + (kStages - 1) * G;
+            const int sn = (s + kStages - 1) % kStages;
+            if (tid == 0 && tn < ntiles) {
+                if (it >= 1) {
+                    mbar_wait(&empty[sn], (eph >> sn) & 1u);
+                    eph ^= 1u << sn;
+                }
+                issue(tn, sn, true);
+            }
+            mbar_wait(&full[s], (fph >> s) & 1u);
+            fph ^= 1u << s;
+            const int2 h = hdr[s];
+            const int row = h.x + tid;
+            const unsigned char *st = smem + s * sb;
+            if (row < n) {
+                const int len = st[o_len + tid];
+                double fi = 0.0;
+                if (MODE != M_SPMV) {
+                    const bool f_staged = it >= kStages - 1 && row < h.x + (min(R, n - h.x) & ~1);
+                    fi = f_staged ? reinterpret_cast<const double *>(st + o_f)[tid] : f[row];
+                }
+                const unsigned char *sv = st + static_cast<size_t>(tid) * VB;
+                const unsigned char *sc = st + o_c + static_cast<size_t>(tid) * CB;
+                double sum = 0.0, d = 0.0, xi = 0.0;
+                if constexpr (MODE >= M_JACOBI) xi = xval<MODE, false>(row, x, f, aux, omega);
+                constexpr int U = MODE == M_JACOBI_ZERO ? 4 : 8;  // (ZERO gathers f and a_jj: fewer in flight)
+                for (int kb = 0; kb < len; kb += U) {
+                    int c[U];
+                    double a[U], xv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (kb + u < len) {
+                            const size_t k = static_cast<size_t>(kb + u) * R;
+                            if constexpr (CF == 1) c[u] = row + static_cast<int>(reinterpret_cast<const int16_t *>(sc)[k]);
+                            else c[u] = reinterpret_cast<const int32_t *>(sc)[k];
+                            if constexpr (VF == 1) a[u] = sdict[sv[k]];
+                            else a[u] = reinterpret_cast<const double *>(sv)[k];
+                        }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (kb + u < len) xv[u] = xval<MODE, false>(c[u], x, f, aux, omega);
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (kb + u < len) {
+                            sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
+                            if (MODE >= M_JACOBI && c[u] == row) d = a[u];
+                        }
+                }
+                double o;
+                if constexpr (MODE == M_SPMV) o = sum;
+                else if constexpr (MODE == M_RESID) o = __dsub_rn(fi, sum);
+                else o = __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
+                out[row] = o;
+                if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row] : o);
+                if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+    }
+    if constexpr (NV > 0) finish_reduction<NV>(red, acc);
+}
+
+// ===========================================================================
 // Cluster-resident tail: the deepest levels (each CTA's slice of every tail
 // level fits in its shared memory), down to the coarsest solve and back up, in
 // ONE launch of a thread-block cluster (16 CTAs where schedulable). CTA r owns
@@ -1028,6 +1179,12 @@ struct DevLevel {
     int vf = 0, cf = 0, ndict = 0;
     const void *sv = nullptr, *sc = nullptr;
     double *dict = nullptr;
+    // sliced-ELL layout (sell = 1): slice offsets, row lengths, slice-major entries
+    int sell = 0, sell_tiles = 0, sell_wmax = 0, sell_grid = 0;
+    size_t sell_smem = 0;
+    int64_t *soff = nullptr;
+    uint8_t *slen = nullptr;
+    const void *sell_v = nullptr, *sell_c = nullptr;
     int2 *mem = nullptr;
     int ntiles = 0, cap = 0, grid = 0;
     size_t smem = 0;
@@ -1151,10 +1308,26 @@ static void launch_csr_f(sb_ctx c, const DevLevel &l, cudaStream_t s, const doub
              red);
 }
 
+template <int MODE, int NV, int VF, int CF>
+static void launch_sell_f(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
+                          double *out, double omega, const int *skip, const Red &red, Aux aux) {
+    launch_k(c, k_sell_tile<MODE, NV, VF, CF>, dim3(std::min(l.sell_tiles, l.sell_grid)), dim3(kTileRows),
+             l.sell_smem, s, static_cast<int>(l.n), static_cast<const int64_t *>(l.soff),
+             static_cast<const uint8_t *>(l.slen), l.sell_c, l.sell_v, static_cast<const double *>(l.dict), l.ndict,
+             l.sell_tiles, l.sell_wmax, x, f, out, omega, skip, aux, red);
+}
+
 template <int MODE, int NV>
 static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
                        double *out, double omega, const int *skip, const Red &red, Aux aux = Aux{}) {
     if (l.n == 0) return;
+    if (l.sell) {
+        if (l.vf && l.cf) launch_sell_f<MODE, NV, 1, 1>(c, l, s, x, f, out, omega, skip, red, aux);
+        else if (l.vf) launch_sell_f<MODE, NV, 1, 0>(c, l, s, x, f, out, omega, skip, red, aux);
+        else if (l.cf) launch_sell_f<MODE, NV, 0, 1>(c, l, s, x, f, out, omega, skip, red, aux);
+        else launch_sell_f<MODE, NV, 0, 0>(c, l, s, x, f, out, omega, skip, red, aux);
+        return;
+    }
     if (l.vf && l.cf) launch_csr_f<MODE, NV, 1, 1>(c, l, s, x, f, out, omega, skip, red, aux);
     else if (l.vf) launch_csr_f<MODE, NV, 1, 0>(c, l, s, x, f, out, omega, skip, red, aux);
     else if (l.cf) launch_csr_f<MODE, NV, 0, 1>(c, l, s, x, f, out, omega, skip, red, aux);
@@ -1542,6 +1715,84 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
         }
     }
     D.smem = kStages * stage_bytes_of(D.cap, D.vf, D.cf);  // pipeline stages
+    // sliced-ELL conversion (SB_SELL=0 keeps the CSR pipeline)
+    const char *se = std::getenv("SB_SELL");
+    if ((!se || std::atoi(se) != 0) && A.n > 0) {
+        const int64_t nt = (A.n + kTileRows - 1) / kTileRows;
+        std::vector<int64_t> off(static_cast<size_t>(nt) + 1, 0);
+        int wmax = 0;
+        bool ok = true;
+        for (int64_t t = 0; t < nt && ok; ++t) {
+            int w = 0;
+            for (int64_t r = t * kTileRows; r < std::min<int64_t>(A.n, (t + 1) * kTileRows); ++r)
+                w = std::max<int>(w, static_cast<int>(A.rp[r + 1] - A.rp[r]));
+            if (w > 64) ok = false;
+            wmax = std::max(wmax, w);
+            off[t + 1] = off[t] + static_cast<int64_t>(w) * kTileRows;
+        }
+        const size_t stage = sell_stage_bytes(wmax, D.vf, D.cf);
+        if (ok && off[nt] <= 3 * A.nnz() / 2 + kTileRows && kStages * stage <= 200 * 1024) {
+            std::vector<uint8_t> len(static_cast<size_t>(nt) * kTileRows, 0);
+            const size_t tot = static_cast<size_t>(off[nt]);
+            std::vector<int16_t> c16(D.cf ? tot : 0, 0);
+            std::vector<int32_t> c32(D.cf ? 0 : tot, 0);
+            std::vector<uint8_t> v8(D.vf ? tot : 0, 0);
+            std::vector<double> v64(D.vf ? 0 : tot, 0.0);
+            std::map<uint64_t, int> ids;
+            if (D.vf) {  // same dictionary order as the CSR-stream arrays
+                std::vector<double> dict(static_cast<size_t>(D.ndict));
+                CK(cudaMemcpy(dict.data(), D.dict, sizeof(double) * dict.size(), cudaMemcpyDeviceToHost));
+                for (int q = 0; q < D.ndict; ++q) {
+                    uint64_t bits;
+                    std::memcpy(&bits, &dict[q], 8);
+                    ids[bits] = q;
+                }
+            }
+            for (int64_t t = 0; t < nt; ++t)
+                for (int64_t r = t * kTileRows; r < std::min<int64_t>(A.n, (t + 1) * kTileRows); ++r) {
+                    const int64_t lane = r - t * kTileRows;
+                    len[static_cast<size_t>(r)] = static_cast<uint8_t>(A.rp[r + 1] - A.rp[r]);
+                    for (int64_t k = A.rp[r]; k < A.rp[r + 1]; ++k) {
+                        const size_t pos = static_cast<size_t>(off[t] + (k - A.rp[r]) * kTileRows + lane);
+                        if (D.cf) c16[pos] = static_cast<int16_t>(A.ci[k] - r);
+                        else c32[pos] = A.ci[k];
+                        if (D.vf) {
+                            uint64_t bits;
+                            std::memcpy(&bits, &A.v[k], 8);
+                            v8[pos] = static_cast<uint8_t>(ids[bits]);
+                        } else {
+                            v64[pos] = A.v[k];
+                        }
+                    }
+                }
+            D.soff = dalloc<int64_t>(c, nt + 1);
+            CK(cudaMemcpy(D.soff, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice));
+            D.slen = dalloc<uint8_t>(c, static_cast<int64_t>(len.size()));
+            CK(cudaMemcpy(D.slen, len.data(), len.size(), cudaMemcpyHostToDevice));
+            if (D.cf) {
+                auto *p = dalloc<int16_t>(c, static_cast<int64_t>(tot));
+                CK(cudaMemcpy(p, c16.data(), sizeof(int16_t) * tot, cudaMemcpyHostToDevice));
+                D.sell_c = p;
+            } else {
+                auto *p = dalloc<int32_t>(c, static_cast<int64_t>(tot));
+                CK(cudaMemcpy(p, c32.data(), sizeof(int32_t) * tot, cudaMemcpyHostToDevice));
+                D.sell_c = p;
+            }
+            if (D.vf) {
+                auto *p = dalloc<uint8_t>(c, static_cast<int64_t>(tot));
+                CK(cudaMemcpy(p, v8.data(), tot, cudaMemcpyHostToDevice));
+                D.sell_v = p;
+            } else {
+                auto *p = dalloc<double>(c, static_cast<int64_t>(tot));
+                CK(cudaMemcpy(p, v64.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
+                D.sell_v = p;
+            }
+            D.sell = 1;
+            D.sell_tiles = static_cast<int>(nt);
+            D.sell_wmax = wmax;
+            D.sell_smem = kStages * stage;
+        }
+    }
     if (!coarsest) {
         D.nc = H.n_coarse;
         D.agg = dalloc<int32_t>(c, A.n);
@@ -1565,6 +1816,10 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
 template <int MODE, int NV> static void set_smem_attr(size_t smem) {
     if (smem <= 48 * 1024) return;
     const int b = static_cast<int>(smem);
+    CK(cudaFuncSetAttribute(k_sell_tile<MODE, NV, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_sell_tile<MODE, NV, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_sell_tile<MODE, NV, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_sell_tile<MODE, NV, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
@@ -1880,7 +2135,7 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
         size_t max_smem = 0;
         for (size_t k = 0; k < h->levels.size(); ++k) {
             upload_level(c, h->levels[k], c->L[k], k + 1 == h->levels.size(), n0);
-            max_smem = std::max(max_smem, c->L[k].smem);
+            max_smem = std::max(max_smem, std::max(c->L[k].smem, c->L[k].sell_smem));
         }
         if (max_smem > 200 * 1024) throw invalid_argument("sb_create: tile staging exceeds shared memory");
         set_smem_attr<M_SPMV, 0>(max_smem);
@@ -1897,6 +2152,12 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
             int occ = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tile<M_JACOBI, 0, 0, 0>, kTileRows, l.smem));
             l.grid = std::max(1, nsm * std::max(occ, 1));
+            if (l.sell) {
+                occ = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell_tile<M_JACOBI, 0, 1, 1>, kTileRows,
+                                                                 l.sell_smem));
+                l.sell_grid = std::max(1, nsm * std::max(occ, 1));
+            }
         }
         c->nc = h->nc;
         if (h->nc > 0) {

@@ -24,11 +24,13 @@ def _mats(sp):
             random_spd(sp, 50, 4), sp.CsrMatrix.from_dense(long_row)]
 
 
-@pytest.mark.parametrize("compress", ["0", "1"])
-def test_spmv_residual_bitexact(sp, oracle_best, compress, monkeypatch):
+@pytest.mark.parametrize("compress,sell", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
+def test_spmv_residual_bitexact(sp, oracle_best, compress, sell, monkeypatch):
     # SB_COMPRESS=1 (default): dictionary values + int16 column deltas where
-    # they fit; 0: raw CSR. Both must give the reference's bits.
+    # they fit; SB_SELL=1 (default): sliced-ELL slices. All must give the
+    # reference's bits.
     monkeypatch.setenv("SB_COMPRESS", compress)
+    monkeypatch.setenv("SB_SELL", sell)
     mats = _mats(sp) + [sp.stencil7(200, 200, 2, 6.0, [-1.0] * 6)]  # |delta| 40000: int32 columns
     for A in mats:
         x = np.random.default_rng(1).uniform(-1, 1, A.ncols())
@@ -47,9 +49,10 @@ def test_spmv_long_rows_unstaged_path(sp, oracle_best):
 
 
 @pytest.mark.parametrize("sweeps", [1, 2, 3, 6])
-@pytest.mark.parametrize("compress", ["0", "1"])
-def test_jacobi_bitexact(sp, oracle_best, sweeps, compress, monkeypatch):
+@pytest.mark.parametrize("compress,sell", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
+def test_jacobi_bitexact(sp, oracle_best, sweeps, compress, sell, monkeypatch):
     monkeypatch.setenv("SB_COMPRESS", compress)
+    monkeypatch.setenv("SB_SELL", sell)
     jac = sp.SmootherKind.weighted_jacobi()
     for A in _mats(sp):
         x = np.random.default_rng(3).uniform(-1, 1, A.nrows())
