@@ -557,21 +557,27 @@ __global__ void __launch_bounds__(kTileRows, 3)
 // aligned (slices start at multiples of 256 entries / rows).
 // ===========================================================================
 
+constexpr int kSellStages = 5;  // deeper than the CSR pipeline: slices are small once compressed
+
 __host__ __device__ __forceinline__ size_t sell_stage_bytes(int wmax, int vf, int cf) {
-    return static_cast<size_t>(wmax) * kTileRows * ((vf ? 1 : 8) + (cf ? 2 : 4)) + kTileRows /* len */ +
+    return static_cast<size_t>(wmax) * kTileRows * ((vf ? 1 : 8) + (cf ? 2 : 4)) + 2 * kTileRows /* len, dpos */ +
            static_cast<size_t>(kTileRows) * 8 /* f */;
 }
 
+#ifndef SB_SELL_MINB
+#define SB_SELL_MINB 4
+#endif
 template <int MODE, int NV, int VF, int CF>
-__global__ void __launch_bounds__(kTileRows, 3)
+__global__ void __launch_bounds__(kTileRows, SB_SELL_MINB)
     k_sell_tile(int n, const int64_t *__restrict__ soff, const uint8_t *__restrict__ slen,
                 const void *__restrict__ cols, const void *__restrict__ vals, const double *__restrict__ dict,
                 int ndict, int ntiles, int wmax, const double *__restrict__ x, const double *__restrict__ f,
                 double *__restrict__ out, double omega, const int *skip, Aux aux, Red red) {
+    constexpr int S = kSellStages;
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full[kStages];
-    __shared__ __align__(8) uint64_t empty[kStages];
-    __shared__ int2 hdr[kStages];
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ __align__(8) uint64_t empty[S];
+    __shared__ int2 hdr[S];
     __shared__ double sdict[VF ? 256 : 1];
     double acc[NV > 0 ? NV : 1];
 #pragma unroll
@@ -582,8 +588,8 @@ __global__ void __launch_bounds__(kTileRows, 3)
     constexpr int R = kTileRows;
     const size_t sb = sell_stage_bytes(wmax, VF, CF);
     const size_t o_c = static_cast<size_t>(wmax) * R * VB;
-    const size_t o_len = o_c + static_cast<size_t>(wmax) * R * CB;
-    const size_t o_f = o_len + R;
+    const size_t o_len = o_c + static_cast<size_t>(wmax) * R * CB;  // len[256] then dpos[256]
+    const size_t o_f = o_len + 2 * R;
     constexpr int kWarps = R / 32;
     const unsigned char *vbase = static_cast<const unsigned char *>(vals);
     const unsigned char *cbase = static_cast<const unsigned char *>(cols);
@@ -598,16 +604,16 @@ __global__ void __launch_bounds__(kTileRows, 3)
         const uint32_t cbytes = static_cast<uint32_t>(w) * R * CB;
         const int rows_here = min(R, n - r0);
         const uint32_t fbytes = (MODE != M_SPMV && with_f) ? static_cast<uint32_t>(rows_here & ~1) * 8u : 0u;
-        mbar_expect_tx(&full[s], vbytes + cbytes + R + fbytes);
+        mbar_expect_tx(&full[s], vbytes + cbytes + 2 * R + fbytes);
         if (vbytes) bulk_g2s(st, vbase + e0 * VB, vbytes, &full[s]);
         if (cbytes) bulk_g2s(st + o_c, cbase + e0 * CB, cbytes, &full[s]);
-        bulk_g2s(st + o_len, slen + static_cast<size_t>(r0), R, &full[s]);
+        bulk_g2s(st + o_len, slen + 2 * static_cast<size_t>(r0), 2 * R, &full[s]);
         if (fbytes) bulk_g2s(st + o_f, f + r0, fbytes, &full[s]);
     };
 
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int q = 0; q < kStages; ++q) {
+        for (int q = 0; q < S; ++q) {
             mbar_init(&full[q], 1);
             mbar_init(&empty[q], kWarps);
         }
@@ -619,12 +625,12 @@ __global__ void __launch_bounds__(kTileRows, 3)
     const int G = static_cast<int>(gridDim.x);
     const int b = static_cast<int>(blockIdx.x);
     if (threadIdx.x == 0)
-        for (int q = 0; q < kStages - 1; ++q)
+        for (int q = 0; q < S - 1; ++q)
             if (b + q * G < ntiles) issue(b + q * G, q, false);
     pdl_wait();
     const bool active = !(skip && *skip);
     if (!active) {
-        for (int q = 0; q < kStages - 1; ++q)
+        for (int q = 0; q < S - 1; ++q)
             if (b + q * G < ntiles) mbar_wait(&full[q], 0u);
         pdl_trigger();
     } else {
@@ -632,10 +638,10 @@ __global__ void __launch_bounds__(kTileRows, 3)
         int s = 0, it = 0;
         const int lane = threadIdx.x & 31;
         const int tid = threadIdx.x;
-        for (int t = b; t < ntiles; t += G, ++it, s = (s + 1 == kStages) ? 0 : s + 1) {
+        for (int t = b; t < ntiles; t += G, ++it, s = (s + 1 == S) ? 0 : s + 1) {
             if (t + G >= ntiles) pdl_trigger();
-            const int tn = t + (kStages - 1) * G;
-            const int sn = (s + kStages - 1) % kStages;
+            const int tn = t + (S - 1) * G;
+            const int sn = (s + S - 1) % S;
             if (tid == 0 && tn < ntiles) {
                 if (it >= 1) {
                     mbar_wait(&empty[sn], (eph >> sn) & 1u);
@@ -647,40 +653,48 @@ __global__ void __launch_bounds__(kTileRows, 3)
             fph ^= 1u << s;
             const int2 h = hdr[s];
             const int row = h.x + tid;
+            const int w = h.y;  // slice width: warp-uniform trip count
             const unsigned char *st = smem + s * sb;
             if (row < n) {
                 const int len = st[o_len + tid];
                 double fi = 0.0;
                 if (MODE != M_SPMV) {
-                    const bool f_staged = it >= kStages - 1 && row < h.x + (min(R, n - h.x) & ~1);
+                    const bool f_staged = it >= S - 1 && row < h.x + (min(R, n - h.x) & ~1);
                     fi = f_staged ? reinterpret_cast<const double *>(st + o_f)[tid] : f[row];
                 }
                 const unsigned char *sv = st + static_cast<size_t>(tid) * VB;
                 const unsigned char *sc = st + o_c + static_cast<size_t>(tid) * CB;
-                double sum = 0.0, d = 0.0, xi = 0.0;
-                if constexpr (MODE >= M_JACOBI) xi = xval<MODE, false>(row, x, f, aux, omega);
-                constexpr int U = MODE == M_JACOBI_ZERO ? 4 : 8;  // (ZERO gathers f and a_jj: fewer in flight)
-                for (int kb = 0; kb < len; kb += U) {
+                auto colv = [&](int k) -> int {
+                    if constexpr (CF == 1) return row + static_cast<int>(reinterpret_cast<const int16_t *>(sc)[k * R]);
+                    else return reinterpret_cast<const int32_t *>(sc)[k * R];
+                };
+                auto valv = [&](int k) -> double {
+                    if constexpr (VF == 1) return sdict[sv[k * R]];
+                    else return reinterpret_cast<const double *>(sv)[k * R];
+                };
+                double sum = 0.0, xi = 0.0, d = 0.0;
+                if constexpr (MODE >= M_JACOBI) {
+                    xi = xval<MODE, false>(row, x, f, aux, omega);
+                    d = valv(st[o_len + R + tid]);  // the row's diagonal slot
+                }
+                constexpr int U = MODE == M_JACOBI_ZERO ? 4 : 8;
+                // Branch-free slices: padding slots (k >= len) hold column =
+                // row, so their gathers are valid; they are masked out of the
+                // sum, which therefore sees exactly the row's entries in order.
+                for (int kb = 0; kb < w; kb += U) {
                     int c[U];
                     double a[U], xv[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (kb + u < len) {
-                            const size_t k = static_cast<size_t>(kb + u) * R;
-                            if constexpr (CF == 1) c[u] = row + static_cast<int>(reinterpret_cast<const int16_t *>(sc)[k]);
-                            else c[u] = reinterpret_cast<const int32_t *>(sc)[k];
-                            if constexpr (VF == 1) a[u] = sdict[sv[k]];
-                            else a[u] = reinterpret_cast<const double *>(sv)[k];
-                        }
+                    for (int u = 0; u < U; ++u) {
+                        const int k = min(kb + u, w - 1);
+                        c[u] = colv(k);
+                        a[u] = valv(k);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) xv[u] = xval<MODE, false>(c[u], x, f, aux, omega);
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        if (kb + u < len) xv[u] = xval<MODE, false>(c[u], x, f, aux, omega);
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (kb + u < len) {
-                            sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
-                            if (MODE >= M_JACOBI && c[u] == row) d = a[u];
-                        }
+                        if (kb + u < len) sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
                 }
                 double o;
                 if constexpr (MODE == M_SPMV) o = sum;
@@ -1731,8 +1745,9 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
             off[t + 1] = off[t] + static_cast<int64_t>(w) * kTileRows;
         }
         const size_t stage = sell_stage_bytes(wmax, D.vf, D.cf);
-        if (ok && off[nt] <= 3 * A.nnz() / 2 + kTileRows && kStages * stage <= 200 * 1024) {
-            std::vector<uint8_t> len(static_cast<size_t>(nt) * kTileRows, 0);
+        if (ok && off[nt] <= 3 * A.nnz() / 2 + kTileRows && kSellStages * stage <= 200 * 1024) {
+            // per slice: 256 row lengths then 256 diagonal slots (255: none)
+            std::vector<uint8_t> len(static_cast<size_t>(nt) * 2 * kTileRows, 0);
             const size_t tot = static_cast<size_t>(off[nt]);
             std::vector<int16_t> c16(D.cf ? tot : 0, 0);
             std::vector<int32_t> c32(D.cf ? 0 : tot, 0);
@@ -1751,7 +1766,17 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
             for (int64_t t = 0; t < nt; ++t)
                 for (int64_t r = t * kTileRows; r < std::min<int64_t>(A.n, (t + 1) * kTileRows); ++r) {
                     const int64_t lane = r - t * kTileRows;
-                    len[static_cast<size_t>(r)] = static_cast<uint8_t>(A.rp[r + 1] - A.rp[r]);
+                    len[static_cast<size_t>(t * 2 * kTileRows + lane)] = static_cast<uint8_t>(A.rp[r + 1] - A.rp[r]);
+                    uint8_t dpos = 0;  // (a missing diagonal is rejected before any sweep)
+                    for (int64_t k = A.rp[r]; k < A.rp[r + 1]; ++k)
+                        if (A.ci[k] == r) dpos = static_cast<uint8_t>(k - A.rp[r]);
+                    len[static_cast<size_t>(t * 2 * kTileRows + kTileRows + lane)] = dpos;
+                    const int w_t = static_cast<int>((off[t + 1] - off[t]) / kTileRows);
+                    for (int64_t k = A.rp[r + 1] - A.rp[r]; k < w_t; ++k) {  // padding: column = row
+                        const size_t pos = static_cast<size_t>(off[t] + k * kTileRows + lane);
+                        if (D.cf) c16[pos] = 0;
+                        else c32[pos] = static_cast<int32_t>(r);
+                    }
                     for (int64_t k = A.rp[r]; k < A.rp[r + 1]; ++k) {
                         const size_t pos = static_cast<size_t>(off[t] + (k - A.rp[r]) * kTileRows + lane);
                         if (D.cf) c16[pos] = static_cast<int16_t>(A.ci[k] - r);
@@ -1790,7 +1815,7 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
             D.sell = 1;
             D.sell_tiles = static_cast<int>(nt);
             D.sell_wmax = wmax;
-            D.sell_smem = kStages * stage;
+            D.sell_smem = kSellStages * stage;
         }
     }
     if (!coarsest) {
