@@ -189,6 +189,10 @@ int sb_time_kernel(sb_ctx ctx, int kind, int level, const sb_cycle *cp, int reps
  * sb_create) and the tail placement (first tail level, cluster CTAs, smem). */
 int sb_tail_trace(sb_ctx ctx, unsigned long long *out, int cap);
 int sb_tail_info(sb_ctx ctx, int *tail_from, int *ctas, int *smem_bytes);
+/* Streamed storage of level k (lossless): fmt = {sliced-ELL?, value dictionary?,
+ * int16 column deltas?, slice width}; *matrix_bytes = HBM bytes one matrix pass
+ * streams (entries incl. padding + per-row metadata); *nnz = stored nonzeros. */
+int sb_level_format(sb_ctx ctx, int level, int *fmt, int64_t *matrix_bytes, int64_t *nnz);
 /* Kernels launched by one V-cycle from level 0 (graph node count). */
 int sb_vcycle_launches(sb_ctx ctx, const sb_cycle *cp);
 

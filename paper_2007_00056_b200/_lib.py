@@ -79,7 +79,7 @@ EXPORTS = [
     "sb_smooth", "sb_residual", "sb_restrict", "sb_prolong", "sb_coarse_solve",
     "sb_gen_convdiff2d", "sb_gen_stencil7", "sb_gen_convdiff3d", "sb_gen_stencil27",
     "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_time_kernel", "sb_vcycle_launches", "sb_tail_trace",
-    "sb_tail_info",
+    "sb_tail_info", "sb_level_format",
 ]
 
 _P = C.c_void_p
@@ -122,6 +122,7 @@ _SIGS = {
     "sb_vcycle_launches": (C.c_int, [_P, C.POINTER(sb_cycle)]),
     "sb_tail_trace": (C.c_int, [_P, C.POINTER(C.c_ulonglong), C.c_int]),
     "sb_tail_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "sb_level_format": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }
 
 
