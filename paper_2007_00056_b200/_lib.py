@@ -79,7 +79,8 @@ EXPORTS = [
     "sb_smooth", "sb_residual", "sb_restrict", "sb_prolong", "sb_coarse_solve",
     "sb_gen_convdiff2d", "sb_gen_stencil7", "sb_gen_convdiff3d", "sb_gen_stencil27",
     "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_time_kernel", "sb_vcycle_launches", "sb_tail_trace",
-    "sb_tail_info", "sb_level_format",
+    "sb_tail_info", "sb_level_format", "sb_partition", "sb_partition_free", "sb_partition_info",
+    "sb_partition_level", "sb_partition_exchange",
 ]
 
 _P = C.c_void_p
@@ -123,6 +124,16 @@ _SIGS = {
     "sb_tail_trace": (C.c_int, [_P, C.POINTER(C.c_ulonglong), C.c_int]),
     "sb_tail_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "sb_level_format": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "sb_partition": (C.c_int, [_P, C.c_int, C.c_int, C.c_int64, C.POINTER(_P)]),
+    "sb_partition_free": (None, [_P]),
+    "sb_partition_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "sb_partition_level": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int64), C.POINTER(sb_csr),
+                                     C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int64)),
+                                     C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int32)),
+                                     C.POINTER(C.POINTER(C.c_int32)), C.POINTER(C.POINTER(C.c_int32))]),
+    "sb_partition_exchange": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.POINTER(C.c_int)),
+                                        C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int32)),
+                                        C.POINTER(C.POINTER(C.c_int)), C.POINTER(C.POINTER(C.c_int64))]),
 }
 
 

@@ -2279,6 +2279,29 @@ int sb_pbicgstab_dev(sb_ctx c, const sb_cycle *cp, const double *d_b, double *d_
 
 double sb_last_solve_ms(sb_ctx c) { return c ? c->last_solve_ms : 0.0; }
 
+// Streamed storage of level k: fmt[0] = 1 sliced-ELL / 0 CSR, fmt[1] = value
+// dictionary, fmt[2] = int16 column deltas, fmt[3] = slice width (max);
+// *matrix_bytes = bytes one pass over the matrix streams from HBM (entries
+// incl. padding + per-row metadata), *nnz = stored nonzeros.
+int sb_level_format(sb_ctx c, int k, int *fmt, int64_t *matrix_bytes, int64_t *nnz) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, k);
+        const int vb = l.vf ? 1 : 8, cb = l.cf ? 2 : 4;
+        fmt[0] = l.sell;
+        fmt[1] = l.vf;
+        fmt[2] = l.cf;
+        fmt[3] = l.sell ? l.sell_wmax : 0;
+        if (l.sell) {
+            int64_t entries = 0;
+            CK(cudaMemcpy(&entries, l.soff + l.sell_tiles, sizeof(int64_t), cudaMemcpyDeviceToHost));
+            *matrix_bytes = entries * (vb + cb) + 2 * static_cast<int64_t>(l.sell_tiles) * kTileRows;
+        } else {
+            *matrix_bytes = l.nnz * (vb + cb) + 4 * (l.n + 1);
+        }
+        *nnz = l.nnz;
+    });
+}
+
 // Diagnostics: copies the tail kernel's phase timestamps (SB_TAIL_TRACE=1) into
 // out (count first); returns the number of entries, or -1 if tracing is off.
 int sb_tail_trace(sb_ctx c, unsigned long long *out, int cap) {
