@@ -231,6 +231,98 @@ def cpu_baseline_sample(A, b, tol, wl, sample_iters):
                       f"scaled x{scale:.2f} to the {k}-iteration solve"}
 
 
+def run_multi(args, wl):
+    """N > 1 GPUs (torchrun, one rank per GPU): the row-partitioned solve
+    (libsparsh_b200 sb_dist_*, NCCL halo exchanges / allreduce; levels below
+    --gather-rows replicated). Default workload: weak scaling of C2 — the
+    7-pt Poisson grid 128 x 128 x (128 N), z-slab row blocks, so N = 1 is C2
+    itself. --workload C3/C4/C1: strong scaling of that config."""
+    import torch
+    import torch.distributed as dist
+    from paper_2007_00056_b200 import sparsh as sp
+    from paper_2007_00056_b200.dist import DistSolver, nccl_unique_id
+
+    ws, rank, local = dist_env()
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    if wl == "C2":
+        A = sp.poisson3d(128, 128, 128 * ws)
+        desc = f"C2 weak-scaled: 3D 7-pt Poisson 128x128x{128 * ws} ({A.nrows() // ws} DOFs per GPU) AMG-PCG, row-partitioned"
+        scaling = "weak"
+    else:
+        A = WORKLOADS[wl]["gen"](sp)
+        desc = WORKLOADS[wl]["desc"] + f", row-partitioned over {ws} GPUs"
+        scaling = "strong"
+    n = A.nrows()
+    cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40, coarse_target=500)
+    t0 = time.perf_counter()
+    h = sp.Hierarchy(A, cfg, device=local)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ds = DistSolver(h, ws, args.gather_rows, local=False, rank=rank, nccl_id=obj[0], device=local)
+    setup_s = time.perf_counter() - t0
+    cp = sp.CycleParams.from_config(cfg)
+    solver = WORKLOADS[wl]["solver"]
+    nloc = ds.hi - ds.lo
+    tol = 1e-8 * float(np.sqrt(n))  # ||ones(n)||
+    fn = ds.pcg if solver == "pcg" else ds.pbicgstab
+    b_dev = torch.ones(nloc, dtype=torch.float64, device=f"cuda:{local}")
+    x_dev = torch.zeros(nloc, dtype=torch.float64, device=f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    for _ in range(max(args.warmup, 3)):
+        rep = fn(b_dev.data_ptr(), cp, tol, 1000, x_dev.data_ptr()).report
+    assert rep.converged(), f"multi-GPU solve did not converge: {rep.termination}"
+    per = []
+    launches = 0
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            rep = fn(b_dev.data_ptr(), cp, tol, 1000, x_dev.data_ptr()).report
+            per.append(ds.last_solve_ms())
+            launches += ds.last_launches()
+        torch.cuda.synchronize()
+        dist.barrier()
+    t = torch.tensor([statistics.mean(per)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # e2e: host (pinned) b / x through the public call
+    b_pin = torch.ones(nloc, dtype=torch.float64).pin_memory().numpy()
+    x_pin = torch.zeros(nloc, dtype=torch.float64).pin_memory().numpy()
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t1 = time.perf_counter()
+        fn(b_pin, cp, tol, 1000, x_pin)
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - t1)
+    te = torch.tensor([statistics.mean(e2e)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": scaling,
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "n": n, "nnz": A.nnz(), "levels": h.nlevels(),
+                           "iterations": rep.iterations, "rhs": "ones", "tol": "1e-8*||b||",
+                           "partition": f"contiguous row blocks; levels with < {args.gather_rows} rows replicated "
+                                        f"(first replicated level {ds.first_replicated})",
+                           "transport": "NCCL grouped send/recv (halos), allreduce (dots)",
+                           "parallelism": f"row-partitioned over {ws} GPUs", "setup_s": round(setup_s, 3),
+                           "l2": "hierarchy > L2 and L2 flushed (256 MB write) before every step"},
+                "roofline": None,
+                "e2e": {"value": float(te.item()), "unit": "s", "h2d_bytes_per_step": 8 * nloc,
+                        "d2h_bytes_per_step": 8 * nloc},
+                "gpu_launches": launches, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    del ds
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,10 +332,14 @@ def main():
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--ref-sample-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather-rows", type=int, default=131072)
+    ap.add_argument("--dist", action="store_true", help="use the partitioned (NCCL) path even at N = 1")
     args = ap.parse_args()
     wl = args.workload
     if args.impl == "reference":
         return run_reference(args, wl)
+    if dist_env()[0] > 1 or args.dist:
+        return run_multi(args, wl)
 
     import ctypes as C
     import torch

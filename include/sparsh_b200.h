@@ -229,6 +229,29 @@ int sb_partition_exchange(sb_part p, int level, int which, int64_t *counts4, con
                           const int64_t **send_off, const int32_t **send_idx, const int **recv_peers,
                           const int64_t **recv_off);
 
+/* Partitioned solve. NCCL mode: one rank per process/GPU; rank 0 calls
+ * sb_nccl_unique_id and broadcasts the 128 bytes (e.g. torch.distributed);
+ * b / x are the rank's own rows [lo, hi) (sb_dist_rows). In-process mode
+ * (sb_dist_create_local): nranks virtual ranks on one device sharing this
+ * process (exchanges are peer-buffer gathers) — b / x are global vectors.
+ * Same termination semantics and report as sb_pcg / sb_pbicgstab; the
+ * V-cycle is bitwise identical to the single-GPU one. */
+typedef struct sb_dist_s *sb_dist;
+int sb_nccl_unique_id(unsigned char *out128);
+int sb_dist_create(sb_hier h, int rank, int nranks, const unsigned char *nccl_id128, int64_t gather_rows,
+                   const sb_device_opts *opts, sb_dist *out);
+int sb_dist_create_local(sb_hier h, int nranks, int64_t gather_rows, const sb_device_opts *opts,
+                         sb_dist *out);
+void sb_dist_destroy(sb_dist d);
+int sb_dist_rows(sb_dist d, int local_rank, int64_t *lo, int64_t *hi, int *first_replicated);
+int sb_dist_pcg(sb_dist d, const sb_cycle *cp, const double *b, double *x, double tol, int max_iters,
+                sb_report *rep, int device_ptrs);
+int sb_dist_pbicgstab(sb_dist d, const sb_cycle *cp, const double *b, double *x, double tol,
+                      int max_iters, sb_report *rep, int device_ptrs);
+int sb_dist_vcycle(sb_dist d, const sb_cycle *cp, const double *f, double *x);
+double sb_dist_last_solve_ms(sb_dist d);   /* CUDA-event time of the last solve, max over hosted ranks */
+int sb_dist_last_launches(sb_dist d);      /* kernels rank 0 of this process launched in it */
+
 /* ---- problem generators (harness inputs) ------------------- */
 
 /* convdiff2d(nx, ny, bx, by, c) — inc/problems.hpp:28-57, bit-identical.

@@ -80,7 +80,9 @@ EXPORTS = [
     "sb_gen_convdiff2d", "sb_gen_stencil7", "sb_gen_convdiff3d", "sb_gen_stencil27",
     "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_time_kernel", "sb_vcycle_launches", "sb_tail_trace",
     "sb_tail_info", "sb_level_format", "sb_partition", "sb_partition_free", "sb_partition_info",
-    "sb_partition_level", "sb_partition_exchange",
+    "sb_partition_level", "sb_partition_exchange", "sb_nccl_unique_id", "sb_dist_create",
+    "sb_dist_create_local", "sb_dist_destroy", "sb_dist_rows", "sb_dist_pcg", "sb_dist_pbicgstab",
+    "sb_dist_vcycle", "sb_dist_last_solve_ms", "sb_dist_last_launches",
 ]
 
 _P = C.c_void_p
@@ -126,6 +128,16 @@ _SIGS = {
     "sb_level_format": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "sb_partition": (C.c_int, [_P, C.c_int, C.c_int, C.c_int64, C.POINTER(_P)]),
     "sb_partition_free": (None, [_P]),
+    "sb_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "sb_dist_create": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p, C.c_int64, C.POINTER(sb_device_opts), C.POINTER(_P)]),
+    "sb_dist_create_local": (C.c_int, [_P, C.c_int, C.c_int64, C.POINTER(sb_device_opts), C.POINTER(_P)]),
+    "sb_dist_destroy": (None, [_P]),
+    "sb_dist_rows": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
+    "sb_dist_pcg": (C.c_int, [_P, C.POINTER(sb_cycle), _P, _P, C.c_double, C.c_int, C.POINTER(sb_report), C.c_int]),
+    "sb_dist_pbicgstab": (C.c_int, [_P, C.POINTER(sb_cycle), _P, _P, C.c_double, C.c_int, C.POINTER(sb_report), C.c_int]),
+    "sb_dist_vcycle": (C.c_int, [_P, C.POINTER(sb_cycle), _D, _D]),
+    "sb_dist_last_solve_ms": (C.c_double, [_P]),
+    "sb_dist_last_launches": (C.c_int, [_P]),
     "sb_partition_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "sb_partition_level": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int64), C.POINTER(sb_csr),
                                      C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int64)),

@@ -1,0 +1,769 @@
+// Multi-rank solve phase, included at the end of sb_runtime.cu.
+//
+// One device context per rank holds the rank's slice of every distributed
+// level (columns [own | ghost]) and the whole of every replicated level. The
+// V-cycle runs the same bitwise kernels level by level; before every kernel
+// that gathers x the ghost region is refreshed (halo exchange), straddling
+// aggregates exchange residuals / coarse corrections, and at the first
+// replicated level the restricted rhs is gathered so every rank solves the
+// bottom of the hierarchy redundantly (no scatter back). Krylov dot products
+// are rank-local deterministic reductions + an allreduce, after which a
+// one-thread kernel runs the reference's scalar logic on every rank.
+//
+// Two transports:
+//  * NCCL (one rank per process / GPU; libnccl.so.2 loaded with dlopen):
+//    grouped send/recv for exchanges, ncclAllReduce for dots;
+//  * in-process "virtual ranks" (all ranks in this process, one device):
+//    receivers pull peer values with a gather kernel; ordering through CUDA
+//    events. Used to test the partitioned GPU path on a single GPU.
+
+#include <dlfcn.h>
+
+#include <nccl.h>
+
+#include "sb_dist.h"
+
+namespace sb {
+
+// ---- NCCL (dlopen) -------------------------------------------------------------
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi &nccl() {
+    static NcclApi api;
+    if (api.h) return api;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw cuda_error(std::string("libnccl.so.2 not loadable: ") + dlerror());
+    auto sym = [&](const char *n) {
+        void *p = dlsym(h, n);
+        if (!p) throw cuda_error(std::string("NCCL symbol missing: ") + n);
+        return p;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.h = h;
+    return api;
+}
+
+#define NC(x)                                                                                        \
+    do {                                                                                             \
+        ncclResult_t r_ = (x);                                                                       \
+        if (r_ != ncclSuccess) throw sb::cuda_error(std::string(#x) + ": " + nccl().GetErrorString(r_)); \
+    } while (0)
+
+// ---- device kernels of the partitioned path ---------------------------------------
+
+// dst[i] = src[idx[i]] (pack for NCCL / pull from a peer's buffer in-process)
+__global__ void k_gather_idx(int64_t n, const double *__restrict__ src, const int32_t *__restrict__ idx,
+                             double *__restrict__ dst) {
+    pdl_wait();
+    GRID_LOOP(i, n) dst[i] = src[idx[i]];
+}
+
+// restriction of owned coarse rows: members index [own r | r ghosts]
+__global__ void k_restrict_dist(int64_t nc, const int2 *__restrict__ mem, const double *__restrict__ r,
+                                const double *__restrict__ rg, int64_t n_own, double *__restrict__ fc) {
+    pdl_wait();
+    GRID_LOOP(c, nc) {
+        const int2 m = mem[c];
+        double s = __dadd_rn(0.0, m.x < n_own ? r[m.x] : rg[m.x - n_own]);
+        if (m.y >= 0) s = __dadd_rn(s, m.y < n_own ? r[m.y] : rg[m.y - n_own]);
+        fc[c] = s;
+    }
+}
+
+// x_out = x_in + (0.0 + x_c[parent]) with parents in [own coarse | ghosts]
+__global__ void k_prolong_dist(int64_t n, const int32_t *__restrict__ parent, const double *xin,
+                               const double *__restrict__ xc, const double *__restrict__ xcg, int64_t nc_own,
+                               double *xout) {
+    pdl_wait();
+    GRID_LOOP(i, n) {
+        const int64_t p = parent[i];
+        xout[i] = __dadd_rn(xin[i], __dadd_rn(0.0, p < nc_own ? xc[p] : xcg[p - nc_own]));
+    }
+}
+
+// in-process allreduce: every rank sums the ranks' partials in rank order
+__global__ void k_sum_partials(const double *const *parts, int nranks, double *out) {
+    pdl_wait();
+    double a = 0.0, b = 0.0;
+    for (int r = 0; r < nranks; ++r) {
+        a += parts[r][0];
+        b += parts[r][1];
+    }
+    out[0] = a;
+    out[1] = b;
+}
+
+// ---- partitioned device hierarchy --------------------------------------------------
+
+struct DevExch {
+    std::vector<int> send_peers, recv_peers;
+    std::vector<int64_t> send_off, recv_off;
+    int32_t *send_idx = nullptr;  // device
+    double *sendbuf = nullptr;    // device (NCCL packing)
+    int64_t nsend = 0, nrecv = 0;
+};
+
+struct DistLevel {
+    bool dist = false, next_rep = false;
+    int64_t n_own = 0, n_ext = 0, nc_own = 0, c_lo = 0;
+    double *rg = nullptr, *xcg = nullptr;  // residual-partner / coarse-parent ghosts
+    DevExch halo, rx, px;
+    std::vector<int64_t> gather_lo;  // first replicated level: owned pieces per rank
+};
+
+struct RankDev {
+    int rank = 0;
+    sb_ctx c = nullptr;
+    Partition P;
+    std::vector<DistLevel> D;
+    cudaEvent_t ready = nullptr, done = nullptr;
+    double **part_ptrs = nullptr;  // in-process: device array of every rank's st->part
+    int64_t lo = 0, hi = 0;        // owned rows of level 0
+};
+
+} // namespace sb
+
+struct sb_dist_s {
+    std::vector<sb::RankDev> R;  // ranks hosted by this process
+    int nranks = 1, fr = 0;
+    bool local = false;
+    ncclComm_t comm = nullptr;
+    double last_ms = 0.0;
+    int last_launches = 0;
+};
+
+namespace sb {
+
+static DevExch upload_exch(sb_ctx c, const Exchange &e) {
+    DevExch d;
+    d.send_peers = e.send_peers;
+    d.recv_peers = e.recv_peers;
+    d.send_off = e.send_off.empty() ? std::vector<int64_t>{0} : e.send_off;
+    d.recv_off = e.recv_off.empty() ? std::vector<int64_t>{0} : e.recv_off;
+    d.nsend = e.total_send();
+    d.nrecv = e.total_recv();
+    d.send_idx = dalloc<int32_t>(c, std::max<int64_t>(d.nsend, 1), false);
+    if (d.nsend)
+        CK(cudaMemcpy(d.send_idx, e.send_idx.data(), sizeof(int32_t) * e.send_idx.size(), cudaMemcpyHostToDevice));
+    d.sendbuf = dalloc<double>(c, std::max<int64_t>(d.nsend, 1), false);
+    return d;
+}
+
+// Partitioned level: local matrix + [own | ghost] workspaces + plans.
+static void upload_dist_level(sb_ctx c, const PartLevel &pl, DevLevel &D, DistLevel &DL) {
+    upload_matrix(c, pl.A, D);
+    DL.dist = true;
+    DL.n_own = pl.hi - pl.lo;
+    DL.n_ext = pl.A.ncols;
+    DL.nc_own = pl.c_hi - pl.c_lo;
+    DL.c_lo = pl.c_lo;
+    D.nc = DL.nc_own;
+    D.agg = dalloc<int32_t>(c, DL.n_own);  // parents
+    CK(cudaMemcpy(D.agg, pl.parent.data(), sizeof(int32_t) * pl.parent.size(), cudaMemcpyHostToDevice));
+    std::vector<int2> mem(static_cast<size_t>(DL.nc_own));
+    for (size_t q = 0; q < mem.size(); ++q) mem[q] = make_int2(pl.mem0[q], pl.mem1[q]);
+    D.mem = dalloc<int2>(c, std::max<int64_t>(DL.nc_own, 1));
+    CK(cudaMemcpy(D.mem, mem.data(), sizeof(int2) * mem.size(), cudaMemcpyHostToDevice));
+    D.t = dalloc<double>(c, DL.n_ext);
+    D.x = dalloc<double>(c, DL.n_ext);
+    D.f = dalloc<double>(c, DL.n_own);
+    DL.rg = dalloc<double>(c, std::max<int64_t>(static_cast<int64_t>(pl.rghost_glob.size()), 1));
+    DL.xcg = dalloc<double>(c, std::max<int64_t>(static_cast<int64_t>(pl.xcghost_glob.size()), 1));
+    DL.halo = upload_exch(c, pl.halo);
+    DL.rx = upload_exch(c, pl.rx);
+    DL.px = upload_exch(c, pl.px);
+    DL.gather_lo = pl.gather_lo;
+}
+
+// ---- collectives ---------------------------------------------------------------------
+
+static void barrier_local(sb_dist d) {
+    for (auto &r : d->R) CK(cudaEventRecord(r.done, r.c->stream));
+    for (auto &r : d->R)
+        for (auto &q : d->R)
+            if (&q != &r) CK(cudaStreamWaitEvent(r.c->stream, q.done, 0));
+}
+
+// Fill ghost(r) from own(q) of every peer q, per the level-k plan `which`.
+static void exchange(sb_dist d, int k, int which, const std::function<const double *(RankDev &)> &own,
+                     const std::function<double *(RankDev &)> &ghost) {
+    auto plan = [&](RankDev &r) -> DevExch & {
+        DistLevel &L = r.D[static_cast<size_t>(k)];
+        return which == 0 ? L.halo : which == 1 ? L.rx : L.px;
+    };
+    if (d->local) {
+        for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.c->stream));
+        for (auto &r : d->R) {
+            DevExch &e = plan(r);
+            for (size_t j = 0; j < e.recv_peers.size(); ++j) {
+                RankDev &q = d->R[static_cast<size_t>(e.recv_peers[j])];
+                DevExch &eq = plan(q);
+                size_t jj = 0;
+                while (jj < eq.send_peers.size() && eq.send_peers[jj] != r.rank) ++jj;
+                if (jj == eq.send_peers.size()) throw runtime_error("exchange: inconsistent plans");
+                const int64_t cnt = e.recv_off[j + 1] - e.recv_off[j];
+                CK(cudaStreamWaitEvent(r.c->stream, q.ready, 0));
+                launch_k(r.c, k_gather_idx, dim3(vec_grid(cnt)), dim3(kVecThreads), 0, r.c->stream, cnt, own(q),
+                         static_cast<const int32_t *>(eq.send_idx + eq.send_off[jj]), ghost(r) + e.recv_off[j]);
+            }
+        }
+        barrier_local(d);
+        return;
+    }
+    RankDev &r = d->R[0];
+    DevExch &e = plan(r);
+    if (e.nsend == 0 && e.nrecv == 0) return;
+    cudaStream_t s = r.c->stream;
+    if (e.nsend)
+        launch_k(r.c, k_gather_idx, dim3(vec_grid(e.nsend)), dim3(kVecThreads), 0, s, e.nsend, own(r),
+                 static_cast<const int32_t *>(e.send_idx), e.sendbuf);
+    NC(nccl().GroupStart());
+    for (size_t j = 0; j < e.send_peers.size(); ++j)
+        NC(nccl().Send(e.sendbuf + e.send_off[j], static_cast<size_t>(e.send_off[j + 1] - e.send_off[j]), ncclFloat64,
+                       e.send_peers[j], d->comm, s));
+    for (size_t j = 0; j < e.recv_peers.size(); ++j)
+        NC(nccl().Recv(ghost(r) + e.recv_off[j], static_cast<size_t>(e.recv_off[j + 1] - e.recv_off[j]), ncclFloat64,
+                       e.recv_peers[j], d->comm, s));
+    NC(nccl().GroupEnd());
+}
+
+// every rank ends with the whole vector v(r) whose piece [b[q], b[q+1]) rank q owns
+static void allgatherv(sb_dist d, const std::vector<int64_t> &b, const std::function<double *(RankDev &)> &v) {
+    if (d->local) {
+        for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.c->stream));
+        for (auto &r : d->R)
+            for (auto &q : d->R) {
+                if (&q == &r || b[q.rank + 1] == b[q.rank]) continue;
+                CK(cudaStreamWaitEvent(r.c->stream, q.ready, 0));
+                CK(cudaMemcpyAsync(v(r) + b[q.rank], v(q) + b[q.rank],
+                                   sizeof(double) * static_cast<size_t>(b[q.rank + 1] - b[q.rank]),
+                                   cudaMemcpyDeviceToDevice, r.c->stream));
+            }
+        barrier_local(d);
+        return;
+    }
+    RankDev &r = d->R[0];
+    NC(nccl().GroupStart());
+    for (int q = 0; q < d->nranks; ++q) {
+        if (q == r.rank) continue;
+        if (b[r.rank + 1] > b[r.rank])
+            NC(nccl().Send(v(r) + b[r.rank], static_cast<size_t>(b[r.rank + 1] - b[r.rank]), ncclFloat64, q, d->comm,
+                           r.c->stream));
+        if (b[q + 1] > b[q])
+            NC(nccl().Recv(v(r) + b[q], static_cast<size_t>(b[q + 1] - b[q]), ncclFloat64, q, d->comm, r.c->stream));
+    }
+    NC(nccl().GroupEnd());
+}
+
+// st->red = sum over ranks of st->part; then the scalar logic `op` on every rank
+static void allreduce_logic(sb_dist d, int op) {
+    if (d->local) {
+        for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.c->stream));
+        for (auto &r : d->R) {
+            for (auto &q : d->R)
+                if (&q != &r) CK(cudaStreamWaitEvent(r.c->stream, q.ready, 0));
+            launch_k(r.c, k_sum_partials, dim3(1), dim3(1), 0, r.c->stream,
+                     static_cast<const double *const *>(r.part_ptrs), d->nranks, r.c->st->red);
+        }
+        barrier_local(d);
+    } else {
+        RankDev &r = d->R[0];
+        NC(nccl().AllReduce(r.c->st->part, r.c->st->red, 2, ncclFloat64, ncclSum, d->comm, r.c->stream));
+    }
+    for (auto &r : d->R) launch_k(r.c, k_logic, dim3(1), dim3(1), 0, r.c->stream, r.c->st, op);
+}
+
+static Red red_partial(sb_ctx c, int nval, const double *w0 = nullptr, const double *w1 = nullptr) {
+    return make_red(c, EP_PARTIAL, nval, w0, w1);
+}
+
+// ---- distributed V-cycle ------------------------------------------------------------------
+
+// One V-cycle from level k with per-rank rhs f(r) and output X(r) (own rows;
+// X has room for ghosts). Bitwise equal to the single-GPU cycle.
+static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const double *> &f,
+                        const std::vector<double *> &X, bool zero) {
+    const size_t N = d->R.size();
+    if (k >= d->fr) {
+        for (size_t i = 0; i < N; ++i) emit_vcycle(d->R[i].c, d->R[i].c->stream, cp, k, f[i], X[i], zero);
+        return;
+    }
+    std::vector<double *> cur(N), oth(N);
+    auto lev = [&](size_t i) -> DevLevel & { return d->R[i].c->L[static_cast<size_t>(k)]; };
+    auto dl = [&](size_t i) -> DistLevel & { return d->R[i].D[static_cast<size_t>(k)]; };
+    auto halo = [&](std::vector<double *> &v) {
+        std::vector<double *> vv = v;
+        exchange(d, k, 0, [&](RankDev &r) -> const double * { return vv[static_cast<size_t>(&r - d->R.data())]; },
+                 [&](RankDev &r) { return vv[static_cast<size_t>(&r - d->R.data())] + r.D[static_cast<size_t>(k)].n_own; });
+    };
+    auto sweep = [&]() {
+        for (size_t i = 0; i < N; ++i) launch_jacobi(d->R[i].c, lev(i), d->R[i].c->stream, cur[i], f[i], oth[i], cp.omega);
+        std::swap(cur, oth);
+    };
+    for (size_t i = 0; i < N; ++i) {
+        cur[i] = X[i];
+        oth[i] = lev(i).t;
+    }
+    if (zero) {
+        if (cp.pre >= 1) {
+            for (size_t i = 0; i < N; ++i)
+                launch_k(d->R[i].c, k_jacobi_zero, dim3(vec_grid(dl(i).n_own)), dim3(kVecThreads), 0,
+                         d->R[i].c->stream, dl(i).n_own, f[i], static_cast<const double *>(lev(i).diag), cur[i],
+                         cp.omega);
+            for (int s = 1; s < cp.pre; ++s) {
+                halo(cur);
+                sweep();
+            }
+        } else {
+            for (size_t i = 0; i < N; ++i)
+                CK(cudaMemsetAsync(cur[i], 0, sizeof(double) * static_cast<size_t>(dl(i).n_own), d->R[i].c->stream));
+        }
+    } else {
+        for (int s = 0; s < cp.pre; ++s) {
+            halo(cur);
+            sweep();
+        }
+    }
+    // residual, partner residuals, restriction
+    halo(cur);
+    for (size_t i = 0; i < N; ++i)
+        launch_csr<M_RESID, 0>(d->R[i].c, lev(i), d->R[i].c->stream, cur[i], f[i], d->R[i].c->rs, 0.0, nullptr,
+                               Red{});
+    exchange(d, k, 1, [&](RankDev &r) -> const double * { return r.c->rs; },
+             [&](RankDev &r) { return r.D[static_cast<size_t>(k)].rg; });
+    const bool next_rep = k + 1 >= d->fr;
+    for (size_t i = 0; i < N; ++i) {
+        DevLevel &lc = d->R[i].c->L[static_cast<size_t>(k) + 1];
+        double *out = next_rep ? lc.f + dl(i).c_lo : lc.f;
+        launch_k(d->R[i].c, k_restrict_dist, dim3(vec_grid(dl(i).nc_own)), dim3(kVecThreads), 0, d->R[i].c->stream,
+                 dl(i).nc_own, static_cast<const int2 *>(lev(i).mem), static_cast<const double *>(d->R[i].c->rs),
+                 static_cast<const double *>(dl(i).rg), dl(i).n_own, out);
+    }
+    if (next_rep)
+        allgatherv(d, dl(0).gather_lo, [&](RankDev &r) { return r.c->L[static_cast<size_t>(k) + 1].f; });
+    std::vector<const double *> fc(N);
+    std::vector<double *> xc(N);
+    for (size_t i = 0; i < N; ++i) {
+        fc[i] = d->R[i].c->L[static_cast<size_t>(k) + 1].f;
+        xc[i] = d->R[i].c->L[static_cast<size_t>(k) + 1].x;
+    }
+    dist_vcycle(d, cp, k + 1, fc, xc, true);
+    if (!next_rep)
+        exchange(d, k, 2, [&](RankDev &r) -> const double * { return r.c->L[static_cast<size_t>(k) + 1].x; },
+                 [&](RankDev &r) { return r.D[static_cast<size_t>(k)].xcg; });
+    std::vector<double *> pout(N);
+    for (size_t i = 0; i < N; ++i) {
+        pout[i] = (cp.post % 2 == 0) ? X[i] : lev(i).t;
+        const int64_t ncown = next_rep ? (int64_t(1) << 62) : dl(i).nc_own;
+        launch_k(d->R[i].c, k_prolong_dist, dim3(vec_grid(dl(i).n_own)), dim3(kVecThreads), 0, d->R[i].c->stream,
+                 dl(i).n_own, static_cast<const int32_t *>(lev(i).agg), static_cast<const double *>(cur[i]),
+                 static_cast<const double *>(xc[i]), static_cast<const double *>(dl(i).xcg), ncown, pout[i]);
+        cur[i] = pout[i];
+        oth[i] = (pout[i] == X[i]) ? lev(i).t : X[i];
+    }
+    for (int s = 0; s < cp.post; ++s) {
+        halo(cur);
+        sweep();
+    }
+}
+
+// ---- distributed Krylov drivers (host-driven iteration, device scalar logic) ----------------
+
+static int read_done(sb_dist d) {
+    RankDev &r = d->R[0];
+    int done = 0;
+    CK(cudaMemcpyAsync(&done, &r.c->st->done, sizeof(int), cudaMemcpyDeviceToHost, r.c->stream));
+    CK(cudaStreamSynchronize(r.c->stream));
+    return done;
+}
+
+static void dist_halo_vec(sb_dist d, int kv) {
+    exchange(d, 0, 0, [&](RankDev &r) -> const double * { return r.c->kv[kv]; },
+             [&](RankDev &r) { return r.c->kv[kv] + r.D[0].n_own; });
+}
+
+// vectors: KX x, KR r, KZ z, KP p, KAP Ap, KB b (own rows; x / p / pt / st with ghost room)
+static void dist_pcg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
+    const size_t N = d->R.size();
+    auto each = [&](const std::function<void(RankDev &, int64_t)> &fn) {
+        for (auto &r : d->R) fn(r, r.D[0].n_own);
+    };
+    auto precond = [&](int in, int out) {
+        if (cp) {
+            std::vector<const double *> f(N);
+            std::vector<double *> X(N);
+            for (size_t i = 0; i < N; ++i) {
+                f[i] = d->R[i].c->kv[in];
+                X[i] = d->R[i].c->kv[out];
+            }
+            dist_vcycle(d, *cp, 0, f, X, true);
+        } else {
+            each([&](RankDev &r, int64_t n) {
+                CK(cudaMemcpyAsync(r.c->kv[out], r.c->kv[in], sizeof(double) * n, cudaMemcpyDeviceToDevice, r.c->stream));
+            });
+        }
+    };
+    each([&](RankDev &r, int64_t n) {
+        launch_k(r.c, k_init, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+                 static_cast<const double *>(r.c->kv[KB]), r.c->kv[KX], r.c->kv[KR], red_partial(r.c, 1));
+    });
+    allreduce_logic(d, EP_INIT_NORM);
+    if (!read_done(d)) {
+        precond(KR, KZ);
+        each([&](RankDev &r, int64_t n) {
+            launch_k(r.c, k_copy_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+                     static_cast<const double *>(r.c->kv[KZ]), r.c->kv[KP], static_cast<double *>(nullptr),
+                     static_cast<const double *>(r.c->kv[KR]), red_partial(r.c, 1));
+        });
+        allreduce_logic(d, EP_PCG_RZ0);
+        for (int j = 0; j < max_iters; ++j) {
+            dist_halo_vec(d, KP);
+            each([&](RankDev &r, int64_t) {
+                launch_csr<M_SPMV, 1>(r.c, r.c->L[0], r.c->stream, r.c->kv[KP], nullptr, r.c->kv[KAP], 0.0, nullptr,
+                                      red_partial(r.c, 1, r.c->kv[KP]));
+            });
+            allreduce_logic(d, EP_PCG_PAP);
+            each([&](RankDev &r, int64_t n) {
+                launch_k(r.c, k_pcg_update, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n, r.c->kv[KX],
+                         r.c->kv[KR], static_cast<const double *>(r.c->kv[KP]),
+                         static_cast<const double *>(r.c->kv[KAP]), red_partial(r.c, 1));
+            });
+            allreduce_logic(d, EP_PCG_RN);
+            if (read_done(d)) break;
+            precond(KR, KZ);
+            each([&](RankDev &r, int64_t n) {
+                launch_k(r.c, k_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+                         static_cast<const double *>(r.c->kv[KR]), static_cast<const double *>(r.c->kv[KZ]),
+                         static_cast<const int *>(nullptr), red_partial(r.c, 1));
+            });
+            allreduce_logic(d, EP_PCG_RZ);
+            each([&](RankDev &r, int64_t n) {
+                launch_k(r.c, k_xpay, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+                         static_cast<const double *>(r.c->kv[KZ]), r.c->kv[KP],
+                         static_cast<const DevState *>(r.c->st));
+            });
+        }
+    }
+    // true residual
+    dist_halo_vec(d, KX);
+    each([&](RankDev &r, int64_t) {
+        launch_csr<M_RESID, 1>(r.c, r.c->L[0], r.c->stream, r.c->kv[KX], r.c->kv[KB], r.c->rs, 0.0, nullptr,
+                               red_partial(r.c, 1));
+    });
+    allreduce_logic(d, EP_STORE);
+}
+
+static void dist_bicg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
+    const size_t N = d->R.size();
+    auto each = [&](const std::function<void(RankDev &, int64_t)> &fn) {
+        for (auto &r : d->R) fn(r, r.D[0].n_own);
+    };
+    auto precond = [&](int in, int out) {
+        if (cp) {
+            std::vector<const double *> f(N);
+            std::vector<double *> X(N);
+            for (size_t i = 0; i < N; ++i) {
+                f[i] = d->R[i].c->kv[in];
+                X[i] = d->R[i].c->kv[out];
+            }
+            dist_vcycle(d, *cp, 0, f, X, true);
+        } else {
+            each([&](RankDev &r, int64_t n) {
+                CK(cudaMemcpyAsync(r.c->kv[out], r.c->kv[in], sizeof(double) * n, cudaMemcpyDeviceToDevice, r.c->stream));
+            });
+        }
+    };
+    auto half = [&]() {
+        each([&](RankDev &r, int64_t n) {
+            launch_k(r.c, k_bi_half, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n, r.c->kv[KX],
+                     static_cast<const double *>(r.c->kv[KPT]), static_cast<const DevState *>(r.c->st));
+        });
+    };
+    each([&](RankDev &r, int64_t n) {
+        launch_k(r.c, k_init, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+                 static_cast<const double *>(r.c->kv[KB]), r.c->kv[KX], r.c->kv[KR], red_partial(r.c, 1));
+    });
+    allreduce_logic(d, EP_INIT_NORM);
+    if (!read_done(d)) {
+        each([&](RankDev &r, int64_t n) {
+            launch_k(r.c, k_copy_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+                     static_cast<const double *>(r.c->kv[KR]), r.c->kv[KRBAR], r.c->kv[KP],
+                     static_cast<const double *>(r.c->kv[KR]), red_partial(r.c, 1));
+        });
+        allreduce_logic(d, EP_BI_RHO0);
+        for (int j = 0; j < max_iters && !read_done(d); ++j) {
+            precond(KP, KPT);
+            dist_halo_vec(d, KPT);
+            each([&](RankDev &r, int64_t) {
+                launch_csr<M_SPMV, 1>(r.c, r.c->L[0], r.c->stream, r.c->kv[KPT], nullptr, r.c->kv[KAPT], 0.0, nullptr,
+                                      red_partial(r.c, 1, r.c->kv[KRBAR]));
+            });
+            allreduce_logic(d, EP_BI_DENOM);
+            each([&](RankDev &r, int64_t n) {
+                launch_k(r.c, k_bi_s, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+                         static_cast<const double *>(r.c->kv[KR]), static_cast<const double *>(r.c->kv[KAPT]),
+                         r.c->kv[KS], red_partial(r.c, 1));
+            });
+            allreduce_logic(d, EP_BI_SN);
+            half();
+            if (read_done(d)) break;
+            precond(KS, KST);
+            dist_halo_vec(d, KST);
+            each([&](RankDev &r, int64_t) {
+                launch_csr<M_SPMV, 2>(r.c, r.c->L[0], r.c->stream, r.c->kv[KST], nullptr, r.c->kv[KAST], 0.0, nullptr,
+                                      red_partial(r.c, 2, nullptr, r.c->kv[KS]));
+            });
+            allreduce_logic(d, EP_BI_AS);
+            each([&](RankDev &r, int64_t n) {
+                launch_k(r.c, k_bi_update, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n, r.c->kv[KX],
+                         r.c->kv[KR], static_cast<const double *>(r.c->kv[KPT]),
+                         static_cast<const double *>(r.c->kv[KST]), static_cast<const double *>(r.c->kv[KS]),
+                         static_cast<const double *>(r.c->kv[KAST]), static_cast<const double *>(r.c->kv[KRBAR]),
+                         red_partial(r.c, 2));
+            });
+            allreduce_logic(d, EP_BI_RN_RHO);
+            each([&](RankDev &r, int64_t n) {
+                launch_k(r.c, k_bi_p, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+                         static_cast<const double *>(r.c->kv[KR]), r.c->kv[KP],
+                         static_cast<const double *>(r.c->kv[KAPT]), static_cast<const DevState *>(r.c->st));
+            });
+        }
+    }
+    dist_halo_vec(d, KX);
+    each([&](RankDev &r, int64_t) {
+        launch_csr<M_RESID, 1>(r.c, r.c->L[0], r.c->stream, r.c->kv[KX], r.c->kv[KB], r.c->rs, 0.0, nullptr,
+                               red_partial(r.c, 1));
+    });
+    allreduce_logic(d, EP_STORE);
+}
+
+// ---- construction ------------------------------------------------------------------------------
+
+static void build_rank(sb_dist d, RankDev &R, const Hier &h, int rank, int64_t gather_rows,
+                       const sb_device_opts &o) {
+    R.rank = rank;
+    R.P = build_partition(h, rank, d->nranks, gather_rows);
+    d->fr = R.P.first_replicated;
+    sb_ctx c = ctx_begin(o);
+    R.c = c;
+    const int L = static_cast<int>(h.levels.size());
+    c->L.resize(static_cast<size_t>(L));
+    R.D.resize(static_cast<size_t>(L));
+    for (int k = 0; k < L; ++k) {
+        if (k < d->fr) upload_dist_level(c, R.P.L[static_cast<size_t>(k)], c->L[static_cast<size_t>(k)], R.D[k]);
+        else upload_level(c, h.levels[static_cast<size_t>(k)], c->L[static_cast<size_t>(k)], k + 1 == L, -1);
+    }
+    const int64_t nvec = d->fr > 0 ? R.D[0].n_ext : h.levels[0].A.n;
+    if (d->fr == 0) R.D[0].n_own = R.D[0].n_ext = h.levels[0].A.n;
+    R.lo = R.P.L[0].lo;
+    R.hi = R.P.L[0].hi;
+    ctx_finish(c, h, o, nvec, d->fr);
+    CK(cudaEventCreateWithFlags(&R.ready, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&R.done, cudaEventDisableTiming));
+}
+
+static int run_dist(sb_dist d, SolveKind kind, const sb_cycle *cpa, const double *b, double *x, double tol,
+                    int max_iters, sb_report *rep, bool device_ptrs) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const char *who = kind == K_PCG ? "pcg" : "pbicgstab";
+    if (!(tol > 0.0)) throw invalid_argument(std::string(who) + ": tol must be > 0");
+    Cyc cyc;
+    const Cyc *cp = nullptr;
+    if (cpa) {
+        for (auto &r : d->R) cyc = check_cycle(r.c, cpa, who);
+        cp = &cyc;
+    }
+    for (auto &r : d->R) {
+        CK(cudaSetDevice(r.c->device));
+        ensure_hist(r.c, std::max(max_iters, 0) + 2);
+        DevState hs;
+        std::memset(&hs, 0, sizeof(hs));
+        hs.tol = tol;
+        hs.max_iters = max_iters;
+        hs.hist_cap = r.c->hist_cap;
+        hs.hist_r = r.c->hist_r;
+        hs.hist_t = r.c->hist_t;
+        CK(cudaMemcpyAsync(r.c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, r.c->stream));
+        // b: in-process mode takes the global vector, NCCL mode the rank's slice
+        const double *src = d->local ? b + r.lo : b;
+        CK(cudaMemcpyAsync(r.c->kv[KB], src, sizeof(double) * static_cast<size_t>(r.hi - r.lo),
+                           device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, r.c->stream));
+    }
+    RankDev &r0 = d->R[0];
+    for (auto &r : d->R) r.c->launch_count = 0;
+    for (auto &r : d->R) CK(cudaEventRecord(r.c->ev0, r.c->stream));
+    if (kind == K_PCG) dist_pcg(d, cp, tol, max_iters);
+    else dist_bicg(d, cp, tol, max_iters);
+    for (auto &r : d->R) CK(cudaEventRecord(r.c->ev1, r.c->stream));
+    DevState hs;
+    for (auto &r : d->R) {
+        double *dst = d->local ? x + r.lo : x;
+        CK(cudaMemcpyAsync(dst, r.c->kv[KX], sizeof(double) * static_cast<size_t>(r.hi - r.lo),
+                           device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, r.c->stream));
+    }
+    CK(cudaMemcpyAsync(&hs, r0.c->st, sizeof(hs), cudaMemcpyDeviceToHost, r0.c->stream));
+    float ms_max = 0.f;
+    for (auto &r : d->R) {
+        CK(cudaStreamSynchronize(r.c->stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.c->ev0, r.c->ev1));
+        ms_max = std::max(ms_max, ms);
+    }
+    d->last_ms = ms_max;
+    d->last_launches = r0.c->launch_count;
+    if (rep) {
+        rep->iterations = hs.iter;
+        rep->termination = hs.term;
+        rep->true_residual = hs.true_res;
+        rep->hist_len = hs.iter + 1;
+        const int m = std::min(rep->hist_len, std::max(rep->hist_cap, 0));
+        if (m > 0 && rep->residual_history)
+            CK(cudaMemcpy(rep->residual_history, r0.c->hist_r, sizeof(double) * m, cudaMemcpyDeviceToHost));
+        if (m > 0 && rep->time_history)
+            CK(cudaMemcpy(rep->time_history, r0.c->hist_t, sizeof(double) * m, cudaMemcpyDeviceToHost));
+        rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return SB_OK;
+}
+
+} // namespace sb
+
+extern "C" {
+
+int sb_nccl_unique_id(unsigned char *out) {
+    return guard([&] {
+        ncclUniqueId id;
+        NC(nccl().GetUniqueId(&id));
+        std::memcpy(out, id.internal, sizeof(id.internal));
+    });
+}
+
+int sb_dist_create(sb_hier hh, int rank, int nranks, const unsigned char *nccl_id, int64_t gather_rows,
+                   const sb_device_opts *opts, sb_dist *out) {
+    sb_dist d = nullptr;
+    const int rc = guard([&] {
+        Hier *h = hier_of(hh);
+        if (!h || !out || !nccl_id) throw invalid_argument("sb_dist_create: null argument");
+        sb_device_opts o{0, 1, -1, 0};
+        if (opts) o = *opts;
+        d = new sb_dist_s;
+        d->nranks = nranks;
+        d->local = false;
+        d->R.resize(1);
+        build_rank(d, d->R[0], *h, rank, gather_rows, o);
+        ncclUniqueId id;
+        std::memcpy(id.internal, nccl_id, sizeof(id.internal));
+        CK(cudaSetDevice(o.device));
+        NC(nccl().CommInitRank(&d->comm, nranks, id, rank));
+        *out = d;
+    });
+    if (rc != SB_OK && d) sb_dist_destroy(d);
+    return rc;
+}
+
+int sb_dist_create_local(sb_hier hh, int nranks, int64_t gather_rows, const sb_device_opts *opts, sb_dist *out) {
+    sb_dist d = nullptr;
+    const int rc = guard([&] {
+        Hier *h = hier_of(hh);
+        if (!h || !out || nranks < 1) throw invalid_argument("sb_dist_create_local: bad argument");
+        sb_device_opts o{0, 1, -1, 0};
+        if (opts) o = *opts;
+        d = new sb_dist_s;
+        d->nranks = nranks;
+        d->local = true;
+        d->R.resize(static_cast<size_t>(nranks));
+        for (int r = 0; r < nranks; ++r) build_rank(d, d->R[static_cast<size_t>(r)], *h, r, gather_rows, o);
+        std::vector<double *> parts(static_cast<size_t>(nranks));
+        for (int r = 0; r < nranks; ++r) parts[static_cast<size_t>(r)] = d->R[static_cast<size_t>(r)].c->st->part;
+        for (auto &r : d->R) {
+            r.part_ptrs = dalloc<double *>(r.c, nranks, false);
+            CK(cudaMemcpy(r.part_ptrs, parts.data(), sizeof(double *) * parts.size(), cudaMemcpyHostToDevice));
+        }
+        *out = d;
+    });
+    if (rc != SB_OK && d) sb_dist_destroy(d);
+    return rc;
+}
+
+void sb_dist_destroy(sb_dist d) {
+    if (!d) return;
+    if (d->comm) nccl().CommDestroy(d->comm);
+    for (auto &r : d->R) {
+        if (r.ready) cudaEventDestroy(r.ready);
+        if (r.done) cudaEventDestroy(r.done);
+        if (r.c) sb_destroy(r.c);
+    }
+    delete d;
+}
+
+int sb_dist_rows(sb_dist d, int local_rank, int64_t *lo, int64_t *hi, int *first_replicated) {
+    return guard([&] {
+        if (!d || local_rank < 0 || local_rank >= static_cast<int>(d->R.size()))
+            throw invalid_argument("sb_dist_rows: bad rank");
+        *lo = d->R[static_cast<size_t>(local_rank)].lo;
+        *hi = d->R[static_cast<size_t>(local_rank)].hi;
+        if (first_replicated) *first_replicated = d->fr;
+    });
+}
+
+int sb_dist_pcg(sb_dist d, const sb_cycle *cp, const double *b, double *x, double tol, int max_iters,
+                sb_report *rep, int device_ptrs) {
+    return guard([&] { run_dist(d, K_PCG, cp, b, x, tol, max_iters, rep, device_ptrs != 0); });
+}
+
+int sb_dist_pbicgstab(sb_dist d, const sb_cycle *cp, const double *b, double *x, double tol, int max_iters,
+                      sb_report *rep, int device_ptrs) {
+    return guard([&] { run_dist(d, K_BICG, cp, b, x, tol, max_iters, rep, device_ptrs != 0); });
+}
+
+int sb_dist_vcycle(sb_dist d, const sb_cycle *cpa, const double *f, double *x) {
+    return guard([&] {
+        Cyc cp;
+        for (auto &r : d->R) cp = check_cycle(r.c, cpa, "vcycle");
+        const size_t N = d->R.size();
+        std::vector<const double *> fv(N);
+        std::vector<double *> xv(N);
+        for (size_t i = 0; i < N; ++i) {
+            RankDev &r = d->R[i];
+            CK(cudaSetDevice(r.c->device));
+            const double *src = d->local ? f + r.lo : f;
+            CK(cudaMemcpyAsync(r.c->kv[KB], src, sizeof(double) * static_cast<size_t>(r.hi - r.lo),
+                               cudaMemcpyHostToDevice, r.c->stream));
+            fv[i] = r.c->kv[KB];
+            xv[i] = r.c->kv[KZ];
+        }
+        dist_vcycle(d, cp, 0, fv, xv, true);
+        for (size_t i = 0; i < N; ++i) {
+            RankDev &r = d->R[i];
+            double *dst = d->local ? x + r.lo : x;
+            CK(cudaMemcpyAsync(dst, r.c->kv[KZ], sizeof(double) * static_cast<size_t>(r.hi - r.lo),
+                               cudaMemcpyDeviceToHost, r.c->stream));
+        }
+        for (auto &r : d->R) CK(cudaStreamSynchronize(r.c->stream));
+    });
+}
+
+double sb_dist_last_solve_ms(sb_dist d) { return d ? d->last_ms : 0.0; }
+int sb_dist_last_launches(sb_dist d) { return d ? d->last_launches : 0; }
+
+} // extern "C"

@@ -28,6 +28,8 @@ constexpr int kVecThreads = 256;
 struct DevState {
     double tol, r0, rn, rz, pAp, alpha, beta;
     double rho, denom, omega, sn, true_res;
+    double part[2];  // multi-rank: this rank's reduction totals
+    double red[2];   // multi-rank: allreduced totals
     int iter, max_iters, done, term, status, half, hist_cap, pad_;
     unsigned long long t0;
     double *hist_r;
@@ -48,6 +50,7 @@ enum EpOp : int {
     EP_BI_AS,        // a = (As,As), b = (As,s); breakdown or omega
     EP_BI_RN_RHO,    // rn = sqrt(a), rho' = b; stop tests; beta; rho
     EP_AMG_RN,       // amg_solve: rn, record, divergence / convergence
+    EP_PARTIAL,      // multi-rank: store this rank's totals (logic runs after the allreduce)
 };
 
 // Conditional-handle set performed by a reduction epilogue: every listed

@@ -122,11 +122,14 @@ __device__ __forceinline__ void record(DevState *st, int k, double v) {
 
 // Krylov scalar logic; runs in ONE thread after the grid-wide reduction.
 // Each case restates the reference's scalar control flow (file:line noted).
-__device__ void epilogue(const Red &r, double a, double b) {
-    DevState *st = r.st;
+__device__ void epilogue_logic(DevState *st, int op, double a, double b) {
     constexpr double eps = 1e-300;  // krylov.hpp:130
     constexpr double divf = 1e6;    // krylov.hpp:26
-    switch (r.op) {
+    switch (op) {
+    case EP_PARTIAL:  // multi-rank: this rank's share, allreduced before the logic runs
+        st->part[0] = a;
+        st->part[1] = b;
+        break;
     case EP_STORE:
         st->true_res = sqrt(a);
         break;
@@ -276,9 +279,19 @@ __device__ void epilogue(const Red &r, double a, double b) {
     default:
         break;
     }
+}
+
+__device__ void epilogue(const Red &r, double a, double b) {
+    epilogue_logic(r.st, r.op, a, b);
     for (int i = 0; i < r.cs.n; ++i)
         cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(r.cs.h[i]),
-                                st->done ? 0u : 1u);
+                                r.st->done ? 0u : 1u);
+}
+
+// Multi-rank: the scalar logic on the allreduced totals (st->red).
+__global__ void k_logic(DevState *st, int op) {
+    pdl_wait();
+    epilogue_logic(st, op, st->red[0], st->red[1]);
 }
 
 // Grid-wide deterministic reduction + epilogue. Every thread of every block
@@ -1247,6 +1260,7 @@ struct sb_ctx_s {
     int tail_from = 1 << 30;  // first level run inside the cluster tail kernel
     int tail_ctas = 0;
     int tail_smem = 0;
+    int tail_min = 0;  // the tail never starts above this level (partitioned levels)
     unsigned long long *trace = nullptr;  // SB_TAIL_TRACE=1: per-phase timestamps of the tail
     bool pdl = true;                      // programmatic dependent launch in the V-cycle (SB_PDL=0 off)
     sb::TailDesc *tail = nullptr;
@@ -1641,8 +1655,10 @@ static void make_tiles(const HostCsr &A, std::vector<int32_t> &tiles, int &cap) 
     }
 }
 
-static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarsest, int64_t n0) {
-    const HostCsr &A = H.A;
+// Matrix part of a level: raw CSR, diagonal, tiles, lossless streamed format
+// (dictionary values / int16 column deltas), sliced-ELL slices. Columns need
+// not be sorted (partitioned levels number ghosts after own rows).
+static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
     if (A.nnz() > INT32_MAX - 16 || A.n > INT32_MAX - 1)
         throw invalid_argument("sb_create: level too large for int32 device offsets");
     D.n = A.n;
@@ -1659,12 +1675,13 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
     std::vector<double> diag(static_cast<size_t>(A.n), 0.0);
     D.bad_diag = -1;
     for (int64_t i = 0; i < A.n; ++i) {
-        const auto *b = A.ci.data() + A.rp[i], *e = A.ci.data() + A.rp[i + 1];
-        const auto *it = std::lower_bound(b, e, static_cast<int32_t>(i));
-        if (it == e || *it != i || A.v[static_cast<size_t>(it - A.ci.data())] == 0.0) {
+        int64_t pos = -1;
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k)
+            if (A.ci[k] == i) pos = k;
+        if (pos < 0 || A.v[pos] == 0.0) {
             if (D.bad_diag < 0) D.bad_diag = i;
         } else {
-            diag[i] = A.v[static_cast<size_t>(it - A.ci.data())];
+            diag[i] = A.v[pos];
         }
     }
     D.diag = dalloc<double>(c, A.n);
@@ -1818,6 +1835,11 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
             D.sell_smem = kSellStages * stage;
         }
     }
+}
+
+static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarsest, int64_t n0) {
+    const HostCsr &A = H.A;
+    upload_matrix(c, A, D);
     if (!coarsest) {
         D.nc = H.n_coarse;
         D.agg = dalloc<int32_t>(c, A.n);
@@ -1930,7 +1952,8 @@ static void setup_tail(sb_ctx c, const Hier &H) {
     const int rows_c = (nc + ctas - 1) / ctas;
     int total = align16(8 * rows_c * nc) + align16(8 * nc) + align16(8 * rows_c) * 2;
     int k0 = L - 1;
-    while (k0 > 0) {
+    if (k0 < c->tail_min) return;
+    while (k0 > c->tail_min) {
         int rp_, nz_;
         const int add = level_bytes(k0 - 1, rp_, nz_);
         if (total + add > budget || c->L[static_cast<size_t>(k0) - 1].n > tail_rows ||
@@ -2129,6 +2152,82 @@ static void d2h(sb_ctx c, double *h, const double *d, int64_t n) {
 
 } // namespace sb
 
+namespace sb {
+
+// Context creation, split so the multi-rank path (sb_distrun.cuh) can upload
+// partitioned levels in between.
+static sb_ctx ctx_begin(const sb_device_opts &o) {
+    if (o.host_levels_from >= 0)
+        throw invalid_argument("sb_create: hybrid host-level placement is not available in this build");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (o.device < 0 || o.device >= ndev) throw invalid_argument("sb_create: no such CUDA device");
+    CK(cudaSetDevice(o.device));
+    sb_ctx c = new sb_ctx_s;
+    c->device = o.device;
+    c->graphs = o.use_graphs != 0;
+    if (const char *e = std::getenv("SB_PDL")) c->pdl = std::atoi(e) != 0;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    for (auto &s : c->cap) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return c;
+}
+
+// Launch configuration, coarse inverse, workspaces (n_vec = length of the
+// Krylov / scratch vectors: n0, or own + ghost rows on a partitioned level 0),
+// the cluster tail (only over levels >= tail_min).
+static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t n_vec, int tail_min) {
+    size_t max_smem = 0;
+    for (auto &l : c->L) max_smem = std::max(max_smem, std::max(l.smem, l.sell_smem));
+    if (max_smem > 200 * 1024) throw invalid_argument("sb_create: tile staging exceeds shared memory");
+    set_smem_attr<M_SPMV, 0>(max_smem);
+    set_smem_attr<M_SPMV, 1>(max_smem);
+    set_smem_attr<M_SPMV, 2>(max_smem);
+    set_smem_attr<M_RESID, 0>(max_smem);
+    set_smem_attr<M_RESID, 1>(max_smem);
+    set_smem_attr<M_JACOBI, 0>(max_smem);
+    set_smem_attr<M_JACOBI_ZERO, 0>(max_smem);
+    set_smem_attr<M_JACOBI_PROLONG, 0>(max_smem);
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
+    for (auto &l : c->L) {
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tile<M_JACOBI, 0, 0, 0>, kTileRows, l.smem));
+        l.grid = std::max(1, nsm * std::max(occ, 1));
+        if (l.sell) {
+            occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell_tile<M_JACOBI, 0, 1, 1>, kTileRows,
+                                                             l.sell_smem));
+            l.sell_grid = std::max(1, nsm * std::max(occ, 1));
+        }
+    }
+    c->nc = h.nc;
+    if (h.nc > 0) {
+        c->inv = dalloc<double>(c, h.nc * h.nc);
+        CK(cudaMemcpy(c->inv, h.inv.data(), sizeof(double) * h.inv.size(), cudaMemcpyHostToDevice));
+        c->coarse_exact = o.coarse_exact != 0;
+        if (c->coarse_exact) {
+            c->lu = dalloc<double>(c, h.nc * h.nc);
+            c->perm = dalloc<int32_t>(c, h.nc);
+            CK(cudaMemcpy(c->lu, h.lu.data(), sizeof(double) * h.lu.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(c->perm, h.perm.data(), sizeof(int32_t) * h.perm.size(), cudaMemcpyHostToDevice));
+        }
+    }
+    c->rs = dalloc<double>(c, n_vec);
+    c->tail_min = tail_min;
+    setup_tail(c, h);
+    for (auto &v : c->kv) v = dalloc<double>(c, n_vec);
+    int maxb = 148 * 8;
+    for (auto &l : c->L) maxb = std::max(maxb, l.ntiles);
+    c->partials = dalloc<double>(c, 2 * static_cast<int64_t>(maxb) + 2, false);
+    c->counter = dalloc<unsigned>(c, 4, false);
+    c->st = dalloc<DevState>(c, 1, false);
+    CK(cudaDeviceSynchronize());
+}
+
+} // namespace sb
+
 extern "C" {
 
 const char *sb_last_error(void) { return sb::g_err.c_str(); }
@@ -2141,70 +2240,12 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
         if (!h || !out) throw invalid_argument("sb_create: null argument");
         sb_device_opts o{0, 1, -1, 0};
         if (opts) o = *opts;
-        if (o.host_levels_from >= 0)
-            throw invalid_argument("sb_create: hybrid host-level placement is not available in this build");
-        int ndev = 0;
-        CK(cudaGetDeviceCount(&ndev));
-        if (o.device < 0 || o.device >= ndev) throw invalid_argument("sb_create: no such CUDA device");
-        CK(cudaSetDevice(o.device));
-        c = new sb_ctx_s;
-        c->device = o.device;
-        c->graphs = o.use_graphs != 0;
-        if (const char *e = std::getenv("SB_PDL")) c->pdl = std::atoi(e) != 0;
-        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        CK(cudaEventCreate(&c->ev0));
-        CK(cudaEventCreate(&c->ev1));
-        for (auto &s : c->cap) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        c = ctx_begin(o);
         const int64_t n0 = h->levels[0].A.n;
         c->L.resize(h->levels.size());
-        size_t max_smem = 0;
-        for (size_t k = 0; k < h->levels.size(); ++k) {
+        for (size_t k = 0; k < h->levels.size(); ++k)
             upload_level(c, h->levels[k], c->L[k], k + 1 == h->levels.size(), n0);
-            max_smem = std::max(max_smem, std::max(c->L[k].smem, c->L[k].sell_smem));
-        }
-        if (max_smem > 200 * 1024) throw invalid_argument("sb_create: tile staging exceeds shared memory");
-        set_smem_attr<M_SPMV, 0>(max_smem);
-        set_smem_attr<M_SPMV, 1>(max_smem);
-        set_smem_attr<M_SPMV, 2>(max_smem);
-        set_smem_attr<M_RESID, 0>(max_smem);
-        set_smem_attr<M_RESID, 1>(max_smem);
-        set_smem_attr<M_JACOBI, 0>(max_smem);
-        set_smem_attr<M_JACOBI_ZERO, 0>(max_smem);
-        set_smem_attr<M_JACOBI_PROLONG, 0>(max_smem);
-        int nsm = 0;
-        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
-        for (auto &l : c->L) {
-            int occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_tile<M_JACOBI, 0, 0, 0>, kTileRows, l.smem));
-            l.grid = std::max(1, nsm * std::max(occ, 1));
-            if (l.sell) {
-                occ = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell_tile<M_JACOBI, 0, 1, 1>, kTileRows,
-                                                                 l.sell_smem));
-                l.sell_grid = std::max(1, nsm * std::max(occ, 1));
-            }
-        }
-        c->nc = h->nc;
-        if (h->nc > 0) {
-            c->inv = dalloc<double>(c, h->nc * h->nc);
-            CK(cudaMemcpy(c->inv, h->inv.data(), sizeof(double) * h->inv.size(), cudaMemcpyHostToDevice));
-            c->coarse_exact = o.coarse_exact != 0;
-            if (c->coarse_exact) {
-                c->lu = dalloc<double>(c, h->nc * h->nc);
-                c->perm = dalloc<int32_t>(c, h->nc);
-                CK(cudaMemcpy(c->lu, h->lu.data(), sizeof(double) * h->lu.size(), cudaMemcpyHostToDevice));
-                CK(cudaMemcpy(c->perm, h->perm.data(), sizeof(int32_t) * h->perm.size(), cudaMemcpyHostToDevice));
-            }
-        }
-        c->rs = dalloc<double>(c, n0);
-        setup_tail(c, *h);
-        for (auto &v : c->kv) v = dalloc<double>(c, n0);
-        int maxb = 148 * 8;
-        for (auto &l : c->L) maxb = std::max(maxb, l.ntiles);
-        c->partials = dalloc<double>(c, 2 * static_cast<int64_t>(maxb) + 2, false);
-        c->counter = dalloc<unsigned>(c, 4, false);
-        c->st = dalloc<DevState>(c, 1, false);
-        CK(cudaDeviceSynchronize());
+        ctx_finish(c, *h, o, n0, 0);
         *out = c;
     });
     if (rc != SB_OK && c) sb_destroy(c);
@@ -2477,3 +2518,5 @@ int sb_coarse_solve(sb_ctx c, const double *f, double *x) {
 }
 
 } // extern "C"
+
+#include "sb_distrun.cuh"

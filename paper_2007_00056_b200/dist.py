@@ -13,7 +13,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import check
-from .sparsh import Hierarchy, _from_abi
+from .sparsh import CycleParams, Hierarchy, SolveResult, _from_abi, _report
 
 
 class Partition:
@@ -71,3 +71,80 @@ class Partition:
         return dict(send_peers=arr(sp_, ns, np.int32), send_off=arr(so, ns + 1, np.int64),
                     send_idx=arr(si, ts, np.int32), recv_peers=arr(rp_, nr, np.int32),
                     recv_off=arr(ro, nr + 1, np.int64))
+
+
+class DistSolver:
+    """Partitioned device solve (C ABI sb_dist_*).
+
+    local=True: `nranks` virtual ranks inside this process on one GPU (the
+    exchanges are peer-buffer gathers) — b / x are GLOBAL vectors.
+    local=False: this process is rank `rank` of `nranks` (one GPU each, NCCL);
+    `nccl_id` is the 128-byte id from rank 0 (``nccl_unique_id()``); b / x are
+    this rank's rows [lo, hi)."""
+
+    def __init__(self, h: Hierarchy, nranks: int, gather_rows: int = 65536, *, local: bool = True,
+                 rank: int = 0, nccl_id: bytes = None, device: int = 0):
+        L = _lib.lib()
+        d = C.c_void_p()
+        opts = _lib.sb_device_opts(device, 1, -1, 0)
+        if local:
+            check(L.sb_dist_create_local(h._h, int(nranks), int(gather_rows), C.byref(opts), C.byref(d)))
+        else:
+            check(L.sb_dist_create(h._h, int(rank), int(nranks), nccl_id, int(gather_rows), C.byref(opts),
+                                   C.byref(d)))
+        self._d, self._h, self.local, self.nranks = d, h, local, nranks
+        lo, hi, fr = C.c_int64(), C.c_int64(), C.c_int()
+        check(L.sb_dist_rows(d, 0, C.byref(lo), C.byref(hi), C.byref(fr)))
+        self.lo, self.hi, self.first_replicated = lo.value, hi.value, fr.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "_d", None):
+                _lib.lib().sb_dist_destroy(self._d)
+                self._d = None
+        except Exception:
+            pass
+
+    def vcycle(self, f, p: CycleParams) -> np.ndarray:
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        x = np.zeros_like(f)
+        cp = p._abi()
+        check(_lib.lib().sb_dist_vcycle(self._d, C.byref(cp), _lib.dptr(f), _lib.dptr(x)))
+        return x
+
+    def _solve(self, fn, b, p, tol, max_iters, x_out=None):
+        """b / x_out: numpy arrays (host) or integer device pointers (x_out required)."""
+        cap = max(int(max_iters), 0) + 2
+        hr, ht = np.zeros(cap), np.zeros(cap)
+        rep = _lib.sb_report()
+        rep.hist_cap = cap
+        rep.residual_history = _lib.dptr(hr)
+        rep.time_history = _lib.dptr(ht)
+        cp = p._abi() if p is not None else None
+        if isinstance(b, int):  # device pointers
+            check(fn(self._d, C.byref(cp) if cp is not None else None, C.c_void_p(b), C.c_void_p(x_out),
+                     float(tol), int(max_iters), C.byref(rep), 1))
+            return SolveResult(None, _report(rep, hr, ht))
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b) if x_out is None else x_out
+        check(fn(self._d, C.byref(cp) if cp is not None else None, b.ctypes.data_as(C.c_void_p),
+                 x.ctypes.data_as(C.c_void_p), float(tol), int(max_iters), C.byref(rep), 0))
+        return SolveResult(x, _report(rep, hr, ht))
+
+    def pcg(self, b, p: CycleParams, tol, max_iters, x_out=None) -> SolveResult:
+        return self._solve(_lib.lib().sb_dist_pcg, b, p, tol, max_iters, x_out)
+
+    def pbicgstab(self, b, p: CycleParams, tol, max_iters, x_out=None) -> SolveResult:
+        return self._solve(_lib.lib().sb_dist_pbicgstab, b, p, tol, max_iters, x_out)
+
+    def last_solve_ms(self) -> float:
+        return float(_lib.lib().sb_dist_last_solve_ms(self._d))
+
+    def last_launches(self) -> int:
+        return int(_lib.lib().sb_dist_last_launches(self._d))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(_lib.lib().sb_nccl_unique_id(buf))
+    return buf.raw

@@ -1,0 +1,73 @@
+"""Partitioned (multi-rank) GPU solve on ONE device: N virtual ranks in this
+process, exchanges as peer-buffer gathers (sb_dist_create_local). The
+partitioned V-cycle must be bit-identical to the single-GPU V-cycle; Krylov
+solves (rank-partial dots + allreduce) agree to rounding with the same
+iteration counts."""
+import numpy as np
+import pytest
+
+from helpers import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _cp(sp):
+    return sp.CycleParams(6, 6, sp.SmootherKind.weighted_jacobi())
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 4])
+@pytest.mark.parametrize("mk,gather", [(lambda sp: sp.poisson3d(32), 4096), (lambda sp: sp.poisson2d(96, 70), 1000),
+                                       (lambda sp: sp.convdiff3d(20, 18, 17, 1.0, 100.0, 1.0, 1.0), 2000)])
+def test_dist_vcycle_bitexact(sp, nranks, mk, gather):
+    from paper_2007_00056_b200.dist import DistSolver
+    A = mk(sp)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40))
+    ds = DistSolver(h, nranks, gather)
+    if nranks > 1:
+        assert ds.first_replicated >= 1
+    f = sp.rhs_random(A.nrows(), 42)
+    xd = ds.vcycle(f, _cp(sp))
+    xs = sp.vcycle(h, 0, f, np.zeros(A.nrows()), _cp(sp))
+    assert np.array_equal(xd, xs)
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_dist_pcg_matches_single(sp, nranks):
+    from paper_2007_00056_b200.dist import DistSolver
+    A = sp.poisson3d(40)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40))
+    b = sp.rhs_ones(A.nrows())
+    tol = 1e-8 * np.linalg.norm(b)
+    ds = DistSolver(h, nranks, 8000)
+    rd = ds.pcg(b, _cp(sp), tol, 200)
+    rs = sp.pcg(A, b, sp.make_amg_preconditioner(h, _cp(sp)), tol, 200)
+    assert rd.report.converged() and rd.report.iterations == rs.report.iterations
+    assert rel(rd.x, rs.x) < 1e-12
+    assert len(rd.report.residual_history) == rd.report.iterations + 1
+    assert rd.report.true_residual < 10 * tol
+    assert ds.last_solve_ms() > 0
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_dist_bicgstab_matches_single(sp, nranks):
+    from paper_2007_00056_b200.dist import DistSolver
+    A = sp.convdiff3d(24, 24, 24, 1.0, 100.0, 1.0, 1.0)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40))
+    b = sp.rhs_ones(A.nrows())
+    tol = 1e-8 * np.linalg.norm(b)
+    ds = DistSolver(h, nranks, 2000)
+    rd = ds.pbicgstab(b, _cp(sp), tol, 200)
+    rs = sp.pbicgstab(A, b, sp.make_amg_preconditioner(h, _cp(sp)), tol, 200)
+    assert rd.report.converged() and abs(rd.report.iterations - rs.report.iterations) <= 1
+    assert rel(rd.x, rs.x) < 1e-9
+
+
+def test_dist_identity_cg(sp):
+    from paper_2007_00056_b200.dist import DistSolver
+    A = sp.poisson2d(64, 64)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40))
+    ds = DistSolver(h, 3, 500)
+    b = sp.rhs_ones(A.nrows())
+    rd = ds.pcg(b, None, 1e-300, 7)
+    rs = sp.cg(A, b, 1e-300, 7)
+    assert rd.report.iterations == 7 and rel(rd.x, rs.x) < 1e-12
