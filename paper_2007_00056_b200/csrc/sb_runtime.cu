@@ -1073,6 +1073,7 @@ __global__ void k_coarse_lu_exact(int n, const double *__restrict__ lu, const in
 // x = 0, r = b, ||b||^2 (krylov.hpp:70-79, cycle.hpp:105-111)
 __global__ void k_init(int64_t n, const double *__restrict__ b, double *__restrict__ x,
                        double *__restrict__ r, Red red) {
+    pdl_wait();  // launched with PDL on the partitioned path
     if (blockIdx.x == 0 && threadIdx.x == 0) red.st->t0 = globaltimer();
     double a[1] = {0.0};
     GRID_LOOP(i, n) {
@@ -1087,6 +1088,7 @@ __global__ void k_init(int64_t n, const double *__restrict__ b, double *__restri
 // dst = src; sum src*w  (PCG: p = z, rz = (r, z); BiCGStab: rbar = p = r, rho = (r, rbar))
 __global__ void k_copy_dot(int64_t n, const double *__restrict__ src, double *__restrict__ dst,
                            double *__restrict__ dst2, const double *__restrict__ w, Red red) {
+    pdl_wait();  // launched with PDL on the partitioned path
     double a[1] = {0.0};
     GRID_LOOP(i, n) {
         const double s = src[i];
@@ -1099,6 +1101,7 @@ __global__ void k_copy_dot(int64_t n, const double *__restrict__ src, double *__
 
 __global__ void k_dot(int64_t n, const double *__restrict__ u, const double *__restrict__ v,
                       const int *skip, Red red) {
+    pdl_wait();  // launched with PDL on the partitioned path
     double a[1] = {0.0};
     if (!(skip && *skip)) {
         GRID_LOOP(i, n) a[0] += u[i] * v[i];
@@ -1109,6 +1112,7 @@ __global__ void k_dot(int64_t n, const double *__restrict__ u, const double *__r
 // PCG update (krylov.hpp:96-98): x += alpha p; r += (-alpha) Ap; ||r||^2
 __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
                              const double *__restrict__ p, const double *__restrict__ Ap, Red red) {
+    pdl_wait();  // launched with PDL on the partitioned path
     double a[1] = {0.0};
     const DevState *st = red.st;
     if (!st->done) {
@@ -1126,6 +1130,7 @@ __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restri
 // p = z + beta p (krylov.hpp:113)
 __global__ void k_xpay(int64_t n, const double *__restrict__ z, double *__restrict__ p,
                        const DevState *__restrict__ st) {
+    pdl_wait();  // launched with PDL on the partitioned path
     const double beta = st->beta;
     GRID_LOOP(i, n) p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
 }
@@ -1133,6 +1138,7 @@ __global__ void k_xpay(int64_t n, const double *__restrict__ z, double *__restri
 // BiCGStab s = r + (-alpha) Ap~; ||s||^2 (krylov.hpp:164-166)
 __global__ void k_bi_s(int64_t n, const double *__restrict__ r, const double *__restrict__ Apt,
                        double *__restrict__ s, Red red) {
+    pdl_wait();  // launched with PDL on the partitioned path
     double a[1] = {0.0};
     const DevState *st = red.st;
     if (!st->done) {
@@ -1149,6 +1155,7 @@ __global__ void k_bi_s(int64_t n, const double *__restrict__ r, const double *__
 // Half-step exit: x += alpha p~ (krylov.hpp:168), only when EP_BI_SN fired.
 __global__ void k_bi_half(int64_t n, double *__restrict__ x, const double *__restrict__ pt,
                           const DevState *__restrict__ st) {
+    pdl_wait();  // launched with PDL on the partitioned path
     if (!st->half) return;
     const double alpha = st->alpha;
     GRID_LOOP(i, n) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pt[i]));
@@ -1159,6 +1166,7 @@ __global__ void k_bi_update(int64_t n, double *__restrict__ x, double *__restric
                             const double *__restrict__ pt, const double *__restrict__ st_,
                             const double *__restrict__ s, const double *__restrict__ Ast,
                             const double *__restrict__ rbar, Red red) {
+    pdl_wait();  // launched with PDL on the partitioned path
     double a[2] = {0.0, 0.0};
     const DevState *st = red.st;
     if (!st->done) {
@@ -1178,6 +1186,7 @@ __global__ void k_bi_update(int64_t n, double *__restrict__ x, double *__restric
 // p = r + beta (p - omega Ap~)  (krylov.hpp:204-205)
 __global__ void k_bi_p(int64_t n, const double *__restrict__ r, double *__restrict__ p,
                        const double *__restrict__ Apt, const DevState *__restrict__ st) {
+    pdl_wait();  // launched with PDL on the partitioned path
     if (st->done) return;
     const double beta = st->beta, omega = st->omega;
     GRID_LOOP(i, n)
@@ -1185,10 +1194,12 @@ __global__ void k_bi_p(int64_t n, const double *__restrict__ r, double *__restri
 }
 
 __global__ void k_fill(int64_t n, double *x, double v) {
+    pdl_wait();  // launched with PDL on the partitioned path
     GRID_LOOP(i, n) x[i] = v;
 }
 
 __global__ void k_set_cond(const DevState *st, CondSet cs) {
+    pdl_wait();  // launched with PDL on the partitioned path
     for (int i = 0; i < cs.n; ++i)
         cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(cs.h[i]), st->done ? 0u : 1u);
 }
