@@ -560,71 +560,115 @@ __global__ void __launch_bounds__(kTileRows, 3)
 }
 
 // ===========================================================================
-// Sliced-ELL tile pipeline (the default streamed format of every level whose
-// 256-row slices pad by <= 50%). Slice t holds rows [256t, 256t+256); entry k
-// of all its rows is contiguous (vals[k*256 + lane], cols[k*256 + lane]), so
-// the thread of row r0+t reads conflict-free shared memory at constant
-// strides with a uniform trip count (the slice width w); its own row length
-// (1 byte) predicates the tail. Entry order within a row is the CSR order:
-// sums are bitwise the reference's. Every TMA window is naturally 16-byte
-// aligned (slices start at multiples of 256 entries / rows).
+// Grouped sliced-ELL ("SELL-G") pipeline: the default streamed format of every
+// level whose slices pad by <= 50%. A slice holds H = 256 * RPT consecutive
+// rows; its block in HBM is contiguous and 16-byte aligned:
+//   vals [ng][H][GS]  (uint8 dictionary indices, or f64 values)
+//   cols [ng][H][GS]  (int16 column - row deltas, or int32 columns)
+//   meta [H] uint16   row length | (dictionary index of a_ii, or its slot) << 8
+// so thread t reads GS consecutive entries of its row with ONE vector LDS per
+// array (conflict-free) and the whole block arrives with ONE TMA bulk copy.
+// Entries of a row keep the CSR order; slots >= the row length are predicated
+// out of the sum, which therefore sees exactly the reference's operands in
+// the reference's order (inc/csr.hpp:185-191): results are bitwise the
+// reference's. The Jacobi division uses the Markstein correction with the
+// host-rounded reciprocal of the (dictionary) diagonal, which is the
+// correctly rounded quotient (IEEE a / a_ii) wherever no intermediate can
+// under/overflow; other operands take __ddiv_rn.
 // ===========================================================================
 
-constexpr int kSellStages = 5;  // deeper than the CSR pipeline: slices are small once compressed
+constexpr int kSgStages = 4;  // slices in flight per CTA (power of two)
 
-__host__ __device__ __forceinline__ size_t sell_stage_bytes(int wmax, int vf, int cf) {
-    return static_cast<size_t>(wmax) * kTileRows * ((vf ? 1 : 8) + (cf ? 2 : 4)) + 2 * kTileRows /* len, dpos */ +
-           static_cast<size_t>(kTileRows) * 8 /* f */;
+__host__ __device__ __forceinline__ int sg_entry_bytes(int vf, int cf) { return (vf ? 1 : 8) + (cf ? 2 : 4); }
+__host__ __device__ __forceinline__ size_t sg_block_bytes(int ng, int gs, int h, int vf, int cf) {
+    return static_cast<size_t>(ng) * h * gs * sg_entry_bytes(vf, cf) + 2 * static_cast<size_t>(h);
+}
+__host__ __device__ __forceinline__ size_t sg_stage_bytes(int ngmax, int gs, int h, int vf, int cf) {
+    return (sg_block_bytes(ngmax, gs, h, vf, cf) + 15) / 16 * 16 + 8 * static_cast<size_t>(h) /* f */;
 }
 
-#ifndef SB_SELL_MINB
-#define SB_SELL_MINB 4
+template <int N> struct RawVec;
+template <> struct RawVec<2> { using T = uint16_t; };
+template <> struct RawVec<4> { using T = uint32_t; };
+template <> struct RawVec<8> { using T = uint2; };
+template <> struct RawVec<16> { using T = uint4; };
+template <> struct RawVec<32> { struct alignas(16) T { uint4 a, b; }; };
+
+template <int N> __device__ __forceinline__ uint32_t word_of(const typename RawVec<N>::T &v, int i) {
+    if constexpr (N == 2) return v;
+    else if constexpr (N == 4) return v;
+    else if constexpr (N == 8) return i == 0 ? v.x : v.y;
+    else if constexpr (N == 16) return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+    else {
+        const uint4 &q = i < 4 ? v.a : v.b;
+        const int j = i & 3;
+        return j == 0 ? q.x : j == 1 ? q.y : j == 2 ? q.z : q.w;
+    }
+}
+
+// a / d correctly rounded; y = RN(1/d) computed on the host (0 = unknown).
+// q = RN(a y); r = a - d q (exact by FMA); q' = RN(q + r y) = RN(a / d)
+// (Markstein) for |a| in [2^-900, 2^900] and |d| in [2^-100, 2^100] (host
+// check); everything else goes through __ddiv_rn.
+__device__ __forceinline__ double div_rn(double a, double d, double y) {
+    const unsigned e = (static_cast<unsigned>(__double2hiint(a)) >> 20) & 0x7ffu;
+    if (e - 123u < 1800u && y != 0.0) {
+        const double q = __dmul_rn(a, y);
+        const double r = __fma_rn(-d, q, a);
+        return __fma_rn(r, y, q);
+    }
+    return __ddiv_rn(a, d);
+}
+
+// sum = sum + p only when pred (a predicated add: the skipped slot leaves
+// every bit of sum unchanged)
+__device__ __forceinline__ void add_if(double &sum, double p, bool pred) {
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q add.rn.f64 %0, %0, %1;\n}" : "+d"(sum) : "d"(p), "r"(static_cast<int>(pred)));
+}
+
+#ifndef SB_SG_MINB
+#define SB_SG_MINB 4
 #endif
-template <int MODE, int NV, int VF, int CF>
-__global__ void __launch_bounds__(kTileRows, SB_SELL_MINB)
-    k_sell_tile(int n, const int64_t *__restrict__ soff, const uint8_t *__restrict__ slen,
-                const void *__restrict__ cols, const void *__restrict__ vals, const double *__restrict__ dict,
-                int ndict, int ntiles, int wmax, const double *__restrict__ x, const double *__restrict__ f,
-                double *__restrict__ out, double omega, const int *skip, Aux aux, Red red) {
-    constexpr int S = kSellStages;
+template <int MODE, int NV, int VF, int CF, int GS, int RPT>
+__global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
+    k_sellg(int n, int nslices, const int64_t *__restrict__ soff, const unsigned char *__restrict__ blk,
+            const double *__restrict__ dict, const double *__restrict__ rdict, int ndict, int ngmax,
+            const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
+            const int *skip, Aux aux, Red red) {
+    constexpr int S = kSgStages;
+    constexpr int H = kTileRows * RPT;
+    constexpr int VB = VF ? 1 : 8, CB = CF ? 2 : 4;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) uint64_t full[S];
     __shared__ __align__(8) uint64_t empty[S];
-    __shared__ int2 hdr[S];
+    __shared__ int hdr[S];
     __shared__ double sdict[VF ? 256 : 1];
+    __shared__ double srdict[VF ? 256 : 1];
     double acc[NV > 0 ? NV : 1];
 #pragma unroll
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
+    const size_t sb = sg_stage_bytes(ngmax, GS, H, VF, CF);
+    constexpr int kWarps = kTileRows / 32;
+    const int tid = threadIdx.x;
+    const bool f_al = (reinterpret_cast<uintptr_t>(f) & 15u) == 0;  // TMA needs 16-byte aligned windows
 
-    constexpr int VB = VF ? 1 : 8;
-    constexpr int CB = CF ? 2 : 4;
-    constexpr int R = kTileRows;
-    const size_t sb = sell_stage_bytes(wmax, VF, CF);
-    const size_t o_c = static_cast<size_t>(wmax) * R * VB;
-    const size_t o_len = o_c + static_cast<size_t>(wmax) * R * CB;  // len[256] then dpos[256]
-    const size_t o_f = o_len + 2 * R;
-    constexpr int kWarps = R / 32;
-    const unsigned char *vbase = static_cast<const unsigned char *>(vals);
-    const unsigned char *cbase = static_cast<const unsigned char *>(cols);
-
+    // thread 0: stage slice t into buffer s (one bulk copy for the matrix
+    // block, one for the rhs window once the predecessor is complete)
     auto issue = [&](int t, int s, bool with_f) {
-        const int64_t e0 = soff[t], e1 = soff[t + 1];
-        const int w = static_cast<int>((e1 - e0) / R);
-        const int r0 = t * R;
-        hdr[s] = make_int2(r0, w);
+        const int64_t b0 = soff[t], b1 = soff[t + 1];
+        const int ng = static_cast<int>((b1 - b0 - 2 * H) / (H * GS * (VB + CB)));
+        hdr[s] = ng;
         unsigned char *st = smem + s * sb;
-        const uint32_t vbytes = static_cast<uint32_t>(w) * R * VB;
-        const uint32_t cbytes = static_cast<uint32_t>(w) * R * CB;
-        const int rows_here = min(R, n - r0);
-        const uint32_t fbytes = (MODE != M_SPMV && with_f) ? static_cast<uint32_t>(rows_here & ~1) * 8u : 0u;
-        mbar_expect_tx(&full[s], vbytes + cbytes + 2 * R + fbytes);
-        if (vbytes) bulk_g2s(st, vbase + e0 * VB, vbytes, &full[s]);
-        if (cbytes) bulk_g2s(st + o_c, cbase + e0 * CB, cbytes, &full[s]);
-        bulk_g2s(st + o_len, slen + 2 * static_cast<size_t>(r0), 2 * R, &full[s]);
-        if (fbytes) bulk_g2s(st + o_f, f + r0, fbytes, &full[s]);
+        const int r0 = t * H;
+        const int rows = min(H, n - r0);
+        const uint32_t fbytes = (MODE != M_SPMV && with_f && f_al) ? static_cast<uint32_t>(rows & ~1) * 8u : 0u;
+        const uint32_t mbytes = static_cast<uint32_t>(b1 - b0);
+        mbar_expect_tx(&full[s], mbytes + fbytes);
+        bulk_g2s(st, blk + b0, mbytes, &full[s]);
+        if (fbytes) bulk_g2s(st + (sb - 8 * H), f + r0, fbytes, &full[s]);
     };
 
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
 #pragma unroll
         for (int q = 0; q < S; ++q) {
             mbar_init(&full[q], 1);
@@ -633,29 +677,31 @@ __global__ void __launch_bounds__(kTileRows, SB_SELL_MINB)
         fence_mbar_init();
     }
     if constexpr (VF == 1)
-        for (int i = threadIdx.x; i < ndict; i += blockDim.x) sdict[i] = dict[i];
+        for (int i = tid; i < ndict; i += blockDim.x) {
+            sdict[i] = dict[i];
+            srdict[i] = rdict[i];
+        }
     __syncthreads();
     const int G = static_cast<int>(gridDim.x);
     const int b = static_cast<int>(blockIdx.x);
-    if (threadIdx.x == 0)
+    if (tid == 0)
         for (int q = 0; q < S - 1; ++q)
-            if (b + q * G < ntiles) issue(b + q * G, q, false);
+            if (b + q * G < nslices) issue(b + q * G, q, false);
     pdl_wait();
     const bool active = !(skip && *skip);
     if (!active) {
         for (int q = 0; q < S - 1; ++q)
-            if (b + q * G < ntiles) mbar_wait(&full[q], 0u);
+            if (b + q * G < nslices) mbar_wait(&full[q], 0u);
         pdl_trigger();
     } else {
         uint32_t fph = 0u, eph = 0u;
-        int s = 0, it = 0;
-        const int lane = threadIdx.x & 31;
-        const int tid = threadIdx.x;
-        for (int t = b; t < ntiles; t += G, ++it, s = (s + 1 == S) ? 0 : s + 1) {
-            if (t + G >= ntiles) pdl_trigger();
+        int it = 0;
+        for (int t = b; t < nslices; t += G, ++it) {
+            const int s = it & (S - 1);
+            if (t + G >= nslices) pdl_trigger();
             const int tn = t + (S - 1) * G;
-            const int sn = (s + S - 1) % S;
-            if (tid == 0 && tn < ntiles) {
+            if (tid == 0 && tn < nslices) {
+                const int sn = (it + S - 1) & (S - 1);
                 if (it >= 1) {
                     mbar_wait(&empty[sn], (eph >> sn) & 1u);
                     eph ^= 1u << sn;
@@ -664,61 +710,79 @@ __global__ void __launch_bounds__(kTileRows, SB_SELL_MINB)
             }
             mbar_wait(&full[s], (fph >> s) & 1u);
             fph ^= 1u << s;
-            const int2 h = hdr[s];
-            const int row = h.x + tid;
-            const int w = h.y;  // slice width: warp-uniform trip count
+            const int ng = hdr[s];
             const unsigned char *st = smem + s * sb;
-            if (row < n) {
-                const int len = st[o_len + tid];
-                double fi = 0.0;
-                if (MODE != M_SPMV) {
-                    const bool f_staged = it >= S - 1 && row < h.x + (min(R, n - h.x) & ~1);
-                    fi = f_staged ? reinterpret_cast<const double *>(st + o_f)[tid] : f[row];
-                }
-                const unsigned char *sv = st + static_cast<size_t>(tid) * VB;
-                const unsigned char *sc = st + o_c + static_cast<size_t>(tid) * CB;
-                auto colv = [&](int k) -> int {
-                    if constexpr (CF == 1) return row + static_cast<int>(reinterpret_cast<const int16_t *>(sc)[k * R]);
-                    else return reinterpret_cast<const int32_t *>(sc)[k * R];
-                };
-                auto valv = [&](int k) -> double {
-                    if constexpr (VF == 1) return sdict[sv[k * R]];
-                    else return reinterpret_cast<const double *>(sv)[k * R];
-                };
-                double sum = 0.0, xi = 0.0, d = 0.0;
-                if constexpr (MODE >= M_JACOBI) {
-                    xi = xval<MODE, false>(row, x, f, aux, omega);
-                    d = valv(st[o_len + R + tid]);  // the row's diagonal slot
-                }
-                constexpr int U = MODE == M_JACOBI_ZERO ? 4 : 8;
-                // Branch-free slices: padding slots (k >= len) hold column =
-                // row, so their gathers are valid; they are masked out of the
-                // sum, which therefore sees exactly the row's entries in order.
-                for (int kb = 0; kb < w; kb += U) {
-                    int c[U];
-                    double a[U], xv[U];
+            const unsigned char *sv = st;
+            const unsigned char *sc = st + static_cast<size_t>(ng) * H * GS * VB;
+            const uint16_t *meta = reinterpret_cast<const uint16_t *>(sc + static_cast<size_t>(ng) * H * GS * CB);
+            const double *sf = reinterpret_cast<const double *>(st + (sb - 8 * H));
+            const bool f_staged = it >= S - 1 && f_al;
+            const int r0 = t * H;
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int k = min(kb + u, w - 1);
-                        c[u] = colv(k);
-                        a[u] = valv(k);
+            for (int rr = 0; rr < RPT; ++rr) {
+                const int lr = tid + rr * kTileRows;  // row within the slice
+                const int row = r0 + lr;
+                if (row < n) {
+                    const uint32_t m = meta[lr];
+                    const int len = static_cast<int>(m & 0xffu);
+                    double fi = 0.0;
+                    if (MODE != M_SPMV) fi = (f_staged && lr < (min(H, n - r0) & ~1)) ? sf[lr] : f[row];
+                    double xi = 0.0;
+                    if constexpr (MODE >= M_JACOBI) xi = xval<MODE, false>(row, x, f, aux, omega);
+                    const double *xrow = x + row;
+                    double sum = 0.0;
+                    for (int g = 0; g < ng; ++g) {
+                        using VT = typename RawVec<GS * VB>::T;
+                        using CT = typename RawVec<GS * CB>::T;
+                        const VT vv = *reinterpret_cast<const VT *>(sv + (static_cast<size_t>(g) * H + lr) * GS * VB);
+                        const CT cc = *reinterpret_cast<const CT *>(sc + (static_cast<size_t>(g) * H + lr) * GS * CB);
+                        double a[GS], xv[GS];
+#pragma unroll
+                        for (int u = 0; u < GS; ++u) {
+                            int col;  // CF 1: the column delta
+                            if constexpr (CF == 1) {
+                                const uint32_t w = word_of<GS * CB>(cc, u >> 1);
+                                col = (u & 1) ? (static_cast<int>(w) >> 16) : static_cast<int>(static_cast<int16_t>(w & 0xffffu));
+                            } else {
+                                col = static_cast<int>(word_of<GS * CB>(cc, u));
+                            }
+                            if constexpr (VF == 1) {
+                                const uint32_t w = word_of<GS * VB>(vv, u >> 2);
+                                a[u] = sdict[(w >> (8 * (u & 3))) & 0xffu];
+                            } else {
+                                const uint32_t lo = word_of<GS * VB>(vv, 2 * u), hi = word_of<GS * VB>(vv, 2 * u + 1);
+                                a[u] = __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+                            }
+                            if constexpr (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV)
+                                xv[u] = (CF == 1) ? __ldg(xrow + col) : __ldg(x + col);
+                            else
+                                xv[u] = xval<MODE, false>((CF == 1) ? row + col : col, x, f, aux, omega);
+                        }
+#pragma unroll
+                        for (int u = 0; u < GS; ++u) add_if(sum, __dmul_rn(a[u], xv[u]), g * GS + u < len);
                     }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) xv[u] = xval<MODE, false>(c[u], x, f, aux, omega);
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (kb + u < len) sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
+                    double o;
+                    if constexpr (MODE == M_SPMV) o = sum;
+                    else if constexpr (MODE == M_RESID) o = __dsub_rn(fi, sum);
+                    else {
+                        double d, y;
+                        const int di = static_cast<int>(m >> 8);
+                        if constexpr (VF == 1) {
+                            d = sdict[di];
+                            y = srdict[di];
+                        } else {
+                            d = *reinterpret_cast<const double *>(sv + ((static_cast<size_t>(di / GS) * H + lr) * GS + (di % GS)) * 8);
+                            y = 0.0;
+                        }
+                        o = __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d, y));
+                    }
+                    out[row] = o;
+                    if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row] : o);
+                    if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
                 }
-                double o;
-                if constexpr (MODE == M_SPMV) o = sum;
-                else if constexpr (MODE == M_RESID) o = __dsub_rn(fi, sum);
-                else o = __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
-                out[row] = o;
-                if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row] : o);
-                if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            if ((tid & 31) == 0) mbar_arrive(&empty[s]);
         }
     }
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
@@ -998,8 +1062,12 @@ __global__ void k_jacobi_zero(int64_t n, const double *__restrict__ f,
 }
 
 // f_c[c] = (0.0 + r[m0]) + r[m1], members ascending (csr.hpp:232-239 with unit P).
+// xc0 != nullptr: also the coarse level's first pre-sweep from x = 0,
+// x0_c = 0 + (omega * f_c) / a_cc (smoother.hpp:112-119 with spmv(A, 0) = +0),
+// so the coarse level starts at its second sweep.
 __global__ void k_restrict(int64_t nc, const int2 *__restrict__ mem, const double *__restrict__ r,
-                           double *__restrict__ fc) {
+                           double *__restrict__ fc, const double *__restrict__ dc, double *__restrict__ xc0,
+                           double omega) {
     pdl_wait();
     for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < nc;
          c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1007,6 +1075,7 @@ __global__ void k_restrict(int64_t nc, const int2 *__restrict__ mem, const doubl
         double s = __dadd_rn(0.0, r[m.x]);
         if (m.y >= 0) s = __dadd_rn(s, r[m.y]);
         fc[c] = s;
+        if (xc0) xc0[c] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), dc[c]));
     }
 }
 
@@ -1217,12 +1286,14 @@ struct DevLevel {
     int vf = 0, cf = 0, ndict = 0;
     const void *sv = nullptr, *sc = nullptr;
     double *dict = nullptr;
-    // sliced-ELL layout (sell = 1): slice offsets, row lengths, slice-major entries
-    int sell = 0, sell_tiles = 0, sell_wmax = 0, sell_grid = 0;
+    // grouped sliced-ELL layout (sell = 1): byte offsets of the slice blocks,
+    // the blocks, the reciprocal dictionary (Markstein division)
+    int sell = 0, sell_tiles = 0, sell_ngmax = 0, sell_gs = 4, sell_rpt = 1, sell_grid = 0;
     size_t sell_smem = 0;
     int64_t *soff = nullptr;
-    uint8_t *slen = nullptr;
-    const void *sell_v = nullptr, *sell_c = nullptr;
+    const unsigned char *sell_blk = nullptr;
+    int64_t sell_slots = 0;  // stored entry slots (incl. padding)
+    double *rdict = nullptr;
     int2 *mem = nullptr;
     int ntiles = 0, cap = 0, grid = 0;
     size_t smem = 0;
@@ -1347,13 +1418,25 @@ static void launch_csr_f(sb_ctx c, const DevLevel &l, cudaStream_t s, const doub
              red);
 }
 
+template <int MODE, int NV, int VF, int CF, int GS, int RPT>
+static void launch_sell_g(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
+                          double *out, double omega, const int *skip, const Red &red, Aux aux) {
+    launch_k(c, k_sellg<MODE, NV, VF, CF, GS, RPT>, dim3(std::min(l.sell_tiles, l.sell_grid)), dim3(kTileRows),
+             l.sell_smem, s, static_cast<int>(l.n), l.sell_tiles, static_cast<const int64_t *>(l.soff), l.sell_blk,
+             static_cast<const double *>(l.dict), static_cast<const double *>(l.rdict), l.ndict, l.sell_ngmax, x, f,
+             out, omega, skip, aux, red);
+}
+
 template <int MODE, int NV, int VF, int CF>
 static void launch_sell_f(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
                           double *out, double omega, const int *skip, const Red &red, Aux aux) {
-    launch_k(c, k_sell_tile<MODE, NV, VF, CF>, dim3(std::min(l.sell_tiles, l.sell_grid)), dim3(kTileRows),
-             l.sell_smem, s, static_cast<int>(l.n), static_cast<const int64_t *>(l.soff),
-             static_cast<const uint8_t *>(l.slen), l.sell_c, l.sell_v, static_cast<const double *>(l.dict), l.ndict,
-             l.sell_tiles, l.sell_wmax, x, f, out, omega, skip, aux, red);
+    if (l.sell_gs == 4) {
+        if (l.sell_rpt == 2) launch_sell_g<MODE, NV, VF, CF, 4, 2>(c, l, s, x, f, out, omega, skip, red, aux);
+        else launch_sell_g<MODE, NV, VF, CF, 4, 1>(c, l, s, x, f, out, omega, skip, red, aux);
+    } else {
+        if (l.sell_rpt == 2) launch_sell_g<MODE, NV, VF, CF, 2, 2>(c, l, s, x, f, out, omega, skip, red, aux);
+        else launch_sell_g<MODE, NV, VF, CF, 2, 1>(c, l, s, x, f, out, omega, skip, red, aux);
+    }
 }
 
 template <int MODE, int NV>
@@ -1408,13 +1491,23 @@ static void emit_tail(sb_ctx c, cudaStream_t s, const Cyc &cp, const double *f, 
                           c->trace));
 }
 
+// Buffer the zero-guess first pre-sweep of level k writes (X = the level's
+// output buffer; see emit_vcycle's buffer plan).
+static double *zero_sweep_dest(sb_ctx c, const Cyc &cp, int k, double *X) {
+    double *T = c->L[static_cast<size_t>(k)].t;
+    double *post_first = (cp.post >= 1) ? (((cp.post - 1) % 2 == 0) ? X : T) : X;
+    double *pre_end = (cp.post >= 1) ? (post_first == X ? T : X) : X;
+    return (cp.pre % 2 == 1) ? pre_end : (pre_end == X ? T : X);
+}
+
 // One V-cycle at level k (cycle.hpp:53-75), result written to X. T is the
 // level's ping-pong partner; the buffer plan makes the last post-sweep land
-// in X without copies, and lets the first two pre-sweeps (from x = 0) and the
-// prolongation + first post-sweep run fused. Levels from
-// c->tail_from down run inside one cluster-resident kernel.
+// in X without copies. From x = 0 the first sweep is x0 = 0 + w f / a_ii
+// (k_jacobi_zero, or written by the parent's restriction when x0_ready);
+// the prolongation + first post-sweep run fused. Levels
+// from c->tail_from down run inside one cluster-resident kernel.
 static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const double *f, double *X,
-                        bool zero) {
+                        bool zero, bool x0_ready = false) {
     const int L = static_cast<int>(c->L.size());
     if (k + 1 == L && !(zero && k == c->tail_from)) {
         emit_coarse(c, s, f, X);
@@ -1434,17 +1527,12 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
             CK(cudaMemsetAsync(pre_end, 0, sizeof(double) * static_cast<size_t>(l.n), s));
             cur = pre_end;
         } else {
-            const int writes = cp.pre >= 2 ? cp.pre - 1 : 1;
-            cur = (writes % 2 == 1) ? pre_end : (pre_end == X ? T : X);
+            cur = zero_sweep_dest(c, cp, k, X);
             other = (cur == X) ? T : X;
-            if (cp.pre == 1) {
+            if (!x0_ready)
                 launch_k(c, k_jacobi_zero, dim3(vec_grid(l.n)), dim3(kVecThreads), 0, s, l.n, f,
                          static_cast<const double *>(l.diag), cur, cp.omega);
-            } else {
-                launch_csr<M_JACOBI_ZERO, 0>(c, l, s, nullptr, f, cur, cp.omega, nullptr, Red{},
-                                             Aux{l.diag, nullptr, nullptr});
-            }
-            for (int i = 2; i < cp.pre; ++i) {
+            for (int i = 1; i < cp.pre; ++i) {
                 launch_jacobi(c, l, s, cur, f, other, cp.omega);
                 std::swap(cur, other);
             }
@@ -1457,9 +1545,14 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
     }
     const DevLevel &lc = c->L[static_cast<size_t>(k) + 1];
     launch_csr<M_RESID, 0>(c, l, s, cur, f, c->rs, 0.0, nullptr, Red{});
+    // the child's zero-guess sweep rides on the restriction (not for the
+    // coarsest level or the cluster tail, which start from x = 0 themselves)
+    const bool child_x0 = cp.pre >= 1 && k + 2 < L && k + 1 != c->tail_from;
+    double *x0 = child_x0 ? zero_sweep_dest(c, cp, k + 1, lc.x) : nullptr;
     launch_k(c, k_restrict, dim3(vec_grid(lc.n)), dim3(kVecThreads), 0, s, lc.n,
-             static_cast<const int2 *>(l.mem), static_cast<const double *>(c->rs), lc.f);
-    emit_vcycle(c, s, cp, k + 1, lc.f, lc.x, true);
+             static_cast<const int2 *>(l.mem), static_cast<const double *>(c->rs), lc.f,
+             static_cast<const double *>(lc.diag), x0, cp.omega);
+    emit_vcycle(c, s, cp, k + 1, lc.f, lc.x, true, child_x0);
     if (cp.post >= 1 && cur != post_first) {
         // x' = cur + P x_c folded into the first post-sweep's gathers
         launch_csr<M_JACOBI_PROLONG, 0>(c, l, s, cur, f, post_first, cp.omega, nullptr, Red{},
@@ -1757,93 +1850,123 @@ static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
         }
     }
     D.smem = kStages * stage_bytes_of(D.cap, D.vf, D.cf);  // pipeline stages
-    // sliced-ELL conversion (SB_SELL=0 keeps the CSR pipeline)
+    // grouped sliced-ELL conversion (SB_SELL=0 keeps the CSR pipeline)
     const char *se = std::getenv("SB_SELL");
     if ((!se || std::atoi(se) != 0) && A.n > 0) {
-        const int64_t nt = (A.n + kTileRows - 1) / kTileRows;
-        std::vector<int64_t> off(static_cast<size_t>(nt) + 1, 0);
+        const char *re = std::getenv("SB_RPT");
+        const int rpt = (re && std::atoi(re) == 2) ? 2 : 1;
+        const int64_t H = static_cast<int64_t>(kTileRows) * rpt;
+        const int64_t nt = (A.n + H - 1) / H;
+        std::vector<int> wt(static_cast<size_t>(nt), 0);
         int wmax = 0;
-        bool ok = true;
-        for (int64_t t = 0; t < nt && ok; ++t) {
+        for (int64_t t = 0; t < nt; ++t) {
             int w = 0;
-            for (int64_t r = t * kTileRows; r < std::min<int64_t>(A.n, (t + 1) * kTileRows); ++r)
+            for (int64_t r = t * H; r < std::min<int64_t>(A.n, (t + 1) * H); ++r)
                 w = std::max<int>(w, static_cast<int>(A.rp[r + 1] - A.rp[r]));
-            if (w > 64) ok = false;
+            wt[static_cast<size_t>(t)] = w;
             wmax = std::max(wmax, w);
-            off[t + 1] = off[t] + static_cast<int64_t>(w) * kTileRows;
         }
-        const size_t stage = sell_stage_bytes(wmax, D.vf, D.cf);
-        if (ok && off[nt] <= 3 * A.nnz() / 2 + kTileRows && kSellStages * stage <= 200 * 1024) {
-            // per slice: 256 row lengths then 256 diagonal slots (255: none)
-            std::vector<uint8_t> len(static_cast<size_t>(nt) * 2 * kTileRows, 0);
-            const size_t tot = static_cast<size_t>(off[nt]);
-            std::vector<int16_t> c16(D.cf ? tot : 0, 0);
-            std::vector<int32_t> c32(D.cf ? 0 : tot, 0);
-            std::vector<uint8_t> v8(D.vf ? tot : 0, 0);
-            std::vector<double> v64(D.vf ? 0 : tot, 0.0);
+        // group size: 4 (fewest instructions) unless 2 saves > 5% of the slots
+        int64_t s2 = 0, s4 = 0;
+        for (int w : wt) {
+            s2 += (w + 1) / 2 * 2;
+            s4 += (w + 3) / 4 * 4;
+        }
+        const int gs = (s4 * 100 <= s2 * 105) ? 4 : 2;
+        const int ngmax = (wmax + gs - 1) / gs;
+        const int64_t slots = (gs == 4 ? s4 : s2) * H;
+        const size_t stage = sg_stage_bytes(ngmax, gs, static_cast<int>(H), D.vf, D.cf);
+        const bool ok = wmax <= 255 && slots <= 3 * A.nnz() / 2 + H && kSgStages * stage <= 200 * 1024;
+        if (ok) {
+            const int VB = D.vf ? 1 : 8, CB = D.cf ? 2 : 4;
+            std::vector<int64_t> off(static_cast<size_t>(nt) + 1, 0);
+            for (int64_t t = 0; t < nt; ++t) {
+                const int ng = (wt[static_cast<size_t>(t)] + gs - 1) / gs;
+                off[static_cast<size_t>(t) + 1] = off[static_cast<size_t>(t)] +
+                    static_cast<int64_t>(sg_block_bytes(ng, gs, static_cast<int>(H), D.vf, D.cf));
+            }
+            std::vector<unsigned char> blk(static_cast<size_t>(off[static_cast<size_t>(nt)]), 0);
             std::map<uint64_t, int> ids;
+            std::vector<double> dict;
             if (D.vf) {  // same dictionary order as the CSR-stream arrays
-                std::vector<double> dict(static_cast<size_t>(D.ndict));
+                dict.resize(static_cast<size_t>(D.ndict));
                 CK(cudaMemcpy(dict.data(), D.dict, sizeof(double) * dict.size(), cudaMemcpyDeviceToHost));
                 for (int q = 0; q < D.ndict; ++q) {
                     uint64_t bits;
-                    std::memcpy(&bits, &dict[q], 8);
+                    std::memcpy(&bits, &dict[static_cast<size_t>(q)], 8);
                     ids[bits] = q;
                 }
             }
-            for (int64_t t = 0; t < nt; ++t)
-                for (int64_t r = t * kTileRows; r < std::min<int64_t>(A.n, (t + 1) * kTileRows); ++r) {
-                    const int64_t lane = r - t * kTileRows;
-                    len[static_cast<size_t>(t * 2 * kTileRows + lane)] = static_cast<uint8_t>(A.rp[r + 1] - A.rp[r]);
-                    uint8_t dpos = 0;  // (a missing diagonal is rejected before any sweep)
+            for (int64_t t = 0; t < nt; ++t) {
+                const int ng = (wt[static_cast<size_t>(t)] + gs - 1) / gs;
+                unsigned char *b = blk.data() + off[static_cast<size_t>(t)];
+                unsigned char *bv = b;
+                unsigned char *bc = b + static_cast<size_t>(ng) * H * gs * VB;
+                unsigned char *bm = bc + static_cast<size_t>(ng) * H * gs * CB;
+                for (int64_t r = t * H; r < std::min<int64_t>(A.n, (t + 1) * H); ++r) {
+                    const int64_t lr = r - t * H;
+                    const int64_t len = A.rp[r + 1] - A.rp[r];
+                    int di = 0;  // diagonal: dictionary index (vf) or slot (a missing one is rejected before a sweep)
                     for (int64_t k = A.rp[r]; k < A.rp[r + 1]; ++k)
-                        if (A.ci[k] == r) dpos = static_cast<uint8_t>(k - A.rp[r]);
-                    len[static_cast<size_t>(t * 2 * kTileRows + kTileRows + lane)] = dpos;
-                    const int w_t = static_cast<int>((off[t + 1] - off[t]) / kTileRows);
-                    for (int64_t k = A.rp[r + 1] - A.rp[r]; k < w_t; ++k) {  // padding: column = row
-                        const size_t pos = static_cast<size_t>(off[t] + k * kTileRows + lane);
-                        if (D.cf) c16[pos] = 0;
-                        else c32[pos] = static_cast<int32_t>(r);
-                    }
-                    for (int64_t k = A.rp[r]; k < A.rp[r + 1]; ++k) {
-                        const size_t pos = static_cast<size_t>(off[t] + (k - A.rp[r]) * kTileRows + lane);
-                        if (D.cf) c16[pos] = static_cast<int16_t>(A.ci[k] - r);
-                        else c32[pos] = A.ci[k];
-                        if (D.vf) {
-                            uint64_t bits;
-                            std::memcpy(&bits, &A.v[k], 8);
-                            v8[pos] = static_cast<uint8_t>(ids[bits]);
+                        if (A.ci[k] == r) {
+                            if (D.vf) {
+                                uint64_t bits;
+                                std::memcpy(&bits, &A.v[k], 8);
+                                di = ids[bits];
+                            } else {
+                                di = static_cast<int>(k - A.rp[r]);
+                            }
+                        }
+                    const uint16_t m = static_cast<uint16_t>(len | (di << 8));
+                    std::memcpy(bm + 2 * lr, &m, 2);
+                    for (int64_t e = 0; e < static_cast<int64_t>(ng) * gs; ++e) {
+                        const size_t pos = static_cast<size_t>((e / gs) * H + lr) * gs + static_cast<size_t>(e % gs);
+                        int64_t col = r;  // padding: column = row, value index 0 / 0.0 (predicated out)
+                        double val = 0.0;
+                        int vi = 0;
+                        if (e < len) {
+                            const int64_t k = A.rp[r] + e;
+                            col = A.ci[k];
+                            val = A.v[k];
+                            if (D.vf) {
+                                uint64_t bits;
+                                std::memcpy(&bits, &A.v[k], 8);
+                                vi = ids[bits];
+                            }
+                        }
+                        if (D.vf) bv[pos] = static_cast<uint8_t>(vi);
+                        else std::memcpy(bv + pos * 8, &val, 8);
+                        if (D.cf) {
+                            const int16_t dl = static_cast<int16_t>(col - r);
+                            std::memcpy(bc + pos * 2, &dl, 2);
                         } else {
-                            v64[pos] = A.v[k];
+                            const int32_t cc = static_cast<int32_t>(col);
+                            std::memcpy(bc + pos * 4, &cc, 4);
                         }
                     }
                 }
+            }
             D.soff = dalloc<int64_t>(c, nt + 1);
             CK(cudaMemcpy(D.soff, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice));
-            D.slen = dalloc<uint8_t>(c, static_cast<int64_t>(len.size()));
-            CK(cudaMemcpy(D.slen, len.data(), len.size(), cudaMemcpyHostToDevice));
-            if (D.cf) {
-                auto *p = dalloc<int16_t>(c, static_cast<int64_t>(tot));
-                CK(cudaMemcpy(p, c16.data(), sizeof(int16_t) * tot, cudaMemcpyHostToDevice));
-                D.sell_c = p;
-            } else {
-                auto *p = dalloc<int32_t>(c, static_cast<int64_t>(tot));
-                CK(cudaMemcpy(p, c32.data(), sizeof(int32_t) * tot, cudaMemcpyHostToDevice));
-                D.sell_c = p;
-            }
-            if (D.vf) {
-                auto *p = dalloc<uint8_t>(c, static_cast<int64_t>(tot));
-                CK(cudaMemcpy(p, v8.data(), tot, cudaMemcpyHostToDevice));
-                D.sell_v = p;
-            } else {
-                auto *p = dalloc<double>(c, static_cast<int64_t>(tot));
-                CK(cudaMemcpy(p, v64.data(), sizeof(double) * tot, cudaMemcpyHostToDevice));
-                D.sell_v = p;
+            auto *p = dalloc<unsigned char>(c, static_cast<int64_t>(blk.size()) + 16);
+            CK(cudaMemcpy(p, blk.data(), blk.size(), cudaMemcpyHostToDevice));
+            D.sell_blk = p;
+            if (D.vf) {  // Markstein reciprocals RN(1/d); 0 where |d| leaves [2^-100, 2^100]
+                std::vector<double> rd(dict.size(), 0.0);
+                for (size_t q = 0; q < dict.size(); ++q) {
+                    const double d = std::fabs(dict[q]);
+                    if (d >= std::ldexp(1.0, -100) && d <= std::ldexp(1.0, 100)) rd[q] = 1.0 / dict[q];
+                }
+                D.rdict = dalloc<double>(c, 256);
+                CK(cudaMemcpy(D.rdict, rd.data(), sizeof(double) * rd.size(), cudaMemcpyHostToDevice));
             }
             D.sell = 1;
             D.sell_tiles = static_cast<int>(nt);
-            D.sell_wmax = wmax;
-            D.sell_smem = kSellStages * stage;
+            D.sell_ngmax = ngmax;
+            D.sell_gs = gs;
+            D.sell_rpt = rpt;
+            D.sell_slots = slots;
+            D.sell_smem = kSgStages * stage;
         }
     }
 }
@@ -1871,13 +1994,20 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
     }
 }
 
+template <int MODE, int NV, int VF, int CF> static void set_sg_attr(int b) {
+    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+}
+
 template <int MODE, int NV> static void set_smem_attr(size_t smem) {
     if (smem <= 48 * 1024) return;
     const int b = static_cast<int>(smem);
-    CK(cudaFuncSetAttribute(k_sell_tile<MODE, NV, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(k_sell_tile<MODE, NV, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(k_sell_tile<MODE, NV, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(k_sell_tile<MODE, NV, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    set_sg_attr<MODE, NV, 0, 0>(b);
+    set_sg_attr<MODE, NV, 1, 0>(b);
+    set_sg_attr<MODE, NV, 0, 1>(b);
+    set_sg_attr<MODE, NV, 1, 1>(b);
     CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_csr_tile<MODE, NV, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
@@ -2198,7 +2328,6 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
     set_smem_attr<M_RESID, 0>(max_smem);
     set_smem_attr<M_RESID, 1>(max_smem);
     set_smem_attr<M_JACOBI, 0>(max_smem);
-    set_smem_attr<M_JACOBI_ZERO, 0>(max_smem);
     set_smem_attr<M_JACOBI_PROLONG, 0>(max_smem);
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
@@ -2208,7 +2337,7 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
         l.grid = std::max(1, nsm * std::max(occ, 1));
         if (l.sell) {
             occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell_tile<M_JACOBI, 0, 1, 1>, kTileRows,
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sellg<M_JACOBI, 0, 1, 1, 4, 1>, kTileRows,
                                                              l.sell_smem));
             l.sell_grid = std::max(1, nsm * std::max(occ, 1));
         }
@@ -2332,7 +2461,8 @@ int sb_pbicgstab_dev(sb_ctx c, const sb_cycle *cp, const double *d_b, double *d_
 double sb_last_solve_ms(sb_ctx c) { return c ? c->last_solve_ms : 0.0; }
 
 // Streamed storage of level k: fmt[0] = 1 sliced-ELL / 0 CSR, fmt[1] = value
-// dictionary, fmt[2] = int16 column deltas, fmt[3] = slice width (max);
+// dictionary, fmt[2] = int16 column deltas, fmt[3] = slice width (max, padded
+// to the group size);
 // *matrix_bytes = bytes one pass over the matrix streams from HBM (entries
 // incl. padding + per-row metadata), *nnz = stored nonzeros.
 int sb_level_format(sb_ctx c, int k, int *fmt, int64_t *matrix_bytes, int64_t *nnz) {
@@ -2342,11 +2472,11 @@ int sb_level_format(sb_ctx c, int k, int *fmt, int64_t *matrix_bytes, int64_t *n
         fmt[0] = l.sell;
         fmt[1] = l.vf;
         fmt[2] = l.cf;
-        fmt[3] = l.sell ? l.sell_wmax : 0;
+        fmt[3] = l.sell ? l.sell_ngmax * l.sell_gs : 0;
         if (l.sell) {
-            int64_t entries = 0;
-            CK(cudaMemcpy(&entries, l.soff + l.sell_tiles, sizeof(int64_t), cudaMemcpyDeviceToHost));
-            *matrix_bytes = entries * (vb + cb) + 2 * static_cast<int64_t>(l.sell_tiles) * kTileRows;
+            int64_t bytes = 0;  // every slice block is streamed once per pass
+            CK(cudaMemcpy(&bytes, l.soff + l.sell_tiles, sizeof(int64_t), cudaMemcpyDeviceToHost));
+            *matrix_bytes = bytes;
         } else {
             *matrix_bytes = l.nnz * (vb + cb) + 4 * (l.n + 1);
         }
@@ -2496,7 +2626,7 @@ int sb_restrict(sb_ctx c, int level, const double *r, double *fc) {
         if (l.nc < 0) throw invalid_argument("restrict: coarsest level has no aggregation");
         with_dev(c, [&](cudaStream_t s) {
             h2d(c, c->kv[KR], r, l.n);
-            k_restrict<<<vec_grid(l.nc), kVecThreads, 0, s>>>(l.nc, l.mem, c->kv[KR], c->kv[KZ]);
+            k_restrict<<<vec_grid(l.nc), kVecThreads, 0, s>>>(l.nc, l.mem, c->kv[KR], c->kv[KZ], nullptr, nullptr, 0.0);
             CK(cudaGetLastError());
             d2h(c, fc, c->kv[KZ], l.nc);
         });
