@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsparsh_b200.so")
+LIB_PATH = os.environ.get("SB_LIB") or os.path.join(_HERE, "_lib", "libsparsh_b200.so")  # SB_LIB: tools/ variant builds
 CSRC = os.path.join(_HERE, "csrc")
 
 SB_OK, SB_EINVAL, SB_ERUNTIME, SB_ECUDA = 0, 1, 2, 3

@@ -24,6 +24,7 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <type_traits>
 
 #include <cuda_runtime.h>
 
@@ -561,8 +562,9 @@ __global__ void __launch_bounds__(kTileRows, 3)
 
 // ===========================================================================
 // Grouped sliced-ELL ("SELL-G") pipeline: the default streamed format of every
-// level whose slices pad by <= 50%. A slice holds H = 256 * RPT consecutive
+// level whose slices pad by <= 50%. A slice holds H = 256 consecutive
 // rows; its block in HBM is contiguous and 16-byte aligned:
+//   hdr  int32 {ng, nfull, 0, 0}: groups, and groups every row fills (no masking)
 //   vals [ng][H][GS]  (uint8 dictionary indices, or f64 values)
 //   cols [ng][H][GS]  (int16 column - row deltas, or int32 columns)
 //   meta [H] uint16   row length | (dictionary index of a_ii, or its slot) << 8
@@ -577,11 +579,15 @@ __global__ void __launch_bounds__(kTileRows, 3)
 // under/overflow; other operands take __ddiv_rn.
 // ===========================================================================
 
-constexpr int kSgStages = 4;  // slices in flight per CTA (power of two)
+#ifndef SB_SG_STAGES
+#define SB_SG_STAGES 4
+#endif
+constexpr int kSgStages = SB_SG_STAGES;  // slices in flight per CTA (power of two)
 
 __host__ __device__ __forceinline__ int sg_entry_bytes(int vf, int cf) { return (vf ? 1 : 8) + (cf ? 2 : 4); }
+constexpr int kSgHdr = 16;  // slice header: int32 {groups, unmasked groups, 0, 0}
 __host__ __device__ __forceinline__ size_t sg_block_bytes(int ng, int gs, int h, int vf, int cf) {
-    return static_cast<size_t>(ng) * h * gs * sg_entry_bytes(vf, cf) + 2 * static_cast<size_t>(h);
+    return kSgHdr + static_cast<size_t>(ng) * h * gs * sg_entry_bytes(vf, cf) + 2 * static_cast<size_t>(h);
 }
 __host__ __device__ __forceinline__ size_t sg_stage_bytes(int ngmax, int gs, int h, int vf, int cf) {
     return (sg_block_bytes(ngmax, gs, h, vf, cf) + 15) / 16 * 16 + 8 * static_cast<size_t>(h) /* f */;
@@ -629,19 +635,18 @@ __device__ __forceinline__ void add_if(double &sum, double p, bool pred) {
 #ifndef SB_SG_MINB
 #define SB_SG_MINB 4
 #endif
-template <int MODE, int NV, int VF, int CF, int GS, int RPT>
+template <int MODE, int NV, int VF, int CF, int GS, int NG>
 __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
     k_sellg(int n, int nslices, const int64_t *__restrict__ soff, const unsigned char *__restrict__ blk,
             const double *__restrict__ dict, const double *__restrict__ rdict, int ndict, int ngmax,
             const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
             const int *skip, Aux aux, Red red) {
     constexpr int S = kSgStages;
-    constexpr int H = kTileRows * RPT;
+    constexpr int H = kTileRows;
     constexpr int VB = VF ? 1 : 8, CB = CF ? 2 : 4;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) uint64_t full[S];
     __shared__ __align__(8) uint64_t empty[S];
-    __shared__ int hdr[S];
     __shared__ double sdict[VF ? 256 : 1];
     __shared__ double srdict[VF ? 256 : 1];
     double acc[NV > 0 ? NV : 1];
@@ -656,8 +661,6 @@ __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
     // block, one for the rhs window once the predecessor is complete)
     auto issue = [&](int t, int s, bool with_f) {
         const int64_t b0 = soff[t], b1 = soff[t + 1];
-        const int ng = static_cast<int>((b1 - b0 - 2 * H) / (H * GS * (VB + CB)));
-        hdr[s] = ng;
         unsigned char *st = smem + s * sb;
         const int r0 = t * H;
         const int rows = min(H, n - r0);
@@ -710,17 +713,17 @@ __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
             }
             mbar_wait(&full[s], (fph >> s) & 1u);
             fph ^= 1u << s;
-            const int ng = hdr[s];
             const unsigned char *st = smem + s * sb;
-            const unsigned char *sv = st;
-            const unsigned char *sc = st + static_cast<size_t>(ng) * H * GS * VB;
+            const int2 gh = *reinterpret_cast<const int2 *>(st);
+            const int ng = gh.x, nfull = gh.y;
+            const unsigned char *sv = st + kSgHdr;
+            const unsigned char *sc = sv + static_cast<size_t>(ng) * H * GS * VB;
             const uint16_t *meta = reinterpret_cast<const uint16_t *>(sc + static_cast<size_t>(ng) * H * GS * CB);
             const double *sf = reinterpret_cast<const double *>(st + (sb - 8 * H));
             const bool f_staged = it >= S - 1 && f_al;
             const int r0 = t * H;
-#pragma unroll
-            for (int rr = 0; rr < RPT; ++rr) {
-                const int lr = tid + rr * kTileRows;  // row within the slice
+            {
+                const int lr = tid;  // row within the slice
                 const int row = r0 + lr;
                 if (row < n) {
                     const uint32_t m = meta[lr];
@@ -731,12 +734,12 @@ __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
                     if constexpr (MODE >= M_JACOBI) xi = xval<MODE, false>(row, x, f, aux, omega);
                     const double *xrow = x + row;
                     double sum = 0.0;
-                    for (int g = 0; g < ng; ++g) {
+                    // slot u of group g: value, gathered x (loads only; no arithmetic)
+                    auto load = [&](int g, double *a, double *xv) {
                         using VT = typename RawVec<GS * VB>::T;
                         using CT = typename RawVec<GS * CB>::T;
                         const VT vv = *reinterpret_cast<const VT *>(sv + (static_cast<size_t>(g) * H + lr) * GS * VB);
                         const CT cc = *reinterpret_cast<const CT *>(sc + (static_cast<size_t>(g) * H + lr) * GS * CB);
-                        double a[GS], xv[GS];
 #pragma unroll
                         for (int u = 0; u < GS; ++u) {
                             int col;  // CF 1: the column delta
@@ -758,8 +761,35 @@ __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
                             else
                                 xv[u] = xval<MODE, false>((CF == 1) ? row + col : col, x, f, aux, omega);
                         }
+                    };
+                    // sum += a*x in slot order; slots past the row length leave sum untouched
+                    auto accumulate = [&](int g, const double *a, const double *xv, bool masked) {
+                        if (masked) {
 #pragma unroll
-                        for (int u = 0; u < GS; ++u) add_if(sum, __dmul_rn(a[u], xv[u]), g * GS + u < len);
+                            for (int u = 0; u < GS; ++u) add_if(sum, __dmul_rn(a[u], xv[u]), g * GS + u < len);
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < GS; ++u) sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
+                        }
+                    };
+                    if constexpr (NG > 0) {  // compile-time group count: the gathers of 2 groups in flight at once
+#pragma unroll
+                        for (int g0 = 0; g0 < NG; g0 += 2) {
+                            constexpr int B = 2;
+                            double a[B * GS], xv[B * GS];
+#pragma unroll
+                            for (int q = 0; q < B; ++q)
+                                if (g0 + q < NG && g0 + q < ng) load(g0 + q, a + q * GS, xv + q * GS);
+#pragma unroll
+                            for (int q = 0; q < B; ++q)
+                                if (g0 + q < NG && g0 + q < ng) accumulate(g0 + q, a + q * GS, xv + q * GS, g0 + q >= nfull);
+                        }
+                    } else {
+                        for (int g = 0; g < ng; ++g) {
+                            double a[GS], xv[GS];
+                            load(g, a, xv);
+                            accumulate(g, a, xv, true);
+                        }
                     }
                     double o;
                     if constexpr (MODE == M_SPMV) o = sum;
@@ -1288,7 +1318,7 @@ struct DevLevel {
     double *dict = nullptr;
     // grouped sliced-ELL layout (sell = 1): byte offsets of the slice blocks,
     // the blocks, the reciprocal dictionary (Markstein division)
-    int sell = 0, sell_tiles = 0, sell_ngmax = 0, sell_gs = 4, sell_rpt = 1, sell_grid = 0;
+    int sell = 0, sell_tiles = 0, sell_ngmax = 0, sell_gs = 4, sell_grid = 0;
     size_t sell_smem = 0;
     int64_t *soff = nullptr;
     const unsigned char *sell_blk = nullptr;
@@ -1418,24 +1448,37 @@ static void launch_csr_f(sb_ctx c, const DevLevel &l, cudaStream_t s, const doub
              red);
 }
 
-template <int MODE, int NV, int VF, int CF, int GS, int RPT>
+template <int MODE, int NV, int VF, int CF, int GS, int NG>
 static void launch_sell_g(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
                           double *out, double omega, const int *skip, const Red &red, Aux aux) {
-    launch_k(c, k_sellg<MODE, NV, VF, CF, GS, RPT>, dim3(std::min(l.sell_tiles, l.sell_grid)), dim3(kTileRows),
+    launch_k(c, k_sellg<MODE, NV, VF, CF, GS, NG>, dim3(std::min(l.sell_tiles, l.sell_grid)), dim3(kTileRows),
              l.sell_smem, s, static_cast<int>(l.n), l.sell_tiles, static_cast<const int64_t *>(l.soff), l.sell_blk,
              static_cast<const double *>(l.dict), static_cast<const double *>(l.rdict), l.ndict, l.sell_ngmax, x, f,
              out, omega, skip, aux, red);
 }
 
+// The fast format (dictionary values, int16 deltas, groups of 4) gets a
+// compile-time group count up to 7 (w <= 28: every 2D/3D 5/7/9/27-point
+// stencil level); everything else runs the runtime group loop.
 template <int MODE, int NV, int VF, int CF>
 static void launch_sell_f(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
                           double *out, double omega, const int *skip, const Red &red, Aux aux) {
     if (l.sell_gs == 4) {
-        if (l.sell_rpt == 2) launch_sell_g<MODE, NV, VF, CF, 4, 2>(c, l, s, x, f, out, omega, skip, red, aux);
-        else launch_sell_g<MODE, NV, VF, CF, 4, 1>(c, l, s, x, f, out, omega, skip, red, aux);
+        if constexpr (VF == 1 && CF == 1) {
+            switch (l.sell_ngmax) {
+            case 1: return launch_sell_g<MODE, NV, 1, 1, 4, 1>(c, l, s, x, f, out, omega, skip, red, aux);
+            case 2: return launch_sell_g<MODE, NV, 1, 1, 4, 2>(c, l, s, x, f, out, omega, skip, red, aux);
+            case 3: return launch_sell_g<MODE, NV, 1, 1, 4, 3>(c, l, s, x, f, out, omega, skip, red, aux);
+            case 4: return launch_sell_g<MODE, NV, 1, 1, 4, 4>(c, l, s, x, f, out, omega, skip, red, aux);
+            case 5: return launch_sell_g<MODE, NV, 1, 1, 4, 5>(c, l, s, x, f, out, omega, skip, red, aux);
+            case 6: return launch_sell_g<MODE, NV, 1, 1, 4, 6>(c, l, s, x, f, out, omega, skip, red, aux);
+            case 7: return launch_sell_g<MODE, NV, 1, 1, 4, 7>(c, l, s, x, f, out, omega, skip, red, aux);
+            default: break;
+            }
+        }
+        launch_sell_g<MODE, NV, VF, CF, 4, 0>(c, l, s, x, f, out, omega, skip, red, aux);
     } else {
-        if (l.sell_rpt == 2) launch_sell_g<MODE, NV, VF, CF, 2, 2>(c, l, s, x, f, out, omega, skip, red, aux);
-        else launch_sell_g<MODE, NV, VF, CF, 2, 1>(c, l, s, x, f, out, omega, skip, red, aux);
+        launch_sell_g<MODE, NV, VF, CF, 2, 0>(c, l, s, x, f, out, omega, skip, red, aux);
     }
 }
 
@@ -1853,9 +1896,7 @@ static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
     // grouped sliced-ELL conversion (SB_SELL=0 keeps the CSR pipeline)
     const char *se = std::getenv("SB_SELL");
     if ((!se || std::atoi(se) != 0) && A.n > 0) {
-        const char *re = std::getenv("SB_RPT");
-        const int rpt = (re && std::atoi(re) == 2) ? 2 : 1;
-        const int64_t H = static_cast<int64_t>(kTileRows) * rpt;
+        const int64_t H = kTileRows;
         const int64_t nt = (A.n + H - 1) / H;
         std::vector<int> wt(static_cast<size_t>(nt), 0);
         int wmax = 0;
@@ -1900,8 +1941,13 @@ static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
             for (int64_t t = 0; t < nt; ++t) {
                 const int ng = (wt[static_cast<size_t>(t)] + gs - 1) / gs;
                 unsigned char *b = blk.data() + off[static_cast<size_t>(t)];
-                unsigned char *bv = b;
-                unsigned char *bc = b + static_cast<size_t>(ng) * H * gs * VB;
+                int lmin = 1 << 30;
+                for (int64_t r = t * H; r < std::min<int64_t>(A.n, (t + 1) * H); ++r)
+                    lmin = std::min<int>(lmin, static_cast<int>(A.rp[r + 1] - A.rp[r]));
+                const int32_t hd[4] = {ng, std::min(ng, lmin / gs), 0, 0};
+                std::memcpy(b, hd, sizeof hd);
+                unsigned char *bv = b + kSgHdr;
+                unsigned char *bc = bv + static_cast<size_t>(ng) * H * gs * VB;
                 unsigned char *bm = bc + static_cast<size_t>(ng) * H * gs * CB;
                 for (int64_t r = t * H; r < std::min<int64_t>(A.n, (t + 1) * H); ++r) {
                     const int64_t lr = r - t * H;
@@ -1964,7 +2010,6 @@ static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
             D.sell_tiles = static_cast<int>(nt);
             D.sell_ngmax = ngmax;
             D.sell_gs = gs;
-            D.sell_rpt = rpt;
             D.sell_slots = slots;
             D.sell_smem = kSgStages * stage;
         }
@@ -1995,10 +2040,17 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
 }
 
 template <int MODE, int NV, int VF, int CF> static void set_sg_attr(int b) {
-    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_sellg<MODE, NV, VF, CF, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    if constexpr (VF == 1 && CF == 1) {
+        CK(cudaFuncSetAttribute(k_sellg<MODE, NV, 1, 1, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_sellg<MODE, NV, 1, 1, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_sellg<MODE, NV, 1, 1, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_sellg<MODE, NV, 1, 1, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_sellg<MODE, NV, 1, 1, 4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_sellg<MODE, NV, 1, 1, 4, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_sellg<MODE, NV, 1, 1, 4, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    }
 }
 
 template <int MODE, int NV> static void set_smem_attr(size_t smem) {
@@ -2337,7 +2389,7 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
         l.grid = std::max(1, nsm * std::max(occ, 1));
         if (l.sell) {
             occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sellg<M_JACOBI, 0, 1, 1, 4, 1>, kTileRows,
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sellg<M_JACOBI, 0, 1, 1, 4, 0>, kTileRows,
                                                              l.sell_smem));
             l.sell_grid = std::max(1, nsm * std::max(occ, 1));
         }
