@@ -834,23 +834,36 @@ __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
 constexpr int kTailMaxLevels = 24;
 constexpr int kTailThreads = 512;
 
+// Per tail level, byte offsets into every CTA's shared memory (identical in
+// all CTAs). The matrix part ("image") of each CTA is prepared on the host and
+// arrives with ONE TMA bulk copy; the vectors follow the image.
+//   ngh  int32[kTailMaxLevels] at offset 0: this CTA's ghost count per level
+//   rp   int32[rows_per + 1]  local CSR offsets of the CTA's rows
+//   col  uint16[nnz_cap]      column renumbered into [own rows | ghosts]
+//   val  uint8 dictionary index (vf) or f64 value, per entry
+//   dix  uint8 dictionary index of a_ii (vf) or f64 a_ii, per row
+//   gh   uint32[gh_cap]       ghost sources: owner CTA << 16 | owner-local row,
+//                             sorted by (owner, row) so pulls are coalesced
+//   agg  uint32 packed coarse parent per row; mem: 2 x uint32 packed members
+//        per owned coarse row (0xffffffff: none)
+//   dict / rdict: the level's distinct values and their RN reciprocals
+// x and t hold [own | ghost] values; a sweep first pulls its input's ghosts
+// over DSMEM (only the halo crosses CTAs), then runs on local shared memory.
 struct TailLevel {
-    int n, nc;        // rows; coarse rows (-1 on the coarsest)
-    int rows_per;     // rows owned per CTA (last CTA may own fewer)
-    int nnz_cap;      // max local nnz over CTAs
-    const int32_t *rp, *ci, *agg;
-    const double *v, *diag;
-    const int2 *mem;  // members of coarse rows (next level)
-    // shared-memory offsets (bytes) of this level's block
-    int o_rp, o_ci, o_v, o_diag, o_agg, o_mem, o_x, o_t, o_f, o_r;
+    int n, rows_per, gh_cap, vf, ndict;
+    int o_rp, o_col, o_val, o_dix, o_gh, o_agg, o_mem, o_dict, o_rdict;
+    int o_x, o_t, o_f, o_r;
 };
 
 struct TailDesc {
-    int nlev;          // including the coarsest
-    int ncoarse;
-    int o_inv, o_fc;   // coarsest: owned inverse rows, full f_c copy
+    int nlev;      // including the coarsest
+    int ncoarse;   // coarsest rows
+    int rows_c;    // coarsest rows per CTA
+    int img_bytes; // per-CTA image (multiple of 16)
+    int o_inv;     // coarsest: the CTA's rows of A_c^{-1} (image)
+    int o_fc;      // coarsest: gathered f_c (all rows)
     int smem_bytes;
-    const double *inv;
+    const unsigned char *img;  // ctas * img_bytes
     TailLevel L[kTailMaxLevels];
 };
 
@@ -863,17 +876,16 @@ __device__ __forceinline__ unsigned cluster_rank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
-__device__ __forceinline__ unsigned cluster_ncta() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-    return r;
-}
-// f64 at the same shared-memory offset in CTA `cta` of the cluster
-__device__ __forceinline__ double dsmem_ld(const double *local, unsigned cta) {
-    uint32_t a = smem_u32(local), ra;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(cta));
+// f64 of vector `o_vec` at packed (owner CTA << 16 | row): local shared load
+// when this CTA owns it, a DSMEM load otherwise
+__device__ __forceinline__ double cl_get(unsigned char *sb, uint32_t base, unsigned me, int o_vec, uint32_t e) {
+    const uint32_t own = e >> 16, row = e & 0xffffu;
+    if (own == me) return reinterpret_cast<const double *>(sb + o_vec)[row];
+    const uint32_t a = base + static_cast<uint32_t>(o_vec) + (row << 3);
+    uint32_t ra;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(own));
     double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
     return v;
 }
 
@@ -881,49 +893,59 @@ template <typename T> __device__ __forceinline__ T *sm(unsigned char *base, int 
     return reinterpret_cast<T *>(base + off);
 }
 
-// value of global row j of a level vector stored block-wise at offset `off`
-__device__ __forceinline__ double tget(unsigned char *base, int off, int j, int rows_per, unsigned me) {
-    const unsigned o = static_cast<unsigned>(j / rows_per);
-    const double *p = sm<double>(base, off) + (j - static_cast<int>(o) * rows_per);
-    return o == me ? *p : dsmem_ld(p, o);
+// ghosts of vector o_vec (level l) <- their owners' values (after a cluster barrier)
+__device__ __forceinline__ void tail_pull(unsigned char *sb, uint32_t base, unsigned me, const TailLevel &l,
+                                          int ngh, int o_vec) {
+    const uint32_t *gh = sm<uint32_t>(sb, l.o_gh);
+    double *dst = sm<double>(sb, o_vec) + l.rows_per;
+    for (int g = threadIdx.x; g < ngh; g += blockDim.x) dst[g] = cl_get(sb, base, me, o_vec, gh[g]);
+    __syncthreads();
 }
 
-// one Jacobi sweep (or residual when RESID) over the CTA's own rows:
-// out_i = x_i + w (f_i - sum_k a_k x_{c_k}) / a_ii, sum in CSR order
+__device__ __forceinline__ void tail_diag(unsigned char *sb, const TailLevel &l, int li, double &d, double &y) {
+    if (l.vf) {
+        const int di = sm<uint8_t>(sb, l.o_dix)[li];
+        d = sm<double>(sb, l.o_dict)[di];
+        y = sm<double>(sb, l.o_rdict)[di];
+    } else {
+        d = sm<double>(sb, l.o_dix)[li];
+        y = 0.0;
+    }
+}
+
+// One sweep over the CTA's rows of level l (CSR order, no FMA: bitwise the
+// reference's), all operands local: RESID: out = f - A x; else
+// out = x + w (f - A x) / a_ii.
 template <bool RESID>
-__device__ __forceinline__ void tail_sweep(unsigned char *sb, const TailLevel &l, int o_in, int o_out,
-                                           double omega, unsigned me, int r0, int m) {
+__device__ __forceinline__ void tail_sweep(unsigned char *sb, const TailLevel &l, int o_in, int o_out, double omega,
+                                           int m) {
     const int32_t *rp = sm<int32_t>(sb, l.o_rp);
-    const int32_t *ci = sm<int32_t>(sb, l.o_ci);
-    const double *v = sm<double>(sb, l.o_v);
-    const double *f = sm<double>(sb, l.o_f);
+    const uint16_t *col = sm<uint16_t>(sb, l.o_col);
     const double *xin = sm<double>(sb, o_in);
-    double *out = sm<double>(sb, o_out);
+    const double *f = sm<double>(sb, l.o_f);
+    const double *dict = sm<double>(sb, l.o_dict);
     for (int li = threadIdx.x; li < m; li += blockDim.x) {
-        const int row = r0 + li;
         const int rs = rp[li], re = rp[li + 1];
-        double sum = 0.0, d = 0.0;
+        double sum = 0.0;
         for (int k = rs; k < re; k += 4) {
-            int c[4];
             double a[4], xv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (k + u < re) {
-                    c[u] = ci[k + u];
-                    a[u] = v[k + u];
+                    a[u] = l.vf ? dict[sm<uint8_t>(sb, l.o_val)[k + u]] : sm<double>(sb, l.o_val)[k + u];
+                    xv[u] = xin[col[k + u]];
                 }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (k + u < re) xv[u] = tget(sb, o_in, c[u], l.rows_per, me);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (k + u < re) {
-                    sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
-                    if (c[u] == row) d = a[u];
-                }
+                if (k + u < re) sum = __dadd_rn(sum, __dmul_rn(a[u], xv[u]));
         }
-        if constexpr (RESID) out[li] = __dsub_rn(f[li], sum);
-        else out[li] = __dadd_rn(xin[li], __ddiv_rn(__dmul_rn(omega, __dsub_rn(f[li], sum)), d));
+        if constexpr (RESID) {
+            sm<double>(sb, o_out)[li] = __dsub_rn(f[li], sum);
+        } else {
+            double d, y;
+            tail_diag(sb, l, li, d, y);
+            sm<double>(sb, o_out)[li] = __dadd_rn(xin[li], div_rn(__dmul_rn(omega, __dsub_rn(f[li], sum)), d, y));
+        }
     }
 }
 
@@ -931,149 +953,143 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     k_tail(const TailDesc *__restrict__ Dg, const double *f0, double *X0, double omega, int pre, int post,
            unsigned long long *trace) {
     extern __shared__ __align__(16) unsigned char sb[];
+    __shared__ TailDesc D;
+    __shared__ __align__(8) uint64_t bar;
     int ntr = 0;
     auto mark = [&]() {
         if (trace && threadIdx.x == 0 && cluster_rank() == 0 && ntr < 255) trace[1 + ntr++] = globaltimer();
     };
     mark();
-    __shared__ TailDesc D;
-    // descriptor into shared memory (uniform reads below)
+    const unsigned me = cluster_rank();
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(TailDesc) / 4); i += blockDim.x)
         reinterpret_cast<int *>(&D)[i] = reinterpret_cast<const int *>(Dg)[i];
-    __syncthreads();
-    const unsigned me = cluster_rank();
-    const int nlev = D.nlev;
-
-    // ---- load this CTA's block of every level into shared memory --------------
-    for (int q = 0; q + 1 < nlev; ++q) {
-        const TailLevel &l = D.L[q];
-        const int r0 = static_cast<int>(me) * l.rows_per;
-        const int m = max(0, min(l.rows_per, l.n - r0));
-        const int e0 = m > 0 ? __ldg(l.rp + r0) : 0;
-        const int e1 = m > 0 ? __ldg(l.rp + r0 + m) : 0;
-        int32_t *rp = sm<int32_t>(sb, l.o_rp);
-        for (int i = threadIdx.x; i <= m; i += blockDim.x) rp[i] = (m > 0 ? __ldg(l.rp + r0 + i) : 0) - e0;
-        for (int k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
-            sm<int32_t>(sb, l.o_ci)[k] = __ldg(l.ci + e0 + k);
-            sm<double>(sb, l.o_v)[k] = __ldg(l.v + e0 + k);
-        }
-        for (int i = threadIdx.x; i < m; i += blockDim.x) {
-            sm<double>(sb, l.o_diag)[i] = __ldg(l.diag + r0 + i);
-            sm<int32_t>(sb, l.o_agg)[i] = __ldg(l.agg + r0 + i);
-        }
-        const TailLevel &lc = D.L[q + 1];
-        const int c0 = static_cast<int>(me) * lc.rows_per;
-        const int mc = max(0, min(lc.rows_per, lc.n - c0));
-        for (int c = threadIdx.x; c < mc; c += blockDim.x) sm<int2>(sb, l.o_mem)[c] = __ldg(l.mem + c0 + c);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // this CTA's matrix image: one bulk copy (constant data: before the dependency wait)
+        mbar_expect_tx(&bar, static_cast<uint32_t>(D.img_bytes));
+        bulk_g2s(sb, D.img + static_cast<size_t>(me) * D.img_bytes, static_cast<uint32_t>(D.img_bytes), &bar);
+    }
+    const int nlev = D.nlev;
+    const uint32_t base = smem_u32(sb);
+    const int *ngh = sm<int>(sb, 0);
+    auto rows_of = [&](const TailLevel &l) { return max(0, min(l.rows_per, l.n - static_cast<int>(me) * l.rows_per)); };
     pdl_wait();  // the predecessor (restriction) has produced f0
     {
         const TailLevel &l = D.L[0];
-        const int r0 = static_cast<int>(me) * l.rows_per;
-        const int m = max(0, min(l.rows_per, l.n - r0));
+        const int r0 = static_cast<int>(me) * l.rows_per, m = rows_of(l);
         for (int i = threadIdx.x; i < m; i += blockDim.x) sm<double>(sb, l.o_f)[i] = __ldcg(f0 + r0 + i);
     }
-    if (nlev >= 1) {  // coarsest: own rows of the inverse
-        const TailLevel &l = D.L[nlev - 1];
-        const int r0 = static_cast<int>(me) * l.rows_per;
-        const int m = max(0, min(l.rows_per, l.n - r0));
-        double *inv = sm<double>(sb, D.o_inv);
-        for (int k = threadIdx.x; k < m * D.ncoarse; k += blockDim.x)
-            inv[k] = __ldg(D.inv + static_cast<size_t>(r0) * D.ncoarse + k);
-    }
-    cluster_sync_all();
+    mbar_wait(&bar, 0u);
+    __syncthreads();
     mark();
 
     uint32_t cur_is_x = 0u;  // per level: pre-smoothed iterate in x (1) or t (0)
-    // ---- down -----------------------------------------------------------------
-    for (int q = 0; q < nlev; ++q) {
+    // ---- down -------------------------------------------------------------------
+    for (int q = 0; q + 1 < nlev; ++q) {
         const TailLevel &l = D.L[q];
-        const int r0 = static_cast<int>(me) * l.rows_per;
-        const int m = max(0, min(l.rows_per, l.n - r0));
-        if (q + 1 == nlev) {  // coarsest: gather f_c, then own rows of A_c^{-1} f_c
-            double *fc = sm<double>(sb, D.o_fc);
-            for (int j = threadIdx.x; j < D.ncoarse; j += blockDim.x) fc[j] = tget(sb, l.o_f, j, l.rows_per, me);
-            __syncthreads();
-            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-            const double *inv = sm<double>(sb, D.o_inv);
-            for (int li = warp; li < m; li += nw) {
-                double acc = 0.0;
-                for (int j = lane; j < D.ncoarse; j += 32) acc += inv[static_cast<size_t>(li) * D.ncoarse + j] * fc[j];
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-                if (lane == 0) sm<double>(sb, l.o_x)[li] = acc;
-            }
-            cluster_sync_all();
-    mark();
-            break;
-        }
-        // plan: the prolongation runs in place on the pre-smoothed iterate and
-        // the post-sweeps must end in x
+        const int m = rows_of(l);
+        // buffer plan: the prolongation runs in place on the pre-smoothed
+        // iterate and the post-sweeps must end in x
         const int pre_end = (post % 2 == 0) ? l.o_x : l.o_t;
         int cur = pre_end;
         if (pre == 0) {
             for (int i = threadIdx.x; i < m; i += blockDim.x) sm<double>(sb, pre_end)[i] = 0.0;
         } else {
             const int first = (pre % 2 == 1) ? pre_end : (pre_end == l.o_x ? l.o_t : l.o_x);
-            const double *f = sm<double>(sb, l.o_f);
-            const double *dg = sm<double>(sb, l.o_diag);
-            for (int i = threadIdx.x; i < m; i += blockDim.x)  // sweep 1 from x = 0
-                sm<double>(sb, first)[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, f[i]), dg[i]));
+            if (q == 0)  // deeper levels: done by the restriction
+                for (int li = threadIdx.x; li < m; li += blockDim.x) {
+                    double d, y;
+                    tail_diag(sb, l, li, d, y);
+                    sm<double>(sb, first)[li] = __dadd_rn(0.0, div_rn(__dmul_rn(omega, sm<double>(sb, l.o_f)[li]), d, y));
+                }
             cur = first;
             for (int sw = 1; sw < pre; ++sw) {
                 cluster_sync_all();
-    mark();
+                mark();
+                tail_pull(sb, base, me, l, ngh[q], cur);
                 const int nxt = cur == l.o_x ? l.o_t : l.o_x;
-                tail_sweep<false>(sb, l, cur, nxt, omega, me, r0, m);
+                tail_sweep<false>(sb, l, cur, nxt, omega, m);
                 cur = nxt;
             }
         }
         if (cur == l.o_x) cur_is_x |= 1u << q;
         cluster_sync_all();
-    mark();
-        tail_sweep<true>(sb, l, cur, l.o_r, omega, me, r0, m);  // r = f - A x
+        mark();
+        tail_pull(sb, base, me, l, ngh[q], cur);
+        tail_sweep<true>(sb, l, cur, l.o_r, omega, m);  // r = f - A x
         cluster_sync_all();
-    mark();
-        // restriction: f_c[c] = (0.0 + r[m0]) + r[m1] (ascending members)
+        mark();
+        // restriction f_c = (0 + r[m0]) + r[m1]; the coarse level's first sweep rides along
         const TailLevel &lc = D.L[q + 1];
-        const int c0 = static_cast<int>(me) * lc.rows_per;
-        const int mc = max(0, min(lc.rows_per, lc.n - c0));
+        const bool coarsest = q + 2 == nlev;
+        const int mc = rows_of(lc);
+        const int pe_c = (post % 2 == 0) ? lc.o_x : lc.o_t;
+        const int first_c = (pre % 2 == 1) ? pe_c : (pe_c == lc.o_x ? lc.o_t : lc.o_x);
+        const uint2 *mem = sm<uint2>(sb, l.o_mem);
         for (int c = threadIdx.x; c < mc; c += blockDim.x) {
-            const int2 mm = sm<int2>(sb, l.o_mem)[c];
-            double acc = __dadd_rn(0.0, tget(sb, l.o_r, mm.x, l.rows_per, me));
-            if (mm.y >= 0) acc = __dadd_rn(acc, tget(sb, l.o_r, mm.y, l.rows_per, me));
+            const uint2 mm = mem[c];
+            double acc = __dadd_rn(0.0, cl_get(sb, base, me, l.o_r, mm.x));
+            if (mm.y != 0xffffffffu) acc = __dadd_rn(acc, cl_get(sb, base, me, l.o_r, mm.y));
             sm<double>(sb, lc.o_f)[c] = acc;
+            if (!coarsest && pre >= 1) {
+                double d, y;
+                tail_diag(sb, lc, c, d, y);
+                sm<double>(sb, first_c)[c] = __dadd_rn(0.0, div_rn(__dmul_rn(omega, acc), d, y));
+            }
         }
-        cluster_sync_all();
-    mark();
     }
-    // ---- up -----------------------------------------------------------------------
+    // ---- coarsest: gather f_c, own rows of A_c^{-1} f_c ------------------------------------
+    {
+        const TailLevel &l = D.L[nlev - 1];
+        cluster_sync_all();
+        mark();
+        double *fc = sm<double>(sb, D.o_fc);
+        for (int j = threadIdx.x; j < D.ncoarse; j += blockDim.x) {
+            const uint32_t own = static_cast<uint32_t>(j / D.rows_c);
+            fc[j] = cl_get(sb, base, me, l.o_f, (own << 16) | static_cast<uint32_t>(j - static_cast<int>(own) * D.rows_c));
+        }
+        __syncthreads();
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        const int mcr = rows_of(l);
+        const double *inv = sm<double>(sb, D.o_inv);
+        for (int li = warp; li < mcr; li += nw) {
+            double acc = 0.0;
+            for (int j = lane; j < D.ncoarse; j += 32) acc += inv[static_cast<size_t>(li) * D.ncoarse + j] * fc[j];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+            if (lane == 0) sm<double>(sb, l.o_x)[li] = acc;
+        }
+    }
+    // ---- up -------------------------------------------------------------------------------
     for (int q = nlev - 2; q >= 0; --q) {
         const TailLevel &l = D.L[q];
         const TailLevel &lc = D.L[q + 1];
-        const int r0 = static_cast<int>(me) * l.rows_per;
-        const int m = max(0, min(l.rows_per, l.n - r0));
+        const int m = rows_of(l);
         int cur = (cur_is_x >> q) & 1u ? l.o_x : l.o_t;
+        cluster_sync_all();
+        mark();
         // x += P x_c: x_i + (0.0 + x_c[agg_i]) (cycle.hpp:72-73), in place
+        const uint32_t *agg = sm<uint32_t>(sb, l.o_agg);
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
             double *xi = sm<double>(sb, cur) + i;
-            *xi = __dadd_rn(*xi, __dadd_rn(0.0, tget(sb, lc.o_x, sm<int32_t>(sb, l.o_agg)[i], lc.rows_per, me)));
+            *xi = __dadd_rn(*xi, __dadd_rn(0.0, cl_get(sb, base, me, lc.o_x, agg[i])));
         }
         for (int sw = 0; sw < post; ++sw) {
             cluster_sync_all();
-    mark();
+            mark();
+            tail_pull(sb, base, me, l, ngh[q], cur);
             const int nxt = cur == l.o_x ? l.o_t : l.o_x;
-            tail_sweep<false>(sb, l, cur, nxt, omega, me, r0, m);
+            tail_sweep<false>(sb, l, cur, nxt, omega, m);
             cur = nxt;
         }
-        cluster_sync_all();
-    mark();
     }
-    // ---- result of tail level 0 -> X0 --------------------------------------------
+    // ---- result of tail level 0 -> X0 ------------------------------------------------------
     {
         const TailLevel &l = D.L[0];
-        const int r0 = static_cast<int>(me) * l.rows_per;
-        const int m = max(0, min(l.rows_per, l.n - r0));
+        const int r0 = static_cast<int>(me) * l.rows_per, m = rows_of(l);
         for (int i = threadIdx.x; i < m; i += blockDim.x) X0[r0 + i] = sm<double>(sb, l.o_x)[i];
     }
     cluster_sync_all();  // no CTA exits while others may still read its shared memory
@@ -2100,13 +2116,15 @@ static void setup_tail(sb_ctx c, const Hier &H) {
     c->tail_from = 1 << 30;
     const char *env = std::getenv("SB_TAIL_ROWS");
     const long long tail_rows = env ? std::atoll(env) : (1ll << 20);
-    if (tail_rows <= 0 || c->nc <= 0 || c->coarse_exact) return;
+    if (tail_rows <= 0 || c->nc <= 0 || c->coarse_exact || L < 2) return;
     CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int dev_smem = 0;
     CK(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
     const int budget = dev_smem - static_cast<int>(sizeof(TailDesc)) - 1024;
     int ctas = 0;
-    for (int want : {16, 8}) {
+    const char *ce = std::getenv("SB_TAIL_CTAS");
+    for (int want : {16, 8, 4}) {
+        if (ce && std::atoi(ce) != want) continue;
         CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(want, 1, 1);
@@ -2127,84 +2145,210 @@ static void setup_tail(sb_ctx c, const Hier &H) {
         cudaGetLastError();
     }
     if (ctas == 0) return;
-    auto align16 = [](int x) { return (x + 15) & ~15; };
-    // per-level block sizes (bytes) for a given start level
-    auto level_bytes = [&](int k, int &rows_per, int &nnz_cap) {
-        const HostLevel &hl = H.levels[static_cast<size_t>(k)];
-        rows_per = static_cast<int>((hl.A.n + ctas - 1) / ctas);
-        nnz_cap = 0;
-        for (int r = 0; r < ctas; ++r) {
-            const int64_t a = std::min<int64_t>(hl.A.n, static_cast<int64_t>(r) * rows_per);
-            const int64_t b = std::min<int64_t>(hl.A.n, static_cast<int64_t>(r + 1) * rows_per);
-            nnz_cap = std::max<int>(nnz_cap, static_cast<int>(hl.A.rp[b] - hl.A.rp[a]));
-        }
-        return align16(4 * (rows_per + 1)) + align16(4 * nnz_cap) + align16(8 * nnz_cap) +
-               align16(8 * rows_per) * 6 /* diag x t f r + agg(4) mem(8/2) */;
-    };
+    auto a16 = [](int64_t x) { return (x + 15) & ~int64_t(15); };
     const int nc = static_cast<int>(c->nc);
     const int rows_c = (nc + ctas - 1) / ctas;
-    int total = align16(8 * rows_c * nc) + align16(8 * nc) + align16(8 * rows_c) * 2;
+    auto rows_per_of = [&](int k) {
+        return k == L - 1 ? rows_c : static_cast<int>((H.levels[static_cast<size_t>(k)].A.n + ctas - 1) / ctas);
+    };
+    // per level: rows per CTA, max local nnz, per-CTA ghost lists, value dictionary (<= 256 distinct)
+    struct LevInfo {
+        int rows_per = 0, nnz_cap = 0, gh_cap = 0, vf = 0;
+        std::vector<std::vector<int64_t>> ghosts;  // per CTA: sorted remote columns
+        std::vector<double> dict;
+        std::map<uint64_t, int> ids;
+    };
+    std::vector<LevInfo> info(static_cast<size_t>(L));
+    auto level_bytes = [&](int k) -> int64_t {  // image + vectors of a non-coarsest tail level, per CTA
+        LevInfo &li = info[static_cast<size_t>(k)];
+        const HostCsr &A = H.levels[static_cast<size_t>(k)].A;
+        li.rows_per = rows_per_of(k);
+        li.nnz_cap = li.gh_cap = 0;
+        li.ghosts.assign(static_cast<size_t>(ctas), {});
+        for (int r = 0; r < ctas; ++r) {
+            const int64_t a = std::min<int64_t>(A.n, static_cast<int64_t>(r) * li.rows_per);
+            const int64_t b = std::min<int64_t>(A.n, static_cast<int64_t>(r + 1) * li.rows_per);
+            li.nnz_cap = std::max<int>(li.nnz_cap, static_cast<int>(A.rp[b] - A.rp[a]));
+            std::vector<int64_t> &g = li.ghosts[static_cast<size_t>(r)];
+            for (int64_t e = A.rp[a]; e < A.rp[b]; ++e)
+                if (A.ci[e] < a || A.ci[e] >= b) g.push_back(A.ci[e]);
+            std::sort(g.begin(), g.end());
+            g.erase(std::unique(g.begin(), g.end()), g.end());
+            li.gh_cap = std::max<int>(li.gh_cap, static_cast<int>(g.size()));
+        }
+        li.dict.clear();
+        li.ids.clear();
+        li.vf = 1;
+        for (int64_t e = 0; e < A.nnz() && li.vf; ++e) {
+            uint64_t bits;
+            std::memcpy(&bits, &A.v[e], 8);
+            if (li.ids.find(bits) == li.ids.end()) {
+                if (li.dict.size() == 256) li.vf = 0;
+                else {
+                    li.ids[bits] = static_cast<int>(li.dict.size());
+                    li.dict.push_back(A.v[e]);
+                }
+            }
+        }
+        if (li.rows_per + li.gh_cap > 65535) return INT64_MAX / 4;
+        const int rpc = rows_per_of(k + 1);
+        const int vb = li.vf ? 1 : 8;
+        return a16(4 * (li.rows_per + 1)) + a16(2 * li.nnz_cap) + a16(vb * li.nnz_cap) + a16(vb * li.rows_per) +
+               a16(4 * li.gh_cap) + a16(4 * li.rows_per) + a16(8 * rpc) +
+               (li.vf ? 2 * a16(8 * static_cast<int64_t>(li.dict.size())) : 0) +
+               2 * a16(8 * (li.rows_per + li.gh_cap)) + 2 * a16(8 * li.rows_per);
+    };
+    int64_t total = a16(4 * kTailMaxLevels) + a16(8 * static_cast<int64_t>(rows_c) * nc) + a16(8 * nc) +
+                    2 * a16(8 * rows_c);
     int k0 = L - 1;
-    if (k0 < c->tail_min) return;
     while (k0 > c->tail_min) {
-        int rp_, nz_;
-        const int add = level_bytes(k0 - 1, rp_, nz_);
-        if (total + add > budget || c->L[static_cast<size_t>(k0) - 1].n > tail_rows ||
-            L - (k0 - 1) > kTailMaxLevels)
-            break;
+        const int k = k0 - 1;
+        if (c->L[static_cast<size_t>(k)].n > tail_rows || L - k > kTailMaxLevels) break;
+        if ((H.levels[static_cast<size_t>(k)].A.n + ctas - 1) / ctas > 32768) break;
+        const int64_t add = level_bytes(k);
+        if (total + add > budget) break;
         total += add;
-        --k0;
+        k0 = k;
     }
+    if (k0 >= L - 1) return;  // nothing above the coarsest fits
+    for (int k = k0; k + 1 < L; ++k) level_bytes(k);  // (re-)fill info for the chosen levels
     TailDesc d;
     std::memset(&d, 0, sizeof(d));
     d.nlev = L - k0;
     d.ncoarse = nc;
-    d.inv = c->inv;
-    int off = 0;
-    auto take = [&](int bytes) {
-        const int o = off;
-        off += align16(bytes);
-        return o;
+    d.rows_c = rows_c;
+    int64_t off = 0;
+    auto take = [&](int64_t bytes) {
+        const int64_t o = off;
+        off += a16(bytes);
+        return static_cast<int>(o);
     };
-    for (int q = 0; q < d.nlev; ++q) {
+    take(4 * kTailMaxLevels);  // per-level ghost counts of this CTA
+    for (int q = 0; q + 1 < d.nlev; ++q) {
         const int k = k0 + q;
-        const DevLevel &l = c->L[static_cast<size_t>(k)];
+        const LevInfo &li = info[static_cast<size_t>(k)];
         TailLevel &t = d.L[q];
-        t.n = static_cast<int>(l.n);
-        t.nc = static_cast<int>(l.nc);
-        t.rp = l.rp;
-        t.ci = l.ci;
-        t.agg = l.agg;
-        t.v = l.v;
-        t.diag = l.diag;
-        t.mem = l.mem;
-        if (q + 1 < d.nlev) {
-            level_bytes(k, t.rows_per, t.nnz_cap);
-            t.o_rp = take(4 * (t.rows_per + 1));
-            t.o_ci = take(4 * t.nnz_cap);
-            t.o_v = take(8 * t.nnz_cap);
-            t.o_diag = take(8 * t.rows_per);
-            t.o_agg = take(4 * t.rows_per);
-            t.o_x = take(8 * t.rows_per);
-            t.o_t = take(8 * t.rows_per);
-            t.o_f = take(8 * t.rows_per);
-            t.o_r = take(8 * t.rows_per);
-        } else {
-            t.rows_per = rows_c;
-            t.o_x = take(8 * rows_c);
-            t.o_f = take(8 * rows_c);
-        }
+        const int vb = li.vf ? 1 : 8;
+        t.n = static_cast<int>(H.levels[static_cast<size_t>(k)].A.n);
+        t.rows_per = li.rows_per;
+        t.gh_cap = li.gh_cap;
+        t.vf = li.vf;
+        t.ndict = static_cast<int>(li.dict.size());
+        t.o_rp = take(4 * (li.rows_per + 1));
+        t.o_col = take(2 * li.nnz_cap);
+        t.o_val = take(vb * li.nnz_cap);
+        t.o_dix = take(vb * li.rows_per);
+        t.o_gh = take(4 * li.gh_cap);
+        t.o_agg = take(4 * li.rows_per);
+        t.o_mem = take(8 * rows_per_of(k + 1));
+        t.o_dict = li.vf ? take(8 * t.ndict) : 0;
+        t.o_rdict = li.vf ? take(8 * t.ndict) : 0;
     }
-    for (int q = 0; q + 1 < d.nlev; ++q) d.L[q].o_mem = take(8 * d.L[q + 1].rows_per);
-    d.o_inv = take(8 * rows_c * nc);
+    d.o_inv = take(8 * static_cast<int64_t>(rows_c) * nc);
+    d.img_bytes = static_cast<int>(off);
+    for (int q = 0; q + 1 < d.nlev; ++q) {  // vectors
+        TailLevel &t = d.L[q];
+        t.o_x = take(8 * (t.rows_per + t.gh_cap));
+        t.o_t = take(8 * (t.rows_per + t.gh_cap));
+        t.o_f = take(8 * t.rows_per);
+        t.o_r = take(8 * t.rows_per);
+    }
+    {
+        TailLevel &t = d.L[d.nlev - 1];
+        t.n = nc;
+        t.rows_per = rows_c;
+        t.o_x = take(8 * rows_c);
+        t.o_f = take(8 * rows_c);
+    }
     d.o_fc = take(8 * nc);
-    d.smem_bytes = off;
-    if (off > budget) return;  // (should not happen: sized above)
+    d.smem_bytes = static_cast<int>(off);
+    if (off > budget) return;
+    // per-CTA images
+    std::vector<unsigned char> img(static_cast<size_t>(ctas) * d.img_bytes, 0);
+    auto pack = [](int64_t j, int rp) { return static_cast<uint32_t>(((j / rp) << 16) | (j % rp)); };
+    for (int r = 0; r < ctas; ++r) {
+        unsigned char *b = img.data() + static_cast<size_t>(r) * d.img_bytes;
+        auto *ngh = reinterpret_cast<int32_t *>(b);
+        for (int q = 0; q + 1 < d.nlev; ++q) {
+            const int k = k0 + q;
+            const LevInfo &li = info[static_cast<size_t>(k)];
+            const HostLevel &hl = H.levels[static_cast<size_t>(k)];
+            const HostCsr &A = hl.A;
+            const TailLevel &t = d.L[q];
+            const int rpc = rows_per_of(k + 1);
+            const int64_t r0 = std::min<int64_t>(A.n, static_cast<int64_t>(r) * t.rows_per);
+            const int64_t r1 = std::min<int64_t>(A.n, static_cast<int64_t>(r + 1) * t.rows_per);
+            const std::vector<int64_t> &g = li.ghosts[static_cast<size_t>(r)];
+            ngh[q] = static_cast<int32_t>(g.size());
+            auto *gh = reinterpret_cast<uint32_t *>(b + t.o_gh);
+            for (size_t qg = 0; qg < g.size(); ++qg) gh[qg] = pack(g[qg], t.rows_per);
+            auto *rp = reinterpret_cast<int32_t *>(b + t.o_rp);
+            auto *col = reinterpret_cast<uint16_t *>(b + t.o_col);
+            auto *agg = reinterpret_cast<uint32_t *>(b + t.o_agg);
+            for (int64_t i = r0; i < r1; ++i) {
+                const int64_t li_ = i - r0;
+                rp[li_] = static_cast<int32_t>(A.rp[i] - A.rp[r0]);
+                double dg = 0.0;
+                for (int64_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+                    const int64_t le = e - A.rp[r0];
+                    const int64_t j = A.ci[e];
+                    col[le] = static_cast<uint16_t>(
+                        (j >= r0 && j < r1) ? j - r0
+                                            : t.rows_per + (std::lower_bound(g.begin(), g.end(), j) - g.begin()));
+                    if (li.vf) {
+                        uint64_t bits;
+                        std::memcpy(&bits, &A.v[e], 8);
+                        b[t.o_val + le] = static_cast<uint8_t>(li.ids.at(bits));
+                        if (j == i) b[t.o_dix + li_] = static_cast<uint8_t>(li.ids.at(bits));
+                    } else {
+                        std::memcpy(b + t.o_val + 8 * le, &A.v[e], 8);
+                    }
+                    if (j == i) dg = A.v[e];
+                }
+                if (!li.vf) std::memcpy(b + t.o_dix + 8 * li_, &dg, 8);
+                agg[li_] = pack(hl.agg[static_cast<size_t>(i)], rpc);
+            }
+            rp[r1 - r0] = static_cast<int32_t>(A.rp[r1] - A.rp[r0]);
+            // members of the owned coarse rows (ascending fine rows)
+            const int64_t ncl = (k + 1 == L - 1) ? nc : H.levels[static_cast<size_t>(k) + 1].A.n;
+            const int64_t c0 = std::min<int64_t>(ncl, static_cast<int64_t>(r) * rpc);
+            const int64_t c1 = std::min<int64_t>(ncl, static_cast<int64_t>(r + 1) * rpc);
+            auto *mem = reinterpret_cast<uint32_t *>(b + t.o_mem);
+            std::vector<int64_t> m0(static_cast<size_t>(c1 - c0), -1), m1(static_cast<size_t>(c1 - c0), -1);
+            for (int64_t i = 0; i < A.n; ++i) {
+                const int64_t p = hl.agg[static_cast<size_t>(i)];
+                if (p < c0 || p >= c1) continue;
+                auto &a = m0[static_cast<size_t>(p - c0)];
+                if (a < 0) a = i;
+                else m1[static_cast<size_t>(p - c0)] = i;
+            }
+            for (int64_t cc = c0; cc < c1; ++cc) {
+                mem[2 * (cc - c0)] = pack(m0[static_cast<size_t>(cc - c0)], t.rows_per);
+                const int64_t b1 = m1[static_cast<size_t>(cc - c0)];
+                mem[2 * (cc - c0) + 1] = b1 < 0 ? 0xffffffffu : pack(b1, t.rows_per);
+            }
+            if (li.vf) {
+                std::memcpy(b + t.o_dict, li.dict.data(), 8 * li.dict.size());
+                for (size_t qd = 0; qd < li.dict.size(); ++qd) {
+                    const double dv = std::fabs(li.dict[qd]);
+                    const double y = (dv >= std::ldexp(1.0, -100) && dv <= std::ldexp(1.0, 100)) ? 1.0 / li.dict[qd] : 0.0;
+                    std::memcpy(b + t.o_rdict + 8 * qd, &y, 8);
+                }
+            }
+        }
+        const int64_t c0 = std::min<int64_t>(nc, static_cast<int64_t>(r) * rows_c);
+        const int64_t c1 = std::min<int64_t>(nc, static_cast<int64_t>(r + 1) * rows_c);
+        std::memcpy(b + d.o_inv, H.inv.data() + c0 * nc, sizeof(double) * static_cast<size_t>((c1 - c0) * nc));
+    }
+    auto *dimg = dalloc<unsigned char>(c, static_cast<int64_t>(img.size()), true);
+    CK(cudaMemcpy(dimg, img.data(), img.size(), cudaMemcpyHostToDevice));
+    d.img = dimg;
     c->tail = dalloc<TailDesc>(c, 1, false);
     CK(cudaMemcpy(c->tail, &d, sizeof(d), cudaMemcpyHostToDevice));
+    CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes));
     c->tail_ctas = ctas;
     c->tail_from = k0;
-    c->tail_smem = off;
+    c->tail_smem = d.smem_bytes;
     if (std::getenv("SB_TAIL_TRACE")) c->trace = dalloc<unsigned long long>(c, 256, false);
 }
 

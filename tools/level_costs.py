@@ -19,7 +19,8 @@ for spec in sys.argv[2:] or ["0:1", "1048576:1"]:
     T, pdl = (spec.split(":") + ["1"])[:2]
     os.environ["SB_TAIL_ROWS"] = T
     os.environ["SB_PDL"] = pdl
-    os.environ["SB_TAIL_TRACE"] = "1"
+    if os.environ.get("LC_TRACE") == "1":
+        os.environ["SB_TAIL_TRACE"] = "1"
     h = sp.Hierarchy(A, cfg)
     ctx = h.ctx()
     tf, ct, smb = C.c_int(), C.c_int(), C.c_int()
