@@ -71,6 +71,8 @@ typedef struct {
     int max_levels;
     int coarse_solver;
     int threads; /* host threads for the Galerkin product (0 = all) */
+    int galerkin_gpu; /* 1: Galerkin products A_c = P^T A P on the GPU (bit-identical; north star (c)) */
+    int gpu_device;   /* CUDA ordinal used when galerkin_gpu = 1 */
 } sb_setup_opts;
 
 /* inc/cycle.hpp:24-32 (CycleParams) */
@@ -120,6 +122,11 @@ const char *sb_version(void);
  * level (inc/coarse_solver.hpp:129-166; > 2000 rows -> SB_EINVAL, the sparse
  * LU path is not provided). Deep-copies A. */
 int sb_setup(const sb_csr *A, const sb_setup_opts *opts, sb_hier *out);
+/* galerkin_product(A, agg) — inc/aggregation.hpp:92-152 — computed on CUDA
+ * device `device`: bit-identical to the reference (one thread per coarse row
+ * replays the reference's accumulation order). Aggregates must have 1 or 2
+ * fine nodes (node-HEM). *out is malloc'ed: free with sb_free_csr. */
+int sb_galerkin_gpu(const sb_csr *A, const int32_t *fine_to_coarse, int64_t n_coarse, int device, sb_csr *out);
 /* Adopt a hierarchy built elsewhere (e.g. by the reference itself): levels[k]
  * and fine_to_coarse[k] (k < nlevels-1) exactly as sparsh::Level holds them
  * (inc/hierarchy.hpp:24-28). The coarse LU is factorized here. */

@@ -281,7 +281,7 @@ Hier *build_hierarchy(HostCsr A0, const sb_setup_opts &o) {
             h->stalled = true;
             break;
         }
-        HostCsr Ac = galerkin(Af, agg, nc, o.threads);
+        HostCsr Ac = o.galerkin_gpu ? galerkin_gpu(Af, agg, nc, o.gpu_device) : galerkin(Af, agg, nc, o.threads);
         h->levels.back().agg = std::move(agg);
         h->levels.back().n_coarse = nc;
         h->levels.push_back(HostLevel{std::move(Ac), {}, -1});
@@ -311,7 +311,7 @@ extern "C" {
 int sb_setup(const sb_csr *A, const sb_setup_opts *opts, sb_hier *out) {
     return guard([&] {
         if (!A || !out) throw invalid_argument("sb_setup: null argument");
-        sb_setup_opts o{0, 500, 10, 0, 0};
+        sb_setup_opts o{0, 500, 10, 0, 0, 0, 0};
         if (opts) o = *opts;
         HostCsr M = csr_from_abi(*A);
         *out = new sb_hier_s{build_hierarchy(std::move(M), o)};
@@ -401,6 +401,18 @@ static void emit(HostCsr &M, sb_csr *out) {
     std::memcpy(v, M.v.data(), sizeof(double) * M.v.size());
     out->col_idx = ci;
     out->values = v;
+}
+
+int sb_galerkin_gpu(const sb_csr *A, const int32_t *f2c, int64_t n_coarse, int device, sb_csr *out) {
+    return guard([&] {
+        if (!A || !f2c || !out) throw invalid_argument("sb_galerkin_gpu: null argument");
+        HostCsr M = csr_from_abi(*A);
+        if (M.n != M.ncols) throw invalid_argument("galerkin_product: matrix must be square");
+        if (n_coarse < 1 || n_coarse > M.n) throw invalid_argument("sb_galerkin_gpu: bad n_coarse");
+        std::vector<int32_t> agg(f2c, f2c + M.n);
+        HostCsr C = galerkin_gpu(M, agg, n_coarse, device);
+        emit(C, out);
+    });
 }
 
 void sb_free_csr(sb_csr *m) {

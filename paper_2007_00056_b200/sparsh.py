@@ -313,7 +313,7 @@ class HierarchyStats:
 # --------------------------------------------------------------------------
 class Hierarchy:
     def __init__(self, A: CsrMatrix, cfg: SolverConfig = None, device: int = 0, *, _coarse_solver=None,
-                 coarse_exact: bool = False):
+                 coarse_exact: bool = False, galerkin_gpu: bool = False):
         cfg = cfg or SolverConfig()
         if not A.is_square():
             raise InvalidArgument("Hierarchy: matrix must be square")
@@ -324,7 +324,8 @@ class Hierarchy:
             raise InvalidArgument("Hierarchy: coarse_solver=cg is not supported on the device path")
         L = _lib.lib()
         opts = _lib.sb_setup_opts(0, cfg.coarse_target, cfg.max_levels,
-                                  0 if _coarse_solver is None else _coarse_solver, 0)
+                                  0 if _coarse_solver is None else _coarse_solver, 0,
+                                  1 if galerkin_gpu else 0, device)
         h = C.c_void_p()
         a = A._abi()
         check(L.sb_setup(C.byref(a), C.byref(opts), C.byref(h)))
@@ -441,6 +442,21 @@ class Hierarchy:
         x = np.empty(n)
         check(_lib.lib().sb_coarse_solve(self.ctx(), dptr(f), dptr(x)))
         return x
+
+
+def galerkin_product_gpu(A: CsrMatrix, agg: "Aggregation", device: int = 0) -> CsrMatrix:
+    """galerkin_product(A, agg) (inc/aggregation.hpp:92-152) computed on the GPU;
+    bit-identical to the reference."""
+    f2c = np.ascontiguousarray(agg.fine_to_coarse, dtype=np.int32)
+    out = _lib.sb_csr()
+    a = A._abi()
+    L = _lib.lib()
+    check(L.sb_galerkin_gpu(C.byref(a), f2c.ctypes.data_as(C.POINTER(C.c_int32)), int(agg.n_coarse), int(device),
+                            C.byref(out)))
+    try:
+        return _from_abi(out)
+    finally:
+        L.sb_free_csr(C.byref(out))
 
 
 def stats(h: Hierarchy) -> HierarchyStats:  # hierarchy.hpp:99-113

@@ -13,7 +13,7 @@ while [ $# -gt 0 ]; do
   d=$ROOT/_variants/$name; mkdir -p $d
   ( nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
       -fmad=false -I$ROOT/include $flags -c -o $d/sb_runtime.o $CS/sb_runtime.cu && \
-    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $d/libsparsh_b200.so $L/sb_host.o $L/sb_dist.o $d/sb_runtime.o -lcudart -lpthread -ldl && \
+    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $d/libsparsh_b200.so $L/sb_host.o $L/sb_dist.o $L/sb_galerkin.o $d/sb_runtime.o -lcudart -lpthread -ldl && \
     rm -f $d/sb_runtime.o && echo "built $name ($flags)" ) &
   pids+=($!)
 done
