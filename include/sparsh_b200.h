@@ -101,8 +101,10 @@ typedef struct {
 typedef struct {
     int device;          /* CUDA ordinal */
     int use_graphs;      /* 1: whole-solve CUDA graph with device-side loop control (default) */
-    int64_t host_levels_from; /* hybrid mode: levels >= this index stay on the host
-                                 (paper's MI scheme); -1 = all levels device-resident */
+    int64_t host_levels_from; /* hybrid mode (paper's MI scheme): the matrix storage of levels
+                                 >= this index stays in pinned host memory and the device
+                                 kernels read it over the host link (zero-copy; no CPU
+                                 compute); -1 = all levels device-resident */
     int coarse_exact;    /* 0: coarsest solve = GEMV with the precomputed inverse (fast);
                             1: the reference's permuted forward/backward substitution in
                                its exact operation order (bit-identical, slow; parity mode) */
@@ -149,6 +151,9 @@ int sb_create(sb_hier h, const sb_device_opts *opts, sb_ctx *out);
 void sb_destroy(sb_ctx ctx);
 /* Device bytes resident for the hierarchy (paper's memory metric). */
 int64_t sb_device_bytes(sb_ctx ctx);
+/* Hybrid mode: bytes of level storage kept in pinned host memory (levels >=
+ * host_levels_from and, when the coarsest level is among them, its inverse). */
+int64_t sb_host_bytes(sb_ctx ctx);
 /* The CUDA stream the context launches on (cudaStream_t as void*). */
 void *sb_stream(sb_ctx ctx);
 

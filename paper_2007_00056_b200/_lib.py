@@ -84,7 +84,7 @@ EXPORTS = [
     "sb_tail_info", "sb_level_format", "sb_partition", "sb_partition_free", "sb_partition_info",
     "sb_partition_level", "sb_partition_exchange", "sb_nccl_unique_id", "sb_dist_create",
     "sb_dist_create_local", "sb_dist_destroy", "sb_dist_rows", "sb_dist_pcg", "sb_dist_pbicgstab",
-    "sb_dist_vcycle", "sb_dist_last_solve_ms", "sb_dist_last_launches", "sb_galerkin_gpu",
+    "sb_dist_vcycle", "sb_dist_last_solve_ms", "sb_dist_last_launches", "sb_galerkin_gpu", "sb_host_bytes",
 ]
 
 _P = C.c_void_p
@@ -102,6 +102,7 @@ _SIGS = {
     "sb_create": (C.c_int, [_P, C.POINTER(sb_device_opts), C.POINTER(_P)]),
     "sb_destroy": (None, [_P]),
     "sb_device_bytes": (C.c_int64, [_P]),
+    "sb_host_bytes": (C.c_int64, [_P]),
     "sb_stream": (_P, [_P]),
     "sb_vcycle": (C.c_int, [_P, C.POINTER(sb_cycle), C.c_int, _D, _D]),
     "sb_vcycle_dev": (C.c_int, [_P, C.POINTER(sb_cycle), C.c_int, _P, _P, C.c_int]),

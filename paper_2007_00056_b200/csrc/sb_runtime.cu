@@ -1380,6 +1380,10 @@ struct sb_ctx_s {
     int nvec_blocks = 1;
     bool graphs = true;
     std::vector<void *> allocs;
+    std::vector<void *> host_allocs;  // hybrid mode: pinned mapped host arrays
+    bool alloc_host = false;
+    int64_t host_bytes = 0;
+    int host_from = 1 << 30;          // first host-resident level (hybrid mode)
     std::map<std::string, sb::GraphEntry> cache;
     double *h_pinned = nullptr;  // staging for host vectors
     int64_t h_pinned_n = 0;
@@ -1399,9 +1403,20 @@ namespace sb {
 
 enum KV { KX = 0, KR, KZ, KP, KAP, KRBAR, KPT, KAPT, KS, KST, KAST, KB };
 
+// Device allocation (zeroed). While c->alloc_host is set (hybrid mode, levels
+// >= host_levels_from) the arrays live in pinned, mapped host memory instead:
+// the same kernels read them over the host link (zero-copy), and they do not
+// count toward the device-resident bytes.
 template <typename T> static T *dalloc(sb_ctx c, int64_t count, bool track = true) {
     void *p = nullptr;
     const size_t bytes = sizeof(T) * static_cast<size_t>(std::max<int64_t>(count, 1));
+    if (c->alloc_host) {
+        CK(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+        std::memset(p, 0, bytes);
+        c->host_allocs.push_back(p);
+        if (track) c->host_bytes += static_cast<int64_t>(bytes);
+        return static_cast<T *>(p);
+    }
     CK(cudaMalloc(&p, bytes));
     CK(cudaMemset(p, 0, bytes));
     c->allocs.push_back(p);
@@ -2034,7 +2049,10 @@ static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
 
 static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarsest, int64_t n0) {
     const HostCsr &A = H.A;
+    // hybrid mode (paper's MI placement): matrix storage of levels >= host_from in host memory
+    c->alloc_host = (&D - c->L.data()) >= c->host_from;
     upload_matrix(c, A, D);
+    c->alloc_host = false;
     if (!coarsest) {
         D.nc = H.n_coarse;
         D.agg = dalloc<int32_t>(c, A.n);
@@ -2494,8 +2512,6 @@ namespace sb {
 // Context creation, split so the multi-rank path (sb_distrun.cuh) can upload
 // partitioned levels in between.
 static sb_ctx ctx_begin(const sb_device_opts &o) {
-    if (o.host_levels_from >= 0)
-        throw invalid_argument("sb_create: hybrid host-level placement is not available in this build");
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (o.device < 0 || o.device >= ndev) throw invalid_argument("sb_create: no such CUDA device");
@@ -2540,7 +2556,9 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
     }
     c->nc = h.nc;
     if (h.nc > 0) {
+        c->alloc_host = c->host_from <= static_cast<int>(c->L.size()) - 1;  // the coarsest level's inverse
         c->inv = dalloc<double>(c, h.nc * h.nc);
+        c->alloc_host = false;
         CK(cudaMemcpy(c->inv, h.inv.data(), sizeof(double) * h.inv.size(), cudaMemcpyHostToDevice));
         c->coarse_exact = o.coarse_exact != 0;
         if (c->coarse_exact) {
@@ -2578,10 +2596,13 @@ int sb_create(sb_hier hh, const sb_device_opts *opts, sb_ctx *out) {
         if (opts) o = *opts;
         c = ctx_begin(o);
         const int64_t n0 = h->levels[0].A.n;
+        const int L = static_cast<int>(h->levels.size());
         c->L.resize(h->levels.size());
-        for (size_t k = 0; k < h->levels.size(); ++k)
-            upload_level(c, h->levels[k], c->L[k], k + 1 == h->levels.size(), n0);
-        ctx_finish(c, *h, o, n0, 0);
+        if (o.host_levels_from >= 0) c->host_from = static_cast<int>(std::min<int64_t>(o.host_levels_from, L));
+        for (int k = 0; k < L; ++k)
+            upload_level(c, h->levels[static_cast<size_t>(k)], c->L[static_cast<size_t>(k)], k + 1 == L, n0);
+        // hybrid mode: no cluster tail (its shared-memory image would copy host levels to the device)
+        ctx_finish(c, *h, o, n0, c->host_from < L ? L : 0);
         *out = c;
     });
     if (rc != SB_OK && c) sb_destroy(c);
@@ -2594,6 +2615,7 @@ void sb_destroy(sb_ctx c) {
     cudaDeviceSynchronize();
     destroy_graphs(c);
     for (void *p : c->allocs) cudaFree(p);
+    for (void *p : c->host_allocs) cudaFreeHost(p);
     if (c->hist_r) cudaFree(c->hist_r);
     if (c->hist_t) cudaFree(c->hist_t);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
@@ -2606,6 +2628,7 @@ void sb_destroy(sb_ctx c) {
 }
 
 int64_t sb_device_bytes(sb_ctx c) { return c ? c->bytes : 0; }
+int64_t sb_host_bytes(sb_ctx c) { return c ? c->host_bytes : 0; }
 void *sb_stream(sb_ctx c) { return c ? static_cast<void *>(c->stream) : nullptr; }
 
 int sb_vcycle_dev(sb_ctx c, const sb_cycle *cp, int level, const double *d_f, double *d_x, int x_is_zero) {

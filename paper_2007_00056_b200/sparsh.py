@@ -313,7 +313,7 @@ class HierarchyStats:
 # --------------------------------------------------------------------------
 class Hierarchy:
     def __init__(self, A: CsrMatrix, cfg: SolverConfig = None, device: int = 0, *, _coarse_solver=None,
-                 coarse_exact: bool = False, galerkin_gpu: bool = False):
+                 coarse_exact: bool = False, galerkin_gpu: bool = False, host_levels_from: int = -1):
         cfg = cfg or SolverConfig()
         if not A.is_square():
             raise InvalidArgument("Hierarchy: matrix must be square")
@@ -333,6 +333,7 @@ class Hierarchy:
         self._ctx = None
         self._device = device
         self._coarse_exact = bool(coarse_exact)
+        self._host_from = int(host_levels_from)  # hybrid mode
         self._levels = None
         self._A0 = A
         self.config = cfg
@@ -388,13 +389,17 @@ class Hierarchy:
     def ctx(self):
         if self._ctx is None:
             c = C.c_void_p()
-            opts = _lib.sb_device_opts(self._device, 1, -1, int(self._coarse_exact))
+            opts = _lib.sb_device_opts(self._device, 1, self._host_from, int(self._coarse_exact))
             check(_lib.lib().sb_create(self._h, C.byref(opts), C.byref(c)))
             self._ctx = c
         return self._ctx
 
     def device_bytes(self) -> int:
         return int(_lib.lib().sb_device_bytes(self.ctx()))
+
+    def host_bytes(self) -> int:
+        """Hybrid mode: level storage held in pinned host memory."""
+        return int(_lib.lib().sb_host_bytes(self.ctx()))
 
     def _n(self, k):
         return self.level(k).A.nrows()
