@@ -10,11 +10,12 @@ PCG solve to tolerance.
            resident in HBM; L2 flushed before every step), max over ranks.
 `e2e`    = the same solve through the public C ABI with host (pinned) b and x:
            H2D of b, solve, D2H of x inside the timed region.
-`roofline` = the L0 Jacobi sweep kernel (dominant: ~80% of solve bytes),
+`roofline` = the L0 Jacobi sweep kernel k_sellg<JACOBI> (the dominant kernel),
            algorithmic bytes / CUDA-event duration vs MEASURED_PEAKS.json.
 `cpu_baseline` = the reference's own CPU code (oracle/_ref) on this host.
-N > 1: replicas (each rank solves its own C2; row partitioning is future work,
-see DESIGN.md §6) — `scaling: weak`.
+N > 1 (torchrun): the row-partitioned solve (sb_dist_*: NCCL halo exchanges and
+dot-product allreduces); default workload = C2 weak-scaled (128 x 128 x 128N
+grid, z-slab row blocks) -> `scaling: weak`; --workload C3/C4 = strong scaling.
 """
 import argparse
 import json
@@ -138,7 +139,11 @@ def bytes_model(h, pre=6, post=6, matrix_bytes=None):
     n0 = lv[0][0]
     spmv = M[0] + 16 * n0
     pcg_it = vc + spmv + 40 * n0 + 16 * n0 + 24 * n0
-    return dict(vcycle=vc, pcg_iter=pcg_it, l0_jacobi=jac(0), l0_spmv=spmv)
+    # BiCGStab (krylov.hpp:156-205 as fused here): 2 V-cycles; 2 SpMVs with their dots
+    # (A pt, (A pt, rbar); A st, (As, As), (As, s)) = 2 M + 48 n; s = r - a Apt (+||s||) 24 n;
+    # x, r update (+2 dots) 64 n; p = r + b (p - w Apt) 32 n
+    bicg_it = 2 * vc + 2 * M[0] + 48 * n0 + 24 * n0 + 64 * n0 + 32 * n0
+    return dict(vcycle=vc, pcg_iter=pcg_it, bicg_iter=bicg_it, l0_jacobi=jac(0), l0_spmv=spmv)
 
 
 def load_traffic():
@@ -452,9 +457,10 @@ def main():
     peak, peak_kind = peaks()
     achieved = bm["l0_jacobi"] / (jac_ms * 1e-3) / 1e9
     vcycle_gbs = bm["vcycle"] / (vc_ms.value * 1e-3) / 1e9
-    solve_gbs = (bm["pcg_iter"] * iters) / value / 1e9
+    it_key = "pcg_iter" if solver == "pcg" else "bicg_iter"
+    solve_gbs = (bm[it_key] * iters) / value / 1e9
     csr_jac_gbs = bm_csr["l0_jacobi"] / (jac_ms * 1e-3) / 1e9
-    csr_solve_gbs = (bm_csr["pcg_iter"] * iters) / value / 1e9
+    csr_solve_gbs = (bm_csr[it_key] * iters) / value / 1e9
 
     # kernels per solve: init + [V-cycle + rz/p] + iters x (SpMV+dot, update) + (iters-1) x
     # (V-cycle, rz, xpay) + true residual
@@ -475,14 +481,15 @@ def main():
                              % (h.device_bytes() / 1e6),
                        "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
                        "setup_s": round(setup_s, 3), "true_rel_residual": true_rel},
-            "roofline": {"bound": "hbm", "kernel": "k_sell_tile<JACOBI> (L0 Jacobi sweep)",
+            "roofline": {"bound": "hbm", "kernel": "k_sellg<JACOBI> (L0 Jacobi sweep)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(),
                          "algorithmic_bytes_per_launch": bm["l0_jacobi"],
                          "bytes_definition": "bytes the shipped lossless format must stream per sweep: "
-                                             "matrix pass (sliced-ELL entries incl. padding: 1 B value index "
-                                             "+ 2 B column delta, + 2 B/row length/diag slot) + 24 B/row "
-                                             "(x, f, x_new); SURVEY §8d CSR-equivalent figures below",
+                                             "matrix pass (grouped sliced-ELL slice blocks incl. padding: 1 B "
+                                             "value index + 2 B column delta per slot, 2 B/row length + "
+                                             "diagonal index, 16 B/slice header) + 24 B/row (x, f, x_new); "
+                                             "SURVEY §8d CSR-equivalent figures below",
                          "launch_ms": jac_ms, "l0_format": fmts[0],
                          "csr_equiv_bytes_per_launch": bm_csr["l0_jacobi"],
                          "csr_equiv_gbs": csr_jac_gbs, "csr_equiv_frac": csr_jac_gbs / peak,
