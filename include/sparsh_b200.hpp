@@ -125,18 +125,30 @@ struct SolveResult {
     ConvergenceReport report;
 };
 
+// B200 placement options (no reference counterpart): device ordinal, hybrid
+// placement of the coarse levels' matrices in host memory (paper's MI scheme),
+// Galerkin products on the GPU (bit-identical to the host / reference).
+struct DeviceOptions {
+    int device = 0;
+    int64_t host_levels_from = -1;  // -1: every level device-resident
+    bool galerkin_gpu = false;
+};
+
 // inc/hierarchy.hpp:49-93: host setup (bit-exact) + device-resident levels.
 class Hierarchy {
 public:
-    Hierarchy(const CsrMatrix &A, const SolverConfig &cfg, int device = 0) : Hierarchy() {
+    Hierarchy(const CsrMatrix &A, const SolverConfig &cfg, int device = 0)
+        : Hierarchy(A, cfg, DeviceOptions{device, -1, false}) {}
+    Hierarchy(const CsrMatrix &A, const SolverConfig &cfg, const DeviceOptions &d) : Hierarchy() {
         if (!A.is_square()) throw std::invalid_argument("Hierarchy: matrix must be square");
         const sb_csr a = A.abi();
         const sb_setup_opts o{cfg.coarsening == CoarseningKind::node_hem ? 0 : 1, cfg.coarse_target,
-                              cfg.max_levels, cfg.coarse_solver == CoarseSolverKind::direct ? 0 : 1, 0};
+                              cfg.max_levels, cfg.coarse_solver == CoarseSolverKind::direct ? 0 : 1, 0,
+                              d.galerkin_gpu ? 1 : 0, d.device};
         sb_hier h = nullptr;
         detail::check(sb_setup(&a, &o, &h));
         hier_.reset(h);
-        init_device(device);
+        init_device(d.device, d.host_levels_from);
     }
     // Adopt levels built elsewhere (e.g. a reference sparsh::Hierarchy):
     // levels[k] plus fine_to_coarse[k] for k < nlevels-1.
@@ -156,7 +168,7 @@ public:
     static Hierarchy plain(const CsrMatrix &A, int device = 0) {
         Hierarchy H;
         const sb_csr a = A.abi();
-        const sb_setup_opts o{0, 1, 1, -1, 0};
+        const sb_setup_opts o{0, 1, 1, -1, 0, 0, 0};
         sb_hier h = nullptr;
         detail::check(sb_setup(&a, &o, &h));
         H.hier_.reset(h);
@@ -167,11 +179,12 @@ public:
     bool coarsening_stalled() const { return sb_hier_stalled(hier_.get()) != 0; }
     sb_ctx ctx() const { return ctx_.get(); }
     int64_t device_bytes() const { return sb_device_bytes(ctx_.get()); }
+    int64_t host_bytes() const { return sb_host_bytes(ctx_.get()); }
 
 private:
     Hierarchy() : hier_(nullptr, &sb_hier_free), ctx_(nullptr, &sb_destroy) {}
-    void init_device(int device) {
-        const sb_device_opts o{device, 1, -1, 0};
+    void init_device(int device, int64_t host_levels_from = -1) {
+        const sb_device_opts o{device, 1, host_levels_from, 0};
         sb_ctx c = nullptr;
         detail::check(sb_create(hier_.get(), &o, &c));
         ctx_.reset(c);

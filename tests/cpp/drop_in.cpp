@@ -41,9 +41,13 @@ int main() {
     } catch (const std::invalid_argument &) {
         threw = true;
     }
+    // B200 placement options: hybrid coarse levels on the host + GPU Galerkin products
+    const sb::Hierarchy hh(A, cfg, sb::DeviceOptions{0, 4, true});
+    const auto rh = sb::pcg(A, b, sb::make_amg_preconditioner(hh, sb::CycleParams::from(cfg)), tol, 200);
+    const bool hybrid_same = rh.report.iterations == res.report.iterations && rh.x == res.x && hh.host_bytes() > 0;
     std::printf("{\"levels\": %zu, \"pcg_iters\": %d, \"pcg_converged\": %d, \"cg_iters\": %d, "
-                "\"amg_iters\": %d, \"true_residual\": %.3e, \"gs_rejected\": %d}\n",
+                "\"amg_iters\": %d, \"true_residual\": %.3e, \"gs_rejected\": %d, \"hybrid_same\": %d}\n",
                 h.nlevels(), res.report.iterations, res.report.converged() ? 1 : 0, plain.report.iterations,
-                amg.report.iterations, res.report.true_residual, threw ? 1 : 0);
+                amg.report.iterations, res.report.true_residual, threw ? 1 : 0, hybrid_same ? 1 : 0);
     return res.report.converged() && threw ? 0 : 1;
 }

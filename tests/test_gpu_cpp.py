@@ -20,7 +20,7 @@ def test_cpp_drop_in(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     d = json.loads(out.stdout.strip().splitlines()[-1])
-    assert d["pcg_converged"] == 1 and d["gs_rejected"] == 1
+    assert d["pcg_converged"] == 1 and d["gs_rejected"] == 1 and d["hybrid_same"] == 1
     assert 5 <= d["pcg_iters"] <= 20 and d["cg_iters"] > d["pcg_iters"]
     assert d["true_residual"] < 1e-6
 
