@@ -1,0 +1,100 @@
+// Row-pattern format ("RPAT"), included by sb_runtime.cu after the SELL-G kernel.
+//
+// A level whose rows repeat a small set of (column - row offsets, values)
+// sequences -- <= 256 distinct rows, which every level of the structured-grid
+// hierarchies has (27 distinct rows at every level of C2/C3/C4, 9 for C1) --
+// is stored as ONE byte per row: the index of its pattern. The pattern table
+// (offsets, values in the row's CSR order, a_ii and RN(1/a_ii)) sits in shared
+// memory. The encoding is lossless (bit-exact values, CSR entry order): the
+// sums are the reference's (inc/csr.hpp:185-191). Levels with more patterns use
+// SELL-G. Per row the sweep streams 1 B of matrix + the vectors, so the pass is
+// bound by x / f / x_new (24 B/row) instead of the matrix.
+//
+// Table layout (bytes, built on the host, copied into shared memory by every
+// CTA before the dependency wait): f64 val[np][W] | f64 diag[np] |
+// f64 rdiag[np] | int32 off[np][W] | uint8 len[np] (padded to 16).
+
+constexpr int kPatThreads = 256;
+// rows per thread per iteration (their gathers in flight together)
+template <int W> struct PatRows { static constexpr int value = W <= 8 ? 2 : 1; };
+
+__host__ __device__ __forceinline__ size_t pat_table_bytes(int np, int w) {
+    return (static_cast<size_t>(np) * w * 12 + static_cast<size_t>(np) * 16 + static_cast<size_t>(np) + 15) & ~size_t(15);
+}
+
+#ifndef SB_PAT_MINB
+#define SB_PAT_MINB 4
+#endif
+template <int MODE, int NV, int W>
+__global__ void __launch_bounds__(kPatThreads, SB_PAT_MINB)
+    k_rowpat(int n, const uint8_t *__restrict__ pid, int np, const unsigned char *__restrict__ table,
+             const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
+             const int *skip, Aux aux, Red red) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double acc[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
+    const int tb = static_cast<int>(pat_table_bytes(np, W));
+    {  // constant table: before the dependency wait (overlaps the predecessor's tail)
+        const uint4 *src = reinterpret_cast<const uint4 *>(table);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem);
+        for (int i = threadIdx.x; i < tb / 16; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    constexpr int kPatRows = PatRows<W>::value;
+    const double *sval = reinterpret_cast<const double *>(smem);
+    const double *sdg = sval + static_cast<size_t>(np) * W;
+    const double *sry = sdg + np;
+    const int32_t *soff = reinterpret_cast<const int32_t *>(sry + np);
+    const uint8_t *slen = reinterpret_cast<const uint8_t *>(soff + static_cast<size_t>(np) * W);
+    pdl_wait();
+    if (!(skip && *skip)) {
+        const int stride = gridDim.x * kPatThreads * kPatRows;
+        for (int base = blockIdx.x * kPatThreads * kPatRows; base < n; base += stride) {
+            if (base + stride >= n) pdl_trigger();
+            int row[kPatRows], p[kPatRows];
+            double a[kPatRows][W], xv[kPatRows][W];
+#pragma unroll
+            for (int q = 0; q < kPatRows; ++q) {
+                row[q] = base + threadIdx.x + q * kPatThreads;
+                p[q] = pid[row[q] < n ? row[q] : n - 1];  // out-of-range threads replay row n-1 (valid gathers)
+            }
+#pragma unroll
+            for (int q = 0; q < kPatRows; ++q) {
+                const int rq = row[q] < n ? row[q] : n - 1;
+                const double *xr = x + rq;
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const int off = soff[p[q] * W + k];
+                    a[q][k] = sval[p[q] * W + k];
+                    if constexpr (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV) xv[q][k] = __ldg(xr + off);
+                    else xv[q][k] = xval<MODE, false>(rq + off, x, f, aux, omega);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kPatRows; ++q) {
+                if (row[q] >= n) continue;
+                const int len = slen[p[q]];
+                double sum = 0.0;
+#pragma unroll
+                for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(a[q][k], xv[q][k]), k < len);
+                double o;
+                if constexpr (MODE == M_SPMV) {
+                    o = sum;
+                } else {
+                    const double fi = f[row[q]];
+                    if constexpr (MODE == M_RESID) {
+                        o = __dsub_rn(fi, sum);
+                    } else {
+                        const double xi = xval<MODE, false>(row[q], x, f, aux, omega);
+                        o = __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), sdg[p[q]], sry[p[q]]));
+                    }
+                }
+                out[row[q]] = o;
+                if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row[q]] : o);
+                if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row[q]] : o);
+            }
+        }
+    }
+    if constexpr (NV > 0) finish_reduction<NV>(red, acc);
+}

@@ -818,6 +818,8 @@ __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
 }
 
+#include "sb_rowpat.cuh"
+
 // ===========================================================================
 // Cluster-resident tail: the deepest levels (each CTA's slice of every tail
 // level fits in its shared memory), down to the coarsest solve and back up, in
@@ -1340,6 +1342,11 @@ struct DevLevel {
     const unsigned char *sell_blk = nullptr;
     int64_t sell_slots = 0;  // stored entry slots (incl. padding)
     double *rdict = nullptr;
+    // row-pattern layout (pat = 1): one pattern index per row + the pattern table
+    int pat = 0, pat_np = 0, pat_w = 0, pat_grid = 0;
+    size_t pat_tb = 0;
+    const uint8_t *pat_id = nullptr;
+    const unsigned char *pat_table = nullptr;
     int2 *mem = nullptr;
     int ntiles = 0, cap = 0, grid = 0;
     size_t smem = 0;
@@ -1513,10 +1520,27 @@ static void launch_sell_f(sb_ctx c, const DevLevel &l, cudaStream_t s, const dou
     }
 }
 
+template <int MODE, int NV, int W>
+static void launch_pat_w(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
+                         double *out, double omega, const int *skip, const Red &red, Aux aux) {
+    launch_k(c, k_rowpat<MODE, NV, W>, dim3(l.pat_grid), dim3(kPatThreads), l.pat_tb, s, static_cast<int>(l.n),
+             l.pat_id, l.pat_np, l.pat_table, x, f, out, omega, skip, aux, red);
+}
+
 template <int MODE, int NV>
 static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
                        double *out, double omega, const int *skip, const Red &red, Aux aux = Aux{}) {
     if (l.n == 0) return;
+    if (l.pat) {
+        switch (l.pat_w) {
+        case 5: return launch_pat_w<MODE, NV, 5>(c, l, s, x, f, out, omega, skip, red, aux);
+        case 7: return launch_pat_w<MODE, NV, 7>(c, l, s, x, f, out, omega, skip, red, aux);
+        case 8: return launch_pat_w<MODE, NV, 8>(c, l, s, x, f, out, omega, skip, red, aux);
+        case 16: return launch_pat_w<MODE, NV, 16>(c, l, s, x, f, out, omega, skip, red, aux);
+        case 28: return launch_pat_w<MODE, NV, 28>(c, l, s, x, f, out, omega, skip, red, aux);
+        default: return launch_pat_w<MODE, NV, 32>(c, l, s, x, f, out, omega, skip, red, aux);
+        }
+    }
     if (l.sell) {
         if (l.vf && l.cf) launch_sell_f<MODE, NV, 1, 1>(c, l, s, x, f, out, omega, skip, red, aux);
         else if (l.vf) launch_sell_f<MODE, NV, 1, 0>(c, l, s, x, f, out, omega, skip, red, aux);
@@ -2045,6 +2069,74 @@ static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
             D.sell_smem = kSgStages * stage;
         }
     }
+    // row-pattern format (SB_RPAT=0 disables): <= 256 distinct rows, W <= 32
+    const char *pe = std::getenv("SB_RPAT");
+    if ((!pe || std::atoi(pe) != 0) && A.n > 0) {
+        std::map<std::vector<uint64_t>, int> ids;
+        std::vector<std::vector<uint64_t>> keys;
+        std::vector<uint8_t> pid(static_cast<size_t>(A.n));
+        int wmax = 0;
+        bool ok = true;
+        std::vector<uint64_t> key;
+        for (int64_t i = 0; i < A.n && ok; ++i) {
+            key.clear();
+            for (int64_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+                uint64_t bits;
+                std::memcpy(&bits, &A.v[e], 8);
+                key.push_back(static_cast<uint64_t>(static_cast<int64_t>(A.ci[e]) - i));
+                key.push_back(bits);
+            }
+            auto it = ids.find(key);
+            if (it == ids.end()) {
+                if (keys.size() == 256) {
+                    ok = false;
+                    break;
+                }
+                it = ids.emplace(key, static_cast<int>(keys.size())).first;
+                keys.push_back(key);
+            }
+            pid[static_cast<size_t>(i)] = static_cast<uint8_t>(it->second);
+            wmax = std::max<int>(wmax, static_cast<int>(A.rp[i + 1] - A.rp[i]));
+        }
+        const int w = wmax <= 5 ? 5 : wmax <= 7 ? 7 : wmax <= 8 ? 8 : wmax <= 16 ? 16 : wmax <= 28 ? 28 : 32;
+        if (ok && wmax <= 32) {
+            const int np = static_cast<int>(keys.size());
+            const size_t tb = pat_table_bytes(np, w);
+            std::vector<unsigned char> tab(tb, 0);
+            auto *val = reinterpret_cast<double *>(tab.data());
+            auto *dg = val + static_cast<size_t>(np) * w;
+            auto *ry = dg + np;
+            auto *off = reinterpret_cast<int32_t *>(ry + np);
+            auto *len = reinterpret_cast<uint8_t *>(off + static_cast<size_t>(np) * w);
+            for (int q = 0; q < np; ++q) {
+                const std::vector<uint64_t> &k = keys[static_cast<size_t>(q)];
+                const int lq = static_cast<int>(k.size() / 2);
+                len[q] = static_cast<uint8_t>(lq);
+                dg[q] = 0.0;
+                for (int e = 0; e < w; ++e) {
+                    off[q * w + e] = 0;  // padding: the row itself, value 0.0 (predicated out)
+                    val[q * w + e] = 0.0;
+                    if (e < lq) {
+                        off[q * w + e] = static_cast<int32_t>(static_cast<int64_t>(k[2 * e]));
+                        std::memcpy(&val[q * w + e], &k[2 * e + 1], 8);
+                        if (off[q * w + e] == 0) dg[q] = val[q * w + e];
+                    }
+                }
+                const double ad = std::fabs(dg[q]);
+                ry[q] = (ad >= std::ldexp(1.0, -100) && ad <= std::ldexp(1.0, 100)) ? 1.0 / dg[q] : 0.0;
+            }
+            auto *dp = dalloc<uint8_t>(c, A.n + 16);
+            CK(cudaMemcpy(dp, pid.data(), pid.size(), cudaMemcpyHostToDevice));
+            auto *dt = dalloc<unsigned char>(c, static_cast<int64_t>(tb));
+            CK(cudaMemcpy(dt, tab.data(), tb, cudaMemcpyHostToDevice));
+            D.pat = 1;
+            D.pat_np = np;
+            D.pat_w = w;
+            D.pat_tb = tb;
+            D.pat_id = dp;
+            D.pat_table = dt;
+        }
+    }
 }
 
 static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarsest, int64_t n0) {
@@ -2090,6 +2182,12 @@ template <int MODE, int NV, int VF, int CF> static void set_sg_attr(int b) {
 template <int MODE, int NV> static void set_smem_attr(size_t smem) {
     if (smem <= 48 * 1024) return;
     const int b = static_cast<int>(smem);
+    CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 28>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     set_sg_attr<MODE, NV, 0, 0>(b);
     set_sg_attr<MODE, NV, 1, 0>(b);
     set_sg_attr<MODE, NV, 0, 1>(b);
@@ -2532,7 +2630,7 @@ static sb_ctx ctx_begin(const sb_device_opts &o) {
 // the cluster tail (only over levels >= tail_min).
 static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t n_vec, int tail_min) {
     size_t max_smem = 0;
-    for (auto &l : c->L) max_smem = std::max(max_smem, std::max(l.smem, l.sell_smem));
+    for (auto &l : c->L) max_smem = std::max({max_smem, l.smem, l.sell_smem, l.pat_tb});
     if (max_smem > 200 * 1024) throw invalid_argument("sb_create: tile staging exceeds shared memory");
     set_smem_attr<M_SPMV, 0>(max_smem);
     set_smem_attr<M_SPMV, 1>(max_smem);
@@ -2552,6 +2650,12 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sellg<M_JACOBI, 0, 1, 1, 4, 0>, kTileRows,
                                                              l.sell_smem));
             l.sell_grid = std::max(1, nsm * std::max(occ, 1));
+        }
+        if (l.pat) {
+            occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowpat<M_JACOBI, 0, 8>, kPatThreads, l.pat_tb));
+            const int64_t need = (l.n + kPatThreads * 2 - 1) / (kPatThreads * 2);
+            l.pat_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
         }
     }
     c->nc = h.nc;
@@ -2679,7 +2783,7 @@ int sb_pbicgstab_dev(sb_ctx c, const sb_cycle *cp, const double *d_b, double *d_
 
 double sb_last_solve_ms(sb_ctx c) { return c ? c->last_solve_ms : 0.0; }
 
-// Streamed storage of level k: fmt[0] = 1 sliced-ELL / 0 CSR, fmt[1] = value
+// Streamed storage of level k: fmt[0] = 2 row patterns / 1 sliced-ELL / 0 CSR, fmt[1] = value
 // dictionary, fmt[2] = int16 column deltas, fmt[3] = slice width (max, padded
 // to the group size);
 // *matrix_bytes = bytes one pass over the matrix streams from HBM (entries
@@ -2688,11 +2792,13 @@ int sb_level_format(sb_ctx c, int k, int *fmt, int64_t *matrix_bytes, int64_t *n
     return guard([&] {
         const DevLevel &l = level_of(c, k);
         const int vb = l.vf ? 1 : 8, cb = l.cf ? 2 : 4;
-        fmt[0] = l.sell;
+        fmt[0] = l.pat ? 2 : l.sell;
         fmt[1] = l.vf;
         fmt[2] = l.cf;
-        fmt[3] = l.sell ? l.sell_ngmax * l.sell_gs : 0;
-        if (l.sell) {
+        fmt[3] = l.pat ? l.pat_w : l.sell ? l.sell_ngmax * l.sell_gs : 0;
+        if (l.pat) {
+            *matrix_bytes = l.n + static_cast<int64_t>(l.pat_tb);  // 1 B/row + the table
+        } else if (l.sell) {
             int64_t bytes = 0;  // every slice block is streamed once per pass
             CK(cudaMemcpy(&bytes, l.soff + l.sell_tiles, sizeof(int64_t), cudaMemcpyDeviceToHost));
             *matrix_bytes = bytes;

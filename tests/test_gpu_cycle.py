@@ -20,15 +20,17 @@ def _cp(sp, pre=6, post=6, omega=2.0 / 3.0):
     lambda sp: sp.convdiff3d(16, 16, 16, 1.0, 100.0, 1.0, 1.0), lambda sp: sp.poisson3d_27(12),
     lambda sp: random_spd(sp, 300, 7, 0.05)])
 @pytest.mark.parametrize("sweeps", [(6, 6), (1, 2), (0, 3), (2, 0), (3, 5)])
-@pytest.mark.parametrize("tail_rows,compress,sell", [("0", "0", "0"), ("0", "1", "0"), ("0", "0", "1"),
-                                                     ("0", "1", "1"), ("2000", "1", "1"), ("1048576", "1", "1")])
-def test_vcycle_matches_oracle(sp, port, mk, sweeps, tail_rows, compress, sell, monkeypatch):
+@pytest.mark.parametrize("tail_rows,compress,sell,rpat", [
+    ("0", "0", "0", "0"), ("0", "1", "0", "0"), ("0", "0", "1", "0"), ("0", "1", "1", "0"), ("0", "1", "1", "1"),
+    ("2000", "1", "1", "1"), ("1048576", "1", "1", "1"), ("1048576", "1", "1", "0")])
+def test_vcycle_matches_oracle(sp, port, mk, sweeps, tail_rows, compress, sell, rpat, monkeypatch):
     # SB_TAIL_ROWS=0: every level as separate kernels; otherwise the small
-    # levels run inside the cluster-resident tail kernel. SB_COMPRESS toggles
-    # the lossless streamed matrix format.
+    # levels run inside the cluster-resident tail kernel. SB_COMPRESS / SB_SELL /
+    # SB_RPAT toggle the lossless streamed matrix formats.
     monkeypatch.setenv("SB_TAIL_ROWS", tail_rows)
     monkeypatch.setenv("SB_COMPRESS", compress)
     monkeypatch.setenv("SB_SELL", sell)
+    monkeypatch.setenv("SB_RPAT", rpat)
     A = mk(sp)
     h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40, coarse_target=min(500, A.nrows() // 4)))
     o = port.hierarchy(A, min(500, A.nrows() // 4), 40)

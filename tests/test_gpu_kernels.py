@@ -24,13 +24,18 @@ def _mats(sp):
             random_spd(sp, 50, 4), sp.CsrMatrix.from_dense(long_row)]
 
 
-@pytest.mark.parametrize("compress,sell", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
-def test_spmv_residual_bitexact(sp, oracle_best, compress, sell, monkeypatch):
+FORMATS = [("0", "0", "0"), ("1", "0", "0"), ("0", "1", "0"), ("1", "1", "0"), ("1", "1", "1")]
+
+
+@pytest.mark.parametrize("compress,sell,rpat", FORMATS)
+def test_spmv_residual_bitexact(sp, oracle_best, compress, sell, rpat, monkeypatch):
     # SB_COMPRESS=1 (default): dictionary values + int16 column deltas where
-    # they fit; SB_SELL=1 (default): sliced-ELL slices. All must give the
-    # reference's bits.
+    # they fit; SB_SELL=1 (default): grouped sliced-ELL slices; SB_RPAT=1
+    # (default): one pattern byte per row where a level has <= 256 distinct
+    # rows. All must give the reference's bits.
     monkeypatch.setenv("SB_COMPRESS", compress)
     monkeypatch.setenv("SB_SELL", sell)
+    monkeypatch.setenv("SB_RPAT", rpat)
     mats = _mats(sp) + [sp.stencil7(200, 200, 2, 6.0, [-1.0] * 6)]  # |delta| 40000: int32 columns
     for A in mats:
         x = np.random.default_rng(1).uniform(-1, 1, A.ncols())
@@ -49,10 +54,11 @@ def test_spmv_long_rows_unstaged_path(sp, oracle_best):
 
 
 @pytest.mark.parametrize("sweeps", [1, 2, 3, 6])
-@pytest.mark.parametrize("compress,sell", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
-def test_jacobi_bitexact(sp, oracle_best, sweeps, compress, sell, monkeypatch):
+@pytest.mark.parametrize("compress,sell,rpat", FORMATS)
+def test_jacobi_bitexact(sp, oracle_best, sweeps, compress, sell, rpat, monkeypatch):
     monkeypatch.setenv("SB_COMPRESS", compress)
     monkeypatch.setenv("SB_SELL", sell)
+    monkeypatch.setenv("SB_RPAT", rpat)
     jac = sp.SmootherKind.weighted_jacobi()
     for A in _mats(sp):
         x = np.random.default_rng(3).uniform(-1, 1, A.nrows())
