@@ -16,17 +16,24 @@
 
 constexpr int kPatThreads = 256;
 // rows per thread per iteration (their gathers in flight together)
-template <int W> struct PatRows { static constexpr int value = W <= 8 ? 2 : 1; };
+#ifndef SB_PAT_ROWS
+#define SB_PAT_ROWS 2
+#endif
+template <int W> struct PatRows { static constexpr int value = W <= 8 ? SB_PAT_ROWS : 1; };
 
 __host__ __device__ __forceinline__ size_t pat_table_bytes(int np, int w) {
     return (static_cast<size_t>(np) * w * 12 + static_cast<size_t>(np) * 16 + static_cast<size_t>(np) + 15) & ~size_t(15);
 }
 
+#ifndef SB_PAT_MINB_WIDE
+#define SB_PAT_MINB_WIDE 2
+#endif
 #ifndef SB_PAT_MINB
 #define SB_PAT_MINB 4
 #endif
+// wide rows (27-point levels) keep all W gathers in flight: more registers, 3 CTAs/SM
 template <int MODE, int NV, int W>
-__global__ void __launch_bounds__(kPatThreads, SB_PAT_MINB)
+__global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MINB_WIDE)
     k_rowpat(int n, const uint8_t *__restrict__ pid, int np, const unsigned char *__restrict__ table,
              const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
              const int *skip, Aux aux, Red red) {
@@ -50,14 +57,24 @@ __global__ void __launch_bounds__(kPatThreads, SB_PAT_MINB)
     pdl_wait();
     if (!(skip && *skip)) {
         const int stride = gridDim.x * kPatThreads * kPatRows;
+        // the pattern bytes of the next iteration are loaded one iteration ahead,
+        // so the x gathers do not wait behind a dependent DRAM load
+        int pn[kPatRows];
+#pragma unroll
+        for (int q = 0; q < kPatRows; ++q) {
+            const int r = blockIdx.x * kPatThreads * kPatRows + threadIdx.x + q * kPatThreads;
+            pn[q] = pid[r < n ? r : n - 1];  // out-of-range threads replay row n-1 (valid gathers)
+        }
         for (int base = blockIdx.x * kPatThreads * kPatRows; base < n; base += stride) {
             if (base + stride >= n) pdl_trigger();
             int row[kPatRows], p[kPatRows];
-            double a[kPatRows][W], xv[kPatRows][W];
+            double xv[kPatRows][W];
 #pragma unroll
             for (int q = 0; q < kPatRows; ++q) {
                 row[q] = base + threadIdx.x + q * kPatThreads;
-                p[q] = pid[row[q] < n ? row[q] : n - 1];  // out-of-range threads replay row n-1 (valid gathers)
+                p[q] = pn[q];
+                const int r = row[q] + stride;
+                pn[q] = pid[r < n ? r : n - 1];
             }
 #pragma unroll
             for (int q = 0; q < kPatRows; ++q) {
@@ -66,7 +83,6 @@ __global__ void __launch_bounds__(kPatThreads, SB_PAT_MINB)
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
                     const int off = soff[p[q] * W + k];
-                    a[q][k] = sval[p[q] * W + k];
                     if constexpr (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV) xv[q][k] = __ldg(xr + off);
                     else xv[q][k] = xval<MODE, false>(rq + off, x, f, aux, omega);
                 }
@@ -77,7 +93,7 @@ __global__ void __launch_bounds__(kPatThreads, SB_PAT_MINB)
                 const int len = slen[p[q]];
                 double sum = 0.0;
 #pragma unroll
-                for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(a[q][k], xv[q][k]), k < len);
+                for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(sval[p[q] * W + k], xv[q][k]), k < len);
                 double o;
                 if constexpr (MODE == M_SPMV) {
                     o = sum;
