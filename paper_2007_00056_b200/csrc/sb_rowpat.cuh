@@ -91,9 +91,18 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
             for (int q = 0; q < kPatRows; ++q) {
                 if (row[q] >= n) continue;
                 const int len = slen[p[q]];
+                // Padding slots hold value +0.0 at offset 0 (the row itself): 0 * x_i
+                // is +-0 and sum + (+-0) == sum bit for bit (sum is never -0), so
+                // the unmasked sum equals the reference's unless x_i is inf / NaN
+                // (0 * inf = NaN); only then replay the row with masked slots.
                 double sum = 0.0;
 #pragma unroll
-                for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(sval[p[q] * W + k], xv[q][k]), k < len);
+                for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(sval[p[q] * W + k], xv[q][k]));
+                if (len < W && !isfinite(xv[q][W - 1])) {
+                    sum = 0.0;
+#pragma unroll
+                    for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(sval[p[q] * W + k], xv[q][k]), k < len);
+                }
                 double o;
                 if constexpr (MODE == M_SPMV) {
                     o = sum;

@@ -124,3 +124,19 @@ def test_golden_kernels(sp, path):
     A = from_npz(sp, d)
     assert np.array_equal(sp.spmv(A, d["f"]), d["spmv_f"])
     assert np.array_equal(sp.smooth(sp.SmootherKind.weighted_jacobi(), A, d["f"], d["b"], 3), d["jacobi3"])
+
+
+@pytest.mark.parametrize("rpat", ["0", "1"])
+def test_spmv_nonfinite_inputs(sp, oracle_best, rpat, monkeypatch):
+    # padded slots (boundary rows) must not turn an inf of the row's own x into
+    # NaN: the pattern kernel replays such rows with masked slots
+    monkeypatch.setenv("SB_RPAT", rpat)
+    for A in [sp.poisson2d(24, 20), sp.poisson3d(12), sp.poisson3d_27(7)]:
+        x = np.random.default_rng(8).uniform(-1, 1, A.ncols())
+        x[[0, 5, A.ncols() - 1]] = [np.inf, -np.inf, np.inf]
+        x[17] = np.nan
+        f = np.random.default_rng(9).uniform(-1, 1, A.nrows())
+        got, want = sp.spmv(A, x), oracle_best.spmv(A, x)
+        assert np.array_equal(got, want, equal_nan=True)
+        assert np.array_equal(np.signbit(got), np.signbit(want))
+        assert np.array_equal(sp.residual(A, x, f), oracle_best.residual(A, x, f), equal_nan=True)
