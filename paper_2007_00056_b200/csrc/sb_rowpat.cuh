@@ -54,17 +54,18 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
     const double *sry = sdg + np;
     const int32_t *soff = reinterpret_cast<const int32_t *>(sry + np);
     const uint8_t *slen = reinterpret_cast<const uint8_t *>(soff + static_cast<size_t>(np) * W);
+    const int stride = gridDim.x * kPatThreads * kPatRows;
+    // the pattern bytes of the next iteration are loaded one iteration ahead,
+    // so the x gathers do not wait behind a dependent DRAM load; the first
+    // ones (constant data) before the dependency wait
+    int pn[kPatRows];
+#pragma unroll
+    for (int q = 0; q < kPatRows; ++q) {
+        const int r = blockIdx.x * kPatThreads * kPatRows + threadIdx.x + q * kPatThreads;
+        pn[q] = pid[r < n ? r : n - 1];  // out-of-range threads replay row n-1 (valid gathers)
+    }
     pdl_wait();
     if (!(skip && *skip)) {
-        const int stride = gridDim.x * kPatThreads * kPatRows;
-        // the pattern bytes of the next iteration are loaded one iteration ahead,
-        // so the x gathers do not wait behind a dependent DRAM load
-        int pn[kPatRows];
-#pragma unroll
-        for (int q = 0; q < kPatRows; ++q) {
-            const int r = blockIdx.x * kPatThreads * kPatRows + threadIdx.x + q * kPatThreads;
-            pn[q] = pid[r < n ? r : n - 1];  // out-of-range threads replay row n-1 (valid gathers)
-        }
         for (int base = blockIdx.x * kPatThreads * kPatRows; base < n; base += stride) {
             if (base + stride >= n) pdl_trigger();
             int row[kPatRows], p[kPatRows];
@@ -122,4 +123,74 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
         }
     }
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
+}
+
+// Residual + restriction fused for a row-pattern level (one launch and no r
+// vector): thread c evaluates r_m = f_m - A_m x for the members m0 < m1 of
+// coarse row c in the reference's order and writes f_c = (0 + r_m0) + r_m1
+// (csr.hpp:267-274 then the unit-P spmv_transpose, csr.hpp:232-239); with
+// xc0, also the coarse level's first sweep from 0, x0_c = 0 + (w f_c) / a_cc.
+template <int W>
+__device__ __forceinline__ double pat_resid_row(int m, int p, const double *sval, const int32_t *soff,
+                                                const uint8_t *slen, const double *__restrict__ x,
+                                                const double *__restrict__ f) {
+    double xv[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) xv[k] = __ldg(x + m + soff[p * W + k]);
+    const double fm = f[m];
+    double sum = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(sval[p * W + k], xv[k]));
+    const int len = slen[p];
+    if (len < W && !isfinite(xv[W - 1])) {  // see k_rowpat: exact replay for a non-finite own x
+        sum = 0.0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(sval[p * W + k], xv[k]), k < len);
+    }
+    return __dsub_rn(fm, sum);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MINB_WIDE)
+    k_pat_resid_restrict(int nc, const int2 *__restrict__ mem, const uint8_t *__restrict__ pid, int np,
+                         const unsigned char *__restrict__ table, const double *__restrict__ x,
+                         const double *__restrict__ f, double *__restrict__ fc, const double *__restrict__ dc,
+                         double *__restrict__ xc0, double omega) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tb = static_cast<int>(pat_table_bytes(np, W));
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(table);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem);
+        for (int i = threadIdx.x; i < tb / 16; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const double *sval = reinterpret_cast<const double *>(smem);
+    const double *sdg = sval + static_cast<size_t>(np) * W;
+    const double *sry = sdg + np;
+    const int32_t *soff = reinterpret_cast<const int32_t *>(sry + np);
+    const uint8_t *slen = reinterpret_cast<const uint8_t *>(soff + static_cast<size_t>(np) * W);
+    (void)sdg;
+    const int c0 = blockIdx.x * blockDim.x + threadIdx.x;
+    int2 mm = make_int2(0, -1);
+    int p0 = 0, p1 = 0;
+    double d = 0.0;
+    if (c0 < nc) {  // constant data before the dependency wait
+        mm = mem[c0];
+        p0 = pid[mm.x];
+        if (mm.y >= 0) p1 = pid[mm.y];
+        if (xc0) d = dc[c0];
+    }
+    pdl_wait();
+    for (int c = c0; c < nc; c += gridDim.x * blockDim.x) {
+        if (c != c0) {
+            mm = mem[c];
+            p0 = pid[mm.x];
+            if (mm.y >= 0) p1 = pid[mm.y];
+            if (xc0) d = dc[c];
+        }
+        double s = __dadd_rn(0.0, pat_resid_row<W>(mm.x, p0, sval, soff, slen, x, f));
+        if (mm.y >= 0) s = __dadd_rn(s, pat_resid_row<W>(mm.y, p1, sval, soff, slen, x, f));
+        fc[c] = s;
+        if (xc0) xc0[c] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), d));
+    }
 }

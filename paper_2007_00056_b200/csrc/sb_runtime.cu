@@ -1554,6 +1554,28 @@ static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double
     else launch_csr_f<MODE, NV, 0, 0>(c, l, s, x, f, out, omega, skip, red, aux);
 }
 
+template <int W>
+static void launch_pat_rr_w(sb_ctx c, const DevLevel &l, const DevLevel &lc, cudaStream_t s, const double *x,
+                            const double *f, double *x0, double omega) {
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((lc.n + kPatThreads - 1) / kPatThreads,
+                                                                             static_cast<int64_t>(l.pat_grid) * 2)));
+    launch_k(c, k_pat_resid_restrict<W>, dim3(grid), dim3(kPatThreads), l.pat_tb, s, static_cast<int>(lc.n),
+             static_cast<const int2 *>(l.mem), l.pat_id, l.pat_np, l.pat_table, x, f, lc.f,
+             static_cast<const double *>(lc.diag), x0, omega);
+}
+
+static void launch_pat_rr(sb_ctx c, const DevLevel &l, const DevLevel &lc, cudaStream_t s, const double *x,
+                          const double *f, double *x0, double omega) {
+    switch (l.pat_w) {
+    case 5: return launch_pat_rr_w<5>(c, l, lc, s, x, f, x0, omega);
+    case 7: return launch_pat_rr_w<7>(c, l, lc, s, x, f, x0, omega);
+    case 8: return launch_pat_rr_w<8>(c, l, lc, s, x, f, x0, omega);
+    case 16: return launch_pat_rr_w<16>(c, l, lc, s, x, f, x0, omega);
+    case 28: return launch_pat_rr_w<28>(c, l, lc, s, x, f, x0, omega);
+    default: return launch_pat_rr_w<32>(c, l, lc, s, x, f, x0, omega);
+    }
+}
+
 static void launch_jacobi(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *xin, const double *f,
                           double *xout, double omega) {
     launch_csr<M_JACOBI, 0>(c, l, s, xin, f, xout, omega, nullptr, Red{});
@@ -1642,14 +1664,18 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
         }
     }
     const DevLevel &lc = c->L[static_cast<size_t>(k) + 1];
-    launch_csr<M_RESID, 0>(c, l, s, cur, f, c->rs, 0.0, nullptr, Red{});
     // the child's zero-guess sweep rides on the restriction (not for the
     // coarsest level or the cluster tail, which start from x = 0 themselves)
     const bool child_x0 = cp.pre >= 1 && k + 2 < L && k + 1 != c->tail_from;
     double *x0 = child_x0 ? zero_sweep_dest(c, cp, k + 1, lc.x) : nullptr;
-    launch_k(c, k_restrict, dim3(vec_grid(lc.n)), dim3(kVecThreads), 0, s, lc.n,
-             static_cast<const int2 *>(l.mem), static_cast<const double *>(c->rs), lc.f,
-             static_cast<const double *>(lc.diag), x0, cp.omega);
+    if (l.pat) {  // residual + restriction in one launch, no r vector
+        launch_pat_rr(c, l, lc, s, cur, f, x0, cp.omega);
+    } else {
+        launch_csr<M_RESID, 0>(c, l, s, cur, f, c->rs, 0.0, nullptr, Red{});
+        launch_k(c, k_restrict, dim3(vec_grid(lc.n)), dim3(kVecThreads), 0, s, lc.n,
+                 static_cast<const int2 *>(l.mem), static_cast<const double *>(c->rs), lc.f,
+                 static_cast<const double *>(lc.diag), x0, cp.omega);
+    }
     emit_vcycle(c, s, cp, k + 1, lc.f, lc.x, true, child_x0);
     if (cp.post >= 1 && cur != post_first) {
         // x' = cur + P x_c folded into the first post-sweep's gathers
@@ -2187,6 +2213,14 @@ template <int MODE, int NV> static void set_smem_attr(size_t smem) {
     CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 28>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    if constexpr (MODE == M_RESID && NV == 0) {
+        CK(cudaFuncSetAttribute(k_pat_resid_restrict<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_pat_resid_restrict<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_pat_resid_restrict<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_pat_resid_restrict<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_pat_resid_restrict<28>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_pat_resid_restrict<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    }
     CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     set_sg_attr<MODE, NV, 0, 0>(b);
     set_sg_attr<MODE, NV, 1, 0>(b);
