@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
                 const int r = row[q] + stride;
                 pn[q] = pid[r < n ? r : n - 1];
             }
+            double fv[kPatRows], xo[kPatRows];  // rhs and own iterate, loaded with the gathers
 #pragma unroll
             for (int q = 0; q < kPatRows; ++q) {
                 const int rq = row[q] < n ? row[q] : n - 1;
@@ -87,6 +88,8 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
                     if constexpr (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV) xv[q][k] = __ldg(xr + off);
                     else xv[q][k] = xval<MODE, false>(rq + off, x, f, aux, omega);
                 }
+                fv[q] = (MODE == M_SPMV) ? 0.0 : __ldg(f + rq);
+                xo[q] = (MODE >= M_JACOBI) ? xval<MODE, false>(rq, x, f, aux, omega) : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < kPatRows; ++q) {
@@ -107,14 +110,10 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
                 double o;
                 if constexpr (MODE == M_SPMV) {
                     o = sum;
+                } else if constexpr (MODE == M_RESID) {
+                    o = __dsub_rn(fv[q], sum);
                 } else {
-                    const double fi = f[row[q]];
-                    if constexpr (MODE == M_RESID) {
-                        o = __dsub_rn(fi, sum);
-                    } else {
-                        const double xi = xval<MODE, false>(row[q], x, f, aux, omega);
-                        o = __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), sdg[p[q]], sry[p[q]]));
-                    }
+                    o = __dadd_rn(xo[q], div_rn(__dmul_rn(omega, __dsub_rn(fv[q], sum)), sdg[p[q]], sry[p[q]]));
                 }
                 out[row[q]] = o;
                 if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row[q]] : o);
