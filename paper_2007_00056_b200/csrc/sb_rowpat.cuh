@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
                     o = __dadd_rn(xo[q], div_rn(__dmul_rn(omega, __dsub_rn(fv[q], sum)), sdg[p[q]], sry[p[q]]));
                 }
                 out[row[q]] = o;
-                if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row[q]] : o);
+                if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fv[q] : red.w0[row[q]]) : o);
                 if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row[q]] : o);
             }
         }

@@ -1404,6 +1404,10 @@ struct sb_ctx_s {
     bool pdl = true;                      // programmatic dependent launch in the V-cycle (SB_PDL=0 off)
     sb::TailDesc *tail = nullptr;
     int launch_count = 0;  // kernels emitted by the last emit_* sequence
+    // PCG: the V-cycle's last level-0 post-sweep also reduces (z, f) = (z, r)
+    // into this reduction (no separate dot kernel); cleared once emitted
+    const sb::Red *final_red = nullptr;
+    bool final_red_used = false;
 };
 
 namespace sb {
@@ -1684,7 +1688,12 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
         cur = post_first;
         other = (cur == X) ? T : X;
         for (int i = 1; i < cp.post; ++i) {
-            launch_jacobi(c, l, s, cur, f, other, cp.omega);
+            if (k == 0 && i + 1 == cp.post && c->final_red) {  // last kernel of the cycle: + (z, r)
+                launch_csr<M_JACOBI, 1>(c, l, s, cur, f, other, cp.omega, nullptr, *c->final_red);
+                c->final_red_used = true;
+            } else {
+                launch_jacobi(c, l, s, cur, f, other, cp.omega);
+            }
             std::swap(cur, other);
         }
     } else {
@@ -1781,9 +1790,15 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
                 n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})));
             CK(cudaGetLastError());
             add_cond(c, s2, d2, h_vc, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
+                const Red rz = make_red(c, EP_PCG_RZ, 1, r);
+                c->final_red = &rz;  // (r, z) rides on the V-cycle's last sweep when it is a Jacobi sweep
+                c->final_red_used = false;
                 precond(s3, r, z);
-                k_dot<<<vb, kVecThreads, 0, s3>>>(n, r, z, nullptr, make_red(c, EP_PCG_RZ, 1));
-                CK(cudaGetLastError());
+                c->final_red = nullptr;
+                if (!c->final_red_used) {
+                    k_dot<<<vb, kVecThreads, 0, s3>>>(n, r, z, nullptr, rz);
+                    CK(cudaGetLastError());
+                }
                 k_xpay<<<vb, kVecThreads, 0, s3>>>(n, z, p, c->st);
                 CK(cudaGetLastError());
             });
@@ -2672,6 +2687,7 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
     set_smem_attr<M_RESID, 0>(max_smem);
     set_smem_attr<M_RESID, 1>(max_smem);
     set_smem_attr<M_JACOBI, 0>(max_smem);
+    set_smem_attr<M_JACOBI, 1>(max_smem);
     set_smem_attr<M_JACOBI_PROLONG, 0>(max_smem);
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
