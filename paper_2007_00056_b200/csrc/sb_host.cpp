@@ -435,6 +435,42 @@ static inline double stored(double v) {
     return s;
 }
 
+} // extern "C"
+namespace sb {
+// 3D 27-point operator (diag, `off` to every neighbour), Dirichlet, rows in
+// (iz*ny + iy)*nx + ix order, columns ascending: built straight into the
+// host CSR (int64 offsets; nnz may exceed int32: C5 512^3 has 3.6e9).
+HostCsr stencil27(int64_t nx, int64_t ny, int64_t nz, double diag, double off) {
+    if (nx < 1 || ny < 1 || nz < 1) throw invalid_argument("stencil27: grid dims must be >= 1");
+    if (nx * ny * nz > INT32_MAX) throw invalid_argument("stencil27: grid too large for int32 columns");
+    HostCsr M;
+    M.n = M.ncols = nx * ny * nz;
+    M.rp.assign(static_cast<size_t>(M.n) + 1, 0);
+    const int64_t nnz = (3 * nx - 2) * (3 * ny - 2) * (3 * nz - 2);
+    M.ci.reserve(static_cast<size_t>(nnz));
+    M.v.reserve(static_cast<size_t>(nnz));
+    const double sd = stored(diag), so = stored(off);
+    for (int64_t iz = 0; iz < nz; ++iz)
+        for (int64_t iy = 0; iy < ny; ++iy)
+            for (int64_t ix = 0; ix < nx; ++ix) {
+                const int64_t m = (iz * ny + iy) * nx + ix;
+                for (int dz = -1; dz <= 1; ++dz)
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            const int64_t jx = ix + dx, jy = iy + dy, jz = iz + dz;
+                            if (jx < 0 || jy < 0 || jz < 0 || jx >= nx || jy >= ny || jz >= nz) continue;
+                            const int64_t col = (jz * ny + jy) * nx + jx;
+                            M.ci.push_back(static_cast<int32_t>(col));
+                            M.v.push_back(col == m ? sd : so);
+                        }
+                M.rp[static_cast<size_t>(m) + 1] = static_cast<int64_t>(M.ci.size());
+            }
+    M.sync_rp32();
+    return M;
+}
+} // namespace sb
+extern "C" {
+
 // inc/problems.hpp:28-57, same expressions in the same order; rows come out
 // sorted (south, west, diag, east, north) as from_triplets would sort them.
 int sb_gen_convdiff2d(int64_t nx, int64_t ny, double bx, double by, double c, sb_csr *out) {
@@ -527,30 +563,18 @@ int sb_gen_convdiff3d(int64_t nx, int64_t ny, int64_t nz, double bx, double by, 
 
 int sb_gen_stencil27(int64_t nx, int64_t ny, int64_t nz, double diag, double off, sb_csr *out) {
     return guard([&] {
-        if (nx < 1 || ny < 1 || nz < 1) throw invalid_argument("stencil27: grid dims must be >= 1");
-        if (nx * ny * nz > INT32_MAX) throw invalid_argument("stencil27: grid too large for int32 columns");
-        HostCsr M;
-        M.n = M.ncols = nx * ny * nz;
-        M.rp.assign(static_cast<size_t>(M.n) + 1, 0);
-        M.ci.reserve(static_cast<size_t>(27 * M.n));
-        M.v.reserve(static_cast<size_t>(27 * M.n));
-        for (int64_t iz = 0; iz < nz; ++iz)
-            for (int64_t iy = 0; iy < ny; ++iy)
-                for (int64_t ix = 0; ix < nx; ++ix) {
-                    const int64_t m = (iz * ny + iy) * nx + ix;
-                    for (int dz = -1; dz <= 1; ++dz)
-                        for (int dy = -1; dy <= 1; ++dy)
-                            for (int dx = -1; dx <= 1; ++dx) {
-                                const int64_t jx = ix + dx, jy = iy + dy, jz = iz + dz;
-                                if (jx < 0 || jy < 0 || jz < 0 || jx >= nx || jy >= ny || jz >= nz)
-                                    continue;
-                                const int64_t col = (jz * ny + jy) * nx + jx;
-                                M.ci.push_back(static_cast<int32_t>(col));
-                                M.v.push_back(stored(col == m ? diag : off));
-                            }
-                    M.rp[m + 1] = static_cast<int64_t>(M.ci.size());
-                }
+        HostCsr M = sb::stencil27(nx, ny, nz, diag, off);
         emit(M, out);
+    });
+}
+
+int sb_setup_stencil27(int64_t nx, int64_t ny, int64_t nz, double diag, double off, const sb_setup_opts *opts,
+                       sb_hier *out) {
+    return guard([&] {
+        if (!out) throw invalid_argument("sb_setup_stencil27: null argument");
+        sb_setup_opts o{0, 500, 10, 0, 0, 0, 0};
+        if (opts) o = *opts;
+        *out = new sb_hier_s{build_hierarchy(sb::stencil27(nx, ny, nz, diag, off), o)};
     });
 }
 

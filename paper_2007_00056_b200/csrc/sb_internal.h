@@ -62,6 +62,7 @@ std::vector<int32_t> node_hem(const HostCsr &A, int64_t *n_coarse);
 HostCsr galerkin(const HostCsr &A, const std::vector<int32_t> &agg, int64_t nc, int threads);
 // the same product computed on CUDA device `device` (sb_galerkin.cu), bit-identical
 HostCsr galerkin_gpu(const HostCsr &A, const std::vector<int32_t> &agg, int64_t nc, int device);
+HostCsr stencil27(int64_t nx, int64_t ny, int64_t nz, double diag, double off);
 void factor_coarse(Hier &h);
 Hier *build_hierarchy(HostCsr A0, const sb_setup_opts &o);
 Hier *hier_of(sb_hier h);

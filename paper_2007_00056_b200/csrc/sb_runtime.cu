@@ -24,6 +24,8 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <unordered_map>
+#include <thread>
 #include <type_traits>
 
 #include <cuda_runtime.h>
@@ -1898,22 +1900,143 @@ static void make_tiles(const HostCsr &A, std::vector<int32_t> &tiles, int &cap) 
     }
 }
 
-// Matrix part of a level: raw CSR, diagonal, tiles, lossless streamed format
-// (dictionary values / int16 column deltas), sliced-ELL slices. Columns need
-// not be sorted (partitioned levels number ghosts after own rows).
+// Row-pattern format (§3.1): one byte per row when the level has <= 256
+// distinct rows (offsets + value bits, CSR order) of length <= 32. Threads
+// hash their rows, first occurrences become patterns, and every row is
+// verified against its pattern's full key (a hash collision only disables the
+// format). Returns false (nothing allocated) when the level does not qualify.
+static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
+    const char *pe = std::getenv("SB_RPAT");
+    if ((pe && std::atoi(pe) == 0) || A.n == 0) return false;
+    const int64_t n = A.n;
+    auto row_hash = [&](int64_t i) {
+        uint64_t h = 1469598103934665603ull ^ static_cast<uint64_t>(A.rp[i + 1] - A.rp[i]);
+        for (int64_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
+            uint64_t bits;
+            std::memcpy(&bits, &A.v[e], 8);
+            const uint64_t o = static_cast<uint64_t>(static_cast<int64_t>(A.ci[e]) - i);
+            h = (h ^ o) * 1099511628211ull;
+            h = (h ^ bits) * 1099511628211ull;
+            h ^= h >> 29;
+        }
+        return h;
+    };
+    auto same_row = [&](int64_t a, int64_t b) {  // rows a and b have identical (offset, value) sequences
+        const int64_t la = A.rp[a + 1] - A.rp[a];
+        if (la != A.rp[b + 1] - A.rp[b]) return false;
+        for (int64_t e = 0; e < la; ++e) {
+            if (static_cast<int64_t>(A.ci[A.rp[a] + e]) - a != static_cast<int64_t>(A.ci[A.rp[b] + e]) - b) return false;
+            if (std::memcmp(&A.v[A.rp[a] + e], &A.v[A.rp[b] + e], 8) != 0) return false;
+        }
+        return true;
+    };
+    // pass 1 (threads): per-row hash + each chunk's distinct hashes (first row of each)
+    const int T = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), n / 65536 + 1)));
+    std::vector<uint64_t> hs(static_cast<size_t>(n));
+    std::vector<std::vector<std::pair<uint64_t, int64_t>>> firsts(static_cast<size_t>(T));
+    std::vector<int> too_many(static_cast<size_t>(T), 0), wide(static_cast<size_t>(T), 0);
+    const int64_t per = (n + T - 1) / T;
+    auto pass1 = [&](int t) {
+        std::unordered_map<uint64_t, int64_t> seen;
+        for (int64_t i = t * per; i < std::min<int64_t>(n, (t + 1) * per); ++i) {
+            if (A.rp[i + 1] - A.rp[i] > 32) {
+                wide[static_cast<size_t>(t)] = 1;
+                return;
+            }
+            const uint64_t h = row_hash(i);
+            hs[static_cast<size_t>(i)] = h;
+            if (seen.emplace(h, i).second) {
+                firsts[static_cast<size_t>(t)].push_back({h, i});
+                if (seen.size() > 256) {
+                    too_many[static_cast<size_t>(t)] = 1;
+                    return;
+                }
+            }
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t) th.emplace_back(pass1, t);
+        for (auto &x : th) x.join();
+    }
+    for (int t = 0; t < T; ++t)
+        if (too_many[static_cast<size_t>(t)] || wide[static_cast<size_t>(t)]) return false;
+    std::unordered_map<uint64_t, int> ids;
+    std::vector<int64_t> rep;  // representative row of each pattern
+    for (int t = 0; t < T; ++t)
+        for (auto &f : firsts[static_cast<size_t>(t)])
+            if (ids.emplace(f.first, static_cast<int>(rep.size())).second) {
+                rep.push_back(f.second);
+                if (rep.size() > 256) return false;
+            }
+    // pass 2 (threads): pattern index per row, verified against the representative
+    std::vector<uint8_t> pid(static_cast<size_t>(n));
+    std::vector<int> bad(static_cast<size_t>(T), 0);
+    auto pass2 = [&](int t) {
+        for (int64_t i = t * per; i < std::min<int64_t>(n, (t + 1) * per); ++i) {
+            const int q = ids.at(hs[static_cast<size_t>(i)]);
+            if (!same_row(i, rep[static_cast<size_t>(q)])) {
+                bad[static_cast<size_t>(t)] = 1;
+                return;
+            }
+            pid[static_cast<size_t>(i)] = static_cast<uint8_t>(q);
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t) th.emplace_back(pass2, t);
+        for (auto &x : th) x.join();
+    }
+    for (int t = 0; t < T; ++t)
+        if (bad[static_cast<size_t>(t)]) return false;  // hash collision: use another format
+    std::vector<uint64_t>().swap(hs);
+    int wmax = 0;
+    for (int64_t r : rep) wmax = std::max<int>(wmax, static_cast<int>(A.rp[r + 1] - A.rp[r]));
+    const int w = wmax <= 5 ? 5 : wmax <= 7 ? 7 : wmax <= 8 ? 8 : wmax <= 16 ? 16 : wmax <= 28 ? 28 : 32;
+    const int np = static_cast<int>(rep.size());
+    const size_t tb = pat_table_bytes(np, w);
+    std::vector<unsigned char> tab(tb, 0);
+    auto *val = reinterpret_cast<double *>(tab.data());
+    auto *dg = val + static_cast<size_t>(np) * w;
+    auto *ry = dg + np;
+    auto *off = reinterpret_cast<int32_t *>(ry + np);
+    auto *len = reinterpret_cast<uint8_t *>(off + static_cast<size_t>(np) * w);
+    for (int q = 0; q < np; ++q) {
+        const int64_t r = rep[static_cast<size_t>(q)];
+        const int lq = static_cast<int>(A.rp[r + 1] - A.rp[r]);
+        len[q] = static_cast<uint8_t>(lq);
+        dg[q] = 0.0;
+        for (int e = 0; e < w; ++e) {
+            off[q * w + e] = 0;  // padding: the row itself, value +0.0 (see k_rowpat)
+            val[q * w + e] = 0.0;
+            if (e < lq) {
+                off[q * w + e] = static_cast<int32_t>(static_cast<int64_t>(A.ci[A.rp[r] + e]) - r);
+                val[q * w + e] = A.v[A.rp[r] + e];
+                if (off[q * w + e] == 0) dg[q] = val[q * w + e];
+            }
+        }
+        const double ad = std::fabs(dg[q]);
+        ry[q] = (ad >= std::ldexp(1.0, -100) && ad <= std::ldexp(1.0, 100)) ? 1.0 / dg[q] : 0.0;
+    }
+    auto *dp = dalloc<uint8_t>(c, A.n + 16);
+    CK(cudaMemcpy(dp, pid.data(), pid.size(), cudaMemcpyHostToDevice));
+    auto *dt = dalloc<unsigned char>(c, static_cast<int64_t>(tb));
+    CK(cudaMemcpy(dt, tab.data(), tb, cudaMemcpyHostToDevice));
+    D.pat = 1;
+    D.pat_np = np;
+    D.pat_w = w;
+    D.pat_tb = tb;
+    D.pat_id = dp;
+    D.pat_table = dt;
+    return true;
+}
+
+// Matrix part of a level: diagonal, then the first format that applies: row
+// patterns (RPAT), grouped sliced-ELL (SELL-G), CSR tiles. Columns need not be
+// sorted (partitioned levels number ghosts after own rows).
 static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
-    if (A.nnz() > INT32_MAX - 16 || A.n > INT32_MAX - 1)
-        throw invalid_argument("sb_create: level too large for int32 device offsets");
     D.n = A.n;
     D.nnz = A.nnz();
-    std::vector<int32_t> rp32(static_cast<size_t>(A.n) + 1);
-    for (int64_t i = 0; i <= A.n; ++i) rp32[i] = static_cast<int32_t>(A.rp[i]);
-    D.rp = dalloc<int32_t>(c, A.n + 1 + 8);  // + slack for 16-byte TMA windows
-    D.ci = dalloc<int32_t>(c, A.nnz() + 8);
-    D.v = dalloc<double>(c, A.nnz() + 2);
-    CK(cudaMemcpy(D.rp, rp32.data(), sizeof(int32_t) * rp32.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(D.ci, A.ci.data(), sizeof(int32_t) * A.ci.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(D.v, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice));
     // diagonal + first bad row (smoother.hpp:55-70)
     std::vector<double> diag(static_cast<size_t>(A.n), 0.0);
     D.bad_diag = -1;
@@ -1929,6 +2052,18 @@ static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
     }
     D.diag = dalloc<double>(c, A.n);
     CK(cudaMemcpy(D.diag, diag.data(), sizeof(double) * diag.size(), cudaMemcpyHostToDevice));
+    if (A.n > INT32_MAX - 1024) throw invalid_argument("sb_create: level too large for int32 row indices");
+    if (build_rpat(c, A, D)) return;  // 1 B/row: no other copy of the matrix on the device
+    if (A.nnz() > INT32_MAX - 16)
+        throw invalid_argument("sb_create: level too large for int32 device offsets (and not row-pattern)");
+    std::vector<int32_t> rp32(static_cast<size_t>(A.n) + 1);
+    for (int64_t i = 0; i <= A.n; ++i) rp32[i] = static_cast<int32_t>(A.rp[i]);
+    D.rp = dalloc<int32_t>(c, A.n + 1 + 8);  // + slack for 16-byte TMA windows
+    D.ci = dalloc<int32_t>(c, A.nnz() + 8);
+    D.v = dalloc<double>(c, A.nnz() + 2);
+    CK(cudaMemcpy(D.rp, rp32.data(), sizeof(int32_t) * rp32.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(D.ci, A.ci.data(), sizeof(int32_t) * A.ci.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(D.v, A.v.data(), sizeof(double) * A.v.size(), cudaMemcpyHostToDevice));
     std::vector<int32_t> tiles;
     make_tiles(A, tiles, D.cap);
     D.ntiles = static_cast<int>(tiles.size()) - 1;
@@ -2108,74 +2243,6 @@ static void upload_matrix(sb_ctx c, const HostCsr &A, DevLevel &D) {
             D.sell_gs = gs;
             D.sell_slots = slots;
             D.sell_smem = kSgStages * stage;
-        }
-    }
-    // row-pattern format (SB_RPAT=0 disables): <= 256 distinct rows, W <= 32
-    const char *pe = std::getenv("SB_RPAT");
-    if ((!pe || std::atoi(pe) != 0) && A.n > 0) {
-        std::map<std::vector<uint64_t>, int> ids;
-        std::vector<std::vector<uint64_t>> keys;
-        std::vector<uint8_t> pid(static_cast<size_t>(A.n));
-        int wmax = 0;
-        bool ok = true;
-        std::vector<uint64_t> key;
-        for (int64_t i = 0; i < A.n && ok; ++i) {
-            key.clear();
-            for (int64_t e = A.rp[i]; e < A.rp[i + 1]; ++e) {
-                uint64_t bits;
-                std::memcpy(&bits, &A.v[e], 8);
-                key.push_back(static_cast<uint64_t>(static_cast<int64_t>(A.ci[e]) - i));
-                key.push_back(bits);
-            }
-            auto it = ids.find(key);
-            if (it == ids.end()) {
-                if (keys.size() == 256) {
-                    ok = false;
-                    break;
-                }
-                it = ids.emplace(key, static_cast<int>(keys.size())).first;
-                keys.push_back(key);
-            }
-            pid[static_cast<size_t>(i)] = static_cast<uint8_t>(it->second);
-            wmax = std::max<int>(wmax, static_cast<int>(A.rp[i + 1] - A.rp[i]));
-        }
-        const int w = wmax <= 5 ? 5 : wmax <= 7 ? 7 : wmax <= 8 ? 8 : wmax <= 16 ? 16 : wmax <= 28 ? 28 : 32;
-        if (ok && wmax <= 32) {
-            const int np = static_cast<int>(keys.size());
-            const size_t tb = pat_table_bytes(np, w);
-            std::vector<unsigned char> tab(tb, 0);
-            auto *val = reinterpret_cast<double *>(tab.data());
-            auto *dg = val + static_cast<size_t>(np) * w;
-            auto *ry = dg + np;
-            auto *off = reinterpret_cast<int32_t *>(ry + np);
-            auto *len = reinterpret_cast<uint8_t *>(off + static_cast<size_t>(np) * w);
-            for (int q = 0; q < np; ++q) {
-                const std::vector<uint64_t> &k = keys[static_cast<size_t>(q)];
-                const int lq = static_cast<int>(k.size() / 2);
-                len[q] = static_cast<uint8_t>(lq);
-                dg[q] = 0.0;
-                for (int e = 0; e < w; ++e) {
-                    off[q * w + e] = 0;  // padding: the row itself, value 0.0 (predicated out)
-                    val[q * w + e] = 0.0;
-                    if (e < lq) {
-                        off[q * w + e] = static_cast<int32_t>(static_cast<int64_t>(k[2 * e]));
-                        std::memcpy(&val[q * w + e], &k[2 * e + 1], 8);
-                        if (off[q * w + e] == 0) dg[q] = val[q * w + e];
-                    }
-                }
-                const double ad = std::fabs(dg[q]);
-                ry[q] = (ad >= std::ldexp(1.0, -100) && ad <= std::ldexp(1.0, 100)) ? 1.0 / dg[q] : 0.0;
-            }
-            auto *dp = dalloc<uint8_t>(c, A.n + 16);
-            CK(cudaMemcpy(dp, pid.data(), pid.size(), cudaMemcpyHostToDevice));
-            auto *dt = dalloc<unsigned char>(c, static_cast<int64_t>(tb));
-            CK(cudaMemcpy(dt, tab.data(), tb, cudaMemcpyHostToDevice));
-            D.pat = 1;
-            D.pat_np = np;
-            D.pat_w = w;
-            D.pat_tb = tb;
-            D.pat_id = dp;
-            D.pat_table = dt;
         }
     }
 }

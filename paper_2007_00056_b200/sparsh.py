@@ -338,6 +338,23 @@ class Hierarchy:
         self._A0 = A
         self.config = cfg
 
+    @classmethod
+    def from_stencil27(cls, nx: int, ny: int, nz: int, diag: float, off: float, cfg: SolverConfig = None,
+                       device: int = 0, galerkin_gpu: bool = False) -> "Hierarchy":
+        """Hierarchy of the 3D 27-point operator generated straight into the setup's
+        host storage (sb_setup_stencil27): no Python-side copy of the fine matrix,
+        int64 row offsets (config 5: 512^3, nnz 3.6e9)."""
+        cfg = cfg or SolverConfig()
+        cfg.validate()
+        self = cls.__new__(cls)
+        opts = _lib.sb_setup_opts(0, cfg.coarse_target, cfg.max_levels, 0, 0, 1 if galerkin_gpu else 0, device)
+        h = C.c_void_p()
+        check(_lib.lib().sb_setup_stencil27(int(nx), int(ny), int(nz), float(diag), float(off), C.byref(opts),
+                                            C.byref(h)))
+        self._h, self._ctx, self._device, self._coarse_exact = h, None, device, False
+        self._host_from, self._levels, self._A0, self.config = -1, None, None, cfg
+        return self
+
     def __del__(self):
         try:
             L = _lib.lib()

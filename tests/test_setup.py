@@ -112,3 +112,17 @@ def test_bad_inputs_raise_like_reference(sp):
     with pytest.raises(sp.InvalidArgument, match="2000"):
         # default max_levels = 10 stops 1024^2 at 2048 rows: dense LU limit
         sp.Hierarchy(sp.poisson2d(64, 64), sp.SolverConfig(max_levels=1))
+
+
+def test_setup_stencil27_matches_generated(sp):
+    # sb_setup_stencil27 (generator fused into the setup, int64 offsets) builds
+    # the same hierarchy as sb_gen_stencil27 + sb_setup
+    cfg = sp.SolverConfig(max_levels=40)
+    ha = sp.Hierarchy(sp._gen(sp._lib.lib().sb_gen_stencil27, 9, 10, 11, 26.0, -1.0), cfg)
+    hb = sp.Hierarchy.from_stencil27(9, 10, 11, 26.0, -1.0, cfg)
+    assert ha.nlevels() == hb.nlevels()
+    for k in range(ha.nlevels()):
+        a, b = ha.level(k), hb.level(k)
+        assert a.A == b.A
+        if a.agg is not None:
+            assert np.array_equal(a.agg.fine_to_coarse, b.agg.fine_to_coarse)
