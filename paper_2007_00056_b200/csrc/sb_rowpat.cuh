@@ -28,6 +28,9 @@ __host__ __device__ __forceinline__ size_t pat_table_bytes(int np, int w) {
 #ifndef SB_PAT_MINB_WIDE
 #define SB_PAT_MINB_WIDE 2
 #endif
+#ifndef SB_PAT_CHUNK
+#define SB_PAT_CHUNK 28
+#endif
 #ifndef SB_PAT_MINB
 #define SB_PAT_MINB 4
 #endif
@@ -65,7 +68,47 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
         pn[q] = pid[r < n ? r : n - 1];  // out-of-range threads replay row n-1 (valid gathers)
     }
     pdl_wait();
-    if (!(skip && *skip)) {
+    if constexpr (W > 8 && (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV)) {
+        // wide rows (27-point levels): one row per thread, the gathers in chunks
+        // of SB_PAT_CHUNK (registers for more resident warps), sums in slot order
+        if (!(skip && *skip)) {
+            for (int base = blockIdx.x * kPatThreads; base < n; base += stride) {
+                if (base + stride >= n) pdl_trigger();
+                const int row = base + threadIdx.x;
+                const int p = pn[0];
+                { const int r = row + stride; pn[0] = pid[r < n ? r : n - 1]; }
+                const int rq = row < n ? row : n - 1;
+                const double *xr = x + rq;
+                const double fi = (MODE == M_SPMV) ? 0.0 : __ldg(f + rq);
+                const double xi = __ldg(xr);
+                double sum = 0.0;
+#pragma unroll
+                for (int c0 = 0; c0 < W; c0 += SB_PAT_CHUNK) {
+                    double xv[SB_PAT_CHUNK];
+#pragma unroll
+                    for (int k = 0; k < SB_PAT_CHUNK; ++k)
+                        if (c0 + k < W) xv[k] = __ldg(xr + soff[p * W + c0 + k]);
+#pragma unroll
+                    for (int k = 0; k < SB_PAT_CHUNK; ++k)
+                        if (c0 + k < W) sum = __dadd_rn(sum, __dmul_rn(sval[p * W + c0 + k], xv[k]));
+                }
+                const int len = slen[p];
+                if (len < W && !isfinite(xi)) {  // exact replay for a non-finite own x (see below)
+                    sum = 0.0;
+                    for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(sval[p * W + k], __ldg(xr + soff[p * W + k])));
+                }
+                if (row < n) {
+                    double o;
+                    if constexpr (MODE == M_SPMV) o = sum;
+                    else if constexpr (MODE == M_RESID) o = __dsub_rn(fi, sum);
+                    else o = __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), sdg[p], sry[p]));
+                    out[row] = o;
+                    if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fi : red.w0[row]) : o);
+                    if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
+                }
+            }
+        }
+    } else if (!(skip && *skip)) {
         for (int base = blockIdx.x * kPatThreads * kPatRows; base < n; base += stride) {
             if (base + stride >= n) pdl_trigger();
             int row[kPatRows], p[kPatRows];
