@@ -446,7 +446,8 @@ static void dist_pcg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
             each([&](RankDev &r, int64_t n) {
                 launch_k(r.c, k_pcg_update, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n, r.c->kv[KX],
                          r.c->kv[KR], static_cast<const double *>(r.c->kv[KP]),
-                         static_cast<const double *>(r.c->kv[KAP]), red_partial(r.c, 1));
+                         static_cast<const double *>(r.c->kv[KAP]), red_partial(r.c, 1),
+                         static_cast<const double *>(nullptr), static_cast<double *>(nullptr), 0.0);
             });
             allreduce_logic(d, EP_PCG_RN);
             if (read_done(d)) break;

@@ -334,13 +334,13 @@ enum CsrMode {
     M_SPMV = 0,          // y = A x                          (csr.hpp:174-194)
     M_RESID = 1,         // r = f - A x                      (csr.hpp:267-274)
     M_JACOBI = 2,        // x' = x + w (f - A x) / a_ii      (smoother.hpp:113-120)
-    M_JACOBI_ZERO = 3,   // first two sweeps from x = 0 fused: neighbours' x0_j = 0 + w f_j / a_jj
+    // 3: retired (the first sweep from x = 0 is written by the parent's restriction)
     M_JACOBI_PROLONG = 4 // prolongation + first post-sweep fused: x_j + (0 + x_c[agg_j])
 };
 
 // Operands of the fused modes.
 struct Aux {
-    const double *diag;   // a_ii (M_JACOBI_ZERO)
+    const double *diag;   // a_ii
     const int32_t *agg;   // fine_to_coarse (M_JACOBI_PROLONG)
     const double *xc;     // coarse correction (M_JACOBI_PROLONG)
 };
@@ -356,9 +356,7 @@ template <bool CG> __device__ __forceinline__ double ldv(const double *p) {
 // The value the reference's sweep sees for x_j (bitwise).
 template <int MODE, bool CG>
 __device__ __forceinline__ double xval(int j, const double *x, const double *f, const Aux &a, double omega) {
-    if constexpr (MODE == M_JACOBI_ZERO)
-        return __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, ldv<CG>(f + j)), __ldg(a.diag + j)));
-    else if constexpr (MODE == M_JACOBI_PROLONG)
+    if constexpr (MODE == M_JACOBI_PROLONG)
         return __dadd_rn(ldv<CG>(x + j), __dadd_rn(0.0, ldv<CG>(a.xc + __ldg(a.agg + j))));
     else
         return ldv<CG>(x + j);
@@ -1229,8 +1227,13 @@ __global__ void k_dot(int64_t n, const double *__restrict__ u, const double *__r
 }
 
 // PCG update (krylov.hpp:96-98): x += alpha p; r += (-alpha) Ap; ||r||^2
+// x0 != nullptr: also the next preconditioner's first Jacobi sweep from 0 on
+// level 0, x0 = 0 + (w r)/a_ii (smoother.hpp:112-119), so the V-cycle skips
+// its zero-sweep kernel (harmless when the loop stops here: x0 is unused).
 __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
-                             const double *__restrict__ p, const double *__restrict__ Ap, Red red) {
+                             const double *__restrict__ p, const double *__restrict__ Ap, Red red,
+                             const double *__restrict__ diag = nullptr, double *__restrict__ x0 = nullptr,
+                             double omega = 0.0) {
     pdl_wait();  // launched with PDL on the partitioned path
     double a[1] = {0.0};
     const DevState *st = red.st;
@@ -1241,6 +1244,7 @@ __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restri
             const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
             r[i] = ri;
             a[0] += ri * ri;
+            if (x0) x0[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, ri), diag[i]));
         }
     }
     finish_reduction<1>(red, a);
@@ -1771,16 +1775,20 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
     const int vb = vec_grid(n);
     double *r = c->kv[KR], *z = c->kv[KZ], *p = c->kv[KP], *Ap = c->kv[KAP];
     cudaStream_t s = c->stream;
-    auto precond = [c, cp, n](cudaStream_t ss, const double *in, double *out) {
-        if (cp) emit_vcycle(c, ss, *cp, 0, in, out, true);
+    auto precond = [c, cp, n](cudaStream_t ss, const double *in, double *out, bool x0_ready) {
+        if (cp) emit_vcycle(c, ss, *cp, 0, in, out, true, x0_ready);
         else CK(cudaMemcpyAsync(out, in, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToDevice, ss));
     };
+    // the update kernel writes the V-cycle's first level-0 sweep when level 0
+    // is an ordinary level with a pre-smoother
+    const int L = static_cast<int>(c->L.size());
+    double *x0 = (cp && cp->pre >= 1 && L >= 2 && c->tail_from != 0) ? zero_sweep_dest(c, *cp, 0, z) : nullptr;
     cudaGraph_t g = begin_capture(c);
     cudaGraphConditionalHandle h_pro = new_handle(s);
     k_init<<<vb, kVecThreads, 0, s>>>(n, b, x, r, make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_pro})));
     CK(cudaGetLastError());
     add_cond(c, s, 0, h_pro, cudaGraphCondTypeIf, [&](cudaStream_t s1, int d1) {
-        precond(s1, r, z);
+        precond(s1, r, z, false);
         cudaGraphConditionalHandle h_loop = new_handle(s1);
         k_copy_dot<<<vb, kVecThreads, 0, s1>>>(n, z, p, nullptr, r,
                                               make_red(c, EP_PCG_RZ0, 1, nullptr, nullptr, conds({h_loop})));
@@ -1789,13 +1797,14 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
             launch_csr<M_SPMV, 1>(c, l0, s2, p, nullptr, Ap, 0.0, &c->st->done, make_red(c, EP_PCG_PAP, 1, p));
             cudaGraphConditionalHandle h_vc = new_handle(s2);
             k_pcg_update<<<vb, kVecThreads, 0, s2>>>(
-                n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})));
+                n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})),
+                static_cast<const double *>(l0.diag), x0, cp ? cp->omega : 0.0);
             CK(cudaGetLastError());
             add_cond(c, s2, d2, h_vc, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
                 const Red rz = make_red(c, EP_PCG_RZ, 1, r);
                 c->final_red = &rz;  // (r, z) rides on the V-cycle's last sweep when it is a Jacobi sweep
                 c->final_red_used = false;
-                precond(s3, r, z);
+                precond(s3, r, z, x0 != nullptr);
                 c->final_red = nullptr;
                 if (!c->final_red_used) {
                     k_dot<<<vb, kVecThreads, 0, s3>>>(n, r, z, nullptr, rz);
