@@ -227,19 +227,21 @@ int sb_coarse_solve(sb_ctx ctx, const double *f, double *x);
 
 /* Rank `rank` of `nranks`: contiguous owned rows per distributed level (level 0
  * split evenly, coarse levels induced by the aggregates), columns renumbered
- * [own | ghost], exchange plans for the x halo, straddling-aggregate residuals
+ * [own | ghost] or kept as global offsets in the window layout (info11[9..10] = rows
+ * below / above own in the x vectors), exchange plans (recv_dst: where each peer's
+ * chunk lands relative to own row 0) for the x halo, straddling-aggregate residuals
  * and coarse parents; levels with < gather_rows rows (and below) replicated.
  * Host-only; every rank computes identical plans from the same hierarchy. */
 typedef struct sb_part_s *sb_part;
 int sb_partition(sb_hier h, int rank, int nranks, int64_t gather_rows, sb_part *out);
 void sb_partition_free(sb_part p);
 int sb_partition_info(sb_part p, int *nlevels, int *first_replicated);
-int sb_partition_level(sb_part p, int level, int64_t *info9, sb_csr *A_local, const int64_t **ghost,
+int sb_partition_level(sb_part p, int level, int64_t *info11, sb_csr *A_local, const int64_t **ghost,
                        const int64_t **rghost, const int64_t **xcghost, const int32_t **mem0,
                        const int32_t **mem1, const int32_t **parent);
 int sb_partition_exchange(sb_part p, int level, int which, int64_t *counts4, const int **send_peers,
                           const int64_t **send_off, const int32_t **send_idx, const int **recv_peers,
-                          const int64_t **recv_off);
+                          const int64_t **recv_off, const int64_t **recv_dst);
 
 /* Partitioned solve. NCCL mode: one rank per process/GPU; rank 0 calls
  * sb_nccl_unique_id and broadcasts the 128 bytes (e.g. torch.distributed);

@@ -151,7 +151,8 @@ _SIGS = {
                                      C.POINTER(C.POINTER(C.c_int32)), C.POINTER(C.POINTER(C.c_int32))]),
     "sb_partition_exchange": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.POINTER(C.c_int)),
                                         C.POINTER(C.POINTER(C.c_int64)), C.POINTER(C.POINTER(C.c_int32)),
-                                        C.POINTER(C.POINTER(C.c_int)), C.POINTER(C.POINTER(C.c_int64))]),
+                                        C.POINTER(C.POINTER(C.c_int)), C.POINTER(C.POINTER(C.c_int64)),
+                                        C.POINTER(C.POINTER(C.c_int64))]),
 }
 
 

@@ -54,6 +54,7 @@ Exchange make_exchange(const std::vector<int64_t> &b, int rank, int nranks, cons
         size_t j = i;
         while (j < need.size() && owner_of(b, need[j]) == o) ++j;
         e.recv_peers.push_back(o);
+        e.recv_dst.push_back(e.recv_off.back());  // packed (callers may remap)
         e.recv_off.push_back(static_cast<int64_t>(j));
         i = j;
     }
@@ -84,6 +85,23 @@ std::vector<int64_t> ghosts_of(const HostCsr &A, int64_t lo, int64_t hi) {
     std::sort(g.begin(), g.end());
     g.erase(std::unique(g.begin(), g.end()), g.end());
     return g;
+}
+
+// Halo ids rank q receives for rows [b[q], b[q+1]) of A, and whether they
+// use the window layout: the ghost ids of each peer widened to the peer's
+// [min, max] range when the widened total stays within 2x the ghosts (+64).
+std::vector<int64_t> halo_need(const HostCsr &A, const std::vector<int64_t> &b, int q, bool *window) {
+    const std::vector<int64_t> g = ghosts_of(A, b[q], b[q + 1]);
+    std::vector<int64_t> w;
+    for (size_t i = 0; i < g.size();) {
+        const int o = owner_of(b, g[i]);
+        size_t j = i;
+        while (j < g.size() && owner_of(b, g[j]) == o) ++j;
+        for (int64_t id = g[i]; id <= g[j - 1]; ++id) w.push_back(id);
+        i = j;
+    }
+    *window = static_cast<int64_t>(w.size()) <= 2 * static_cast<int64_t>(g.size()) + 64;
+    return *window ? w : g;
 }
 
 // second members (owned elsewhere) of the coarse rows [c_lo, c_hi)
@@ -156,16 +174,25 @@ Partition build_partition(const Hier &h, int rank, int nranks, int64_t gather_ro
         pl.lo = b[rank];
         pl.hi = b[rank + 1];
         const int64_t nl = pl.hi - pl.lo;
-        // local matrix with [own | ghost] columns
-        pl.ghost_glob = ghosts_of(H.A, pl.lo, pl.hi);
+        // local matrix: window layout (global offsets kept) or [own | ghost] columns
+        bool window = false;
+        pl.ghost_glob = halo_need(H.A, b, rank, &window);
+        const int64_t n_below = std::lower_bound(pl.ghost_glob.begin(), pl.ghost_glob.end(), pl.lo) - pl.ghost_glob.begin();
+        if (window) {
+            pl.wb = n_below ? pl.lo - pl.ghost_glob.front() : 0;
+            pl.wa = static_cast<int64_t>(pl.ghost_glob.size()) > n_below ? pl.ghost_glob.back() + 1 - pl.hi : 0;
+        } else {
+            pl.wb = 0;
+            pl.wa = static_cast<int64_t>(pl.ghost_glob.size());
+        }
         pl.A.n = nl;
-        pl.A.ncols = nl + static_cast<int64_t>(pl.ghost_glob.size());
+        pl.A.ncols = nl + pl.wa;
         pl.A.rp.assign(static_cast<size_t>(nl) + 1, 0);
         for (int64_t i = pl.lo; i < pl.hi; ++i) {
             for (int64_t kk = H.A.rp[i]; kk < H.A.rp[i + 1]; ++kk) {
                 const int64_t c = H.A.ci[kk];
                 int64_t lc;
-                if (c >= pl.lo && c < pl.hi) lc = c - pl.lo;
+                if (window || (c >= pl.lo && c < pl.hi)) lc = c - pl.lo;
                 else lc = nl + (std::lower_bound(pl.ghost_glob.begin(), pl.ghost_glob.end(), c) - pl.ghost_glob.begin());
                 pl.A.ci.push_back(static_cast<int32_t>(lc));
                 pl.A.v.push_back(H.A.v[kk]);
@@ -173,8 +200,13 @@ Partition build_partition(const Hier &h, int rank, int nranks, int64_t gather_ro
             pl.A.rp[i - pl.lo + 1] = static_cast<int64_t>(pl.A.ci.size());
         }
         pl.A.sync_rp32();
-        pl.halo = make_exchange(b, rank, nranks, pl.ghost_glob,
-                                [&](int q) { return ghosts_of(H.A, b[q], b[q + 1]); });
+        pl.halo = make_exchange(b, rank, nranks, pl.ghost_glob, [&](int q) {
+            bool wq = false;
+            return halo_need(H.A, b, q, &wq);
+        });
+        for (size_t j = 0; j < pl.halo.recv_peers.size(); ++j)  // chunk destinations (relative to own row 0)
+            pl.halo.recv_dst[j] = window ? pl.ghost_glob[static_cast<size_t>(pl.halo.recv_off[j])] - pl.lo
+                                         : nl + pl.halo.recv_off[j];
         // restriction / prolongation with the next level
         const bool next_rep = k + 1 >= fr;
         const std::vector<int64_t> cb =
@@ -253,8 +285,8 @@ int sb_partition_info(sb_part p, int *nlevels, int *first_replicated) {
     return SB_OK;
 }
 
-// Level k of this rank. i64[0..8] = {n_glob, lo, hi, n_ghost, c_lo, c_hi,
-// n_rghost, n_xcghost, replicated}. Borrowed arrays (valid while p lives):
+// Level k of this rank. i64[0..10] = {n_glob, lo, hi, n_ghost, c_lo, c_hi,
+// n_rghost, n_xcghost, replicated, wb, wa}. Borrowed arrays (valid while p lives):
 // A (local CSR), ghost / rghost / xcghost global ids, mem0 / mem1 / parent,
 // and the three exchange plans (peers, offsets, send indices).
 int sb_partition_level(sb_part p, int k, int64_t *i64, sb_csr *A, const int64_t **ghost, const int64_t **rghost,
@@ -262,9 +294,9 @@ int sb_partition_level(sb_part p, int k, int64_t *i64, sb_csr *A, const int64_t 
     return guard([&] {
         if (!p || k < 0 || k >= static_cast<int>(p->p.L.size())) throw invalid_argument("sb_partition_level: level");
         const PartLevel &l = p->p.L[static_cast<size_t>(k)];
-        const int64_t v[9] = {l.n_glob, l.lo, l.hi, static_cast<int64_t>(l.ghost_glob.size()), l.c_lo, l.c_hi,
-                              static_cast<int64_t>(l.rghost_glob.size()), static_cast<int64_t>(l.xcghost_glob.size()),
-                              l.replicated ? 1 : 0};
+        const int64_t v[11] = {l.n_glob, l.lo, l.hi, static_cast<int64_t>(l.ghost_glob.size()), l.c_lo, l.c_hi,
+                               static_cast<int64_t>(l.rghost_glob.size()), static_cast<int64_t>(l.xcghost_glob.size()),
+                               l.replicated ? 1 : 0, l.wb, l.wa};
         std::memcpy(i64, v, sizeof(v));
         if (A) {
             A->nrows = l.A.n;
@@ -287,7 +319,7 @@ int sb_partition_level(sb_part p, int k, int64_t *i64, sb_csr *A, const int64_t 
 // level k: counts[0..3] = {n_send_peers, n_recv_peers, total_send, total_recv}.
 int sb_partition_exchange(sb_part p, int k, int which, int64_t *counts, const int **send_peers,
                           const int64_t **send_off, const int32_t **send_idx, const int **recv_peers,
-                          const int64_t **recv_off) {
+                          const int64_t **recv_off, const int64_t **recv_dst) {
     return guard([&] {
         if (!p || k < 0 || k >= static_cast<int>(p->p.L.size())) throw invalid_argument("sb_partition_exchange: level");
         const PartLevel &l = p->p.L[static_cast<size_t>(k)];
@@ -301,6 +333,7 @@ int sb_partition_exchange(sb_part p, int k, int which, int64_t *counts, const in
         *send_idx = e.send_idx.data();
         *recv_peers = e.recv_peers.data();
         *recv_off = e.recv_off.data();
+        if (recv_dst) *recv_dst = e.recv_dst.data();
     });
 }
 

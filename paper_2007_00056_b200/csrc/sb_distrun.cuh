@@ -117,7 +117,7 @@ __global__ void k_sum_partials(const double *const *parts, int nranks, double *o
 
 struct DevExch {
     std::vector<int> send_peers, recv_peers;
-    std::vector<int64_t> send_off, recv_off;
+    std::vector<int64_t> send_off, recv_off, recv_dst;
     int32_t *send_idx = nullptr;  // device
     double *sendbuf = nullptr;    // device (NCCL packing)
     int64_t nsend = 0, nrecv = 0;
@@ -126,6 +126,7 @@ struct DevExch {
 struct DistLevel {
     bool dist = false, next_rep = false;
     int64_t n_own = 0, n_ext = 0, nc_own = 0, c_lo = 0;
+    int64_t wb = 0, wa = 0;  // x-like vectors: wb rows below own row 0, wa above (n_ext = n_own + wa)
     double *rg = nullptr, *xcg = nullptr;  // residual-partner / coarse-parent ghosts
     DevExch halo, rx, px;
     std::vector<int64_t> gather_lo;  // first replicated level: owned pieces per rank
@@ -160,6 +161,7 @@ static DevExch upload_exch(sb_ctx c, const Exchange &e) {
     d.recv_peers = e.recv_peers;
     d.send_off = e.send_off.empty() ? std::vector<int64_t>{0} : e.send_off;
     d.recv_off = e.recv_off.empty() ? std::vector<int64_t>{0} : e.recv_off;
+    d.recv_dst = e.recv_dst;
     d.nsend = e.total_send();
     d.nrecv = e.total_recv();
     d.send_idx = dalloc<int32_t>(c, std::max<int64_t>(d.nsend, 1), false);
@@ -175,6 +177,8 @@ static void upload_dist_level(sb_ctx c, const PartLevel &pl, DevLevel &D, DistLe
     DL.dist = true;
     DL.n_own = pl.hi - pl.lo;
     DL.n_ext = pl.A.ncols;
+    DL.wb = pl.wb;
+    DL.wa = pl.wa;
     DL.nc_own = pl.c_hi - pl.c_lo;
     DL.c_lo = pl.c_lo;
     D.nc = DL.nc_own;
@@ -184,8 +188,8 @@ static void upload_dist_level(sb_ctx c, const PartLevel &pl, DevLevel &D, DistLe
     for (size_t q = 0; q < mem.size(); ++q) mem[q] = make_int2(pl.mem0[q], pl.mem1[q]);
     D.mem = dalloc<int2>(c, std::max<int64_t>(DL.nc_own, 1));
     CK(cudaMemcpy(D.mem, mem.data(), sizeof(int2) * mem.size(), cudaMemcpyHostToDevice));
-    D.t = dalloc<double>(c, DL.n_ext);
-    D.x = dalloc<double>(c, DL.n_ext);
+    D.t = dalloc<double>(c, DL.wb + DL.n_ext) + DL.wb;  // own row 0 at the returned pointer
+    D.x = dalloc<double>(c, DL.wb + DL.n_ext) + DL.wb;
     D.f = dalloc<double>(c, DL.n_own);
     DL.rg = dalloc<double>(c, std::max<int64_t>(static_cast<int64_t>(pl.rghost_glob.size()), 1));
     DL.xcg = dalloc<double>(c, std::max<int64_t>(static_cast<int64_t>(pl.xcghost_glob.size()), 1));
@@ -204,7 +208,9 @@ static void barrier_local(sb_dist d) {
             if (&q != &r) CK(cudaStreamWaitEvent(r.c->stream, q.done, 0));
 }
 
-// Fill ghost(r) from own(q) of every peer q, per the level-k plan `which`.
+// Fill the ghost entries of every rank r from own(q) of its peers q, per the
+// level-k plan `which`: chunk j of r lands at dst(r) + recv_dst[j] (halo: dst
+// is the own-rows pointer of the x vector; rx / px: the packed ghost buffers).
 static void exchange(sb_dist d, int k, int which, const std::function<const double *(RankDev &)> &own,
                      const std::function<double *(RankDev &)> &ghost) {
     auto plan = [&](RankDev &r) -> DevExch & {
@@ -224,7 +230,7 @@ static void exchange(sb_dist d, int k, int which, const std::function<const doub
                 const int64_t cnt = e.recv_off[j + 1] - e.recv_off[j];
                 CK(cudaStreamWaitEvent(r.c->stream, q.ready, 0));
                 launch_k(r.c, k_gather_idx, dim3(vec_grid(cnt)), dim3(kVecThreads), 0, r.c->stream, cnt, own(q),
-                         static_cast<const int32_t *>(eq.send_idx + eq.send_off[jj]), ghost(r) + e.recv_off[j]);
+                         static_cast<const int32_t *>(eq.send_idx + eq.send_off[jj]), ghost(r) + e.recv_dst[j]);
             }
         }
         barrier_local(d);
@@ -242,7 +248,7 @@ static void exchange(sb_dist d, int k, int which, const std::function<const doub
         NC(nccl().Send(e.sendbuf + e.send_off[j], static_cast<size_t>(e.send_off[j + 1] - e.send_off[j]), ncclFloat64,
                        e.send_peers[j], d->comm, s));
     for (size_t j = 0; j < e.recv_peers.size(); ++j)
-        NC(nccl().Recv(ghost(r) + e.recv_off[j], static_cast<size_t>(e.recv_off[j + 1] - e.recv_off[j]), ncclFloat64,
+        NC(nccl().Recv(ghost(r) + e.recv_dst[j], static_cast<size_t>(e.recv_off[j + 1] - e.recv_off[j]), ncclFloat64,
                        e.recv_peers[j], d->comm, s));
     NC(nccl().GroupEnd());
 }
@@ -314,7 +320,7 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
     auto halo = [&](std::vector<double *> &v) {
         std::vector<double *> vv = v;
         exchange(d, k, 0, [&](RankDev &r) -> const double * { return vv[static_cast<size_t>(&r - d->R.data())]; },
-                 [&](RankDev &r) { return vv[static_cast<size_t>(&r - d->R.data())] + r.D[static_cast<size_t>(k)].n_own; });
+                 [&](RankDev &r) { return vv[static_cast<size_t>(&r - d->R.data())]; });
     };
     auto sweep = [&]() {
         for (size_t i = 0; i < N; ++i) launch_jacobi(d->R[i].c, lev(i), d->R[i].c->stream, cur[i], f[i], oth[i], cp.omega);
@@ -399,7 +405,7 @@ static int read_done(sb_dist d) {
 
 static void dist_halo_vec(sb_dist d, int kv) {
     exchange(d, 0, 0, [&](RankDev &r) -> const double * { return r.c->kv[kv]; },
-             [&](RankDev &r) { return r.c->kv[kv] + r.D[0].n_own; });
+             [&](RankDev &r) { return r.c->kv[kv]; });
 }
 
 // vectors: KX x, KR r, KZ z, KP p, KAP Ap, KB b (own rows; x / p / pt / st with ghost room)
@@ -578,7 +584,7 @@ static void build_rank(sb_dist d, RankDev &R, const Hier &h, int rank, int64_t g
     if (d->fr == 0) R.D[0].n_own = R.D[0].n_ext = h.levels[0].A.n;
     R.lo = R.P.L[0].lo;
     R.hi = R.P.L[0].hi;
-    ctx_finish(c, h, o, nvec, d->fr);
+    ctx_finish(c, h, o, nvec, d->fr, d->fr > 0 ? R.D[0].wb : 0);
     CK(cudaEventCreateWithFlags(&R.ready, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&R.done, cudaEventDisableTiming));
 }

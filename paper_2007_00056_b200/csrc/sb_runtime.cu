@@ -2753,7 +2753,8 @@ static sb_ctx ctx_begin(const sb_device_opts &o) {
 // Launch configuration, coarse inverse, workspaces (n_vec = length of the
 // Krylov / scratch vectors: n0, or own + ghost rows on a partitioned level 0),
 // the cluster tail (only over levels >= tail_min).
-static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t n_vec, int tail_min) {
+static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t n_vec, int tail_min,
+                       int64_t vec_headroom = 0) {
     size_t max_smem = 0;
     for (auto &l : c->L) max_smem = std::max({max_smem, l.smem, l.sell_smem, l.pat_tb});
     if (max_smem > 200 * 1024) throw invalid_argument("sb_create: tile staging exceeds shared memory");
@@ -2801,7 +2802,9 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
     c->rs = dalloc<double>(c, n_vec);
     c->tail_min = tail_min;
     setup_tail(c, h);
-    for (auto &v : c->kv) v = dalloc<double>(c, n_vec);
+    // Krylov vectors; on a partitioned level 0 in the window layout the halo
+    // below own row 0 lives at negative indices (vec_headroom rows)
+    for (auto &v : c->kv) v = dalloc<double>(c, vec_headroom + n_vec) + vec_headroom;
     int maxb = 148 * 8;
     for (auto &l : c->L) maxb = std::max(maxb, l.ntiles);
     c->partials = dalloc<double>(c, 2 * static_cast<int64_t>(maxb) + 2, false);

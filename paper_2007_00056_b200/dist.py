@@ -38,19 +38,21 @@ class Partition:
             pass
 
     def level(self, k: int) -> dict:
-        info = (C.c_int64 * 9)()
+        info = (C.c_int64 * 11)()
         A = _lib.sb_csr()
         g, rg, xg = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
         m0, m1, par = C.POINTER(C.c_int32)(), C.POINTER(C.c_int32)(), C.POINTER(C.c_int32)()
         check(_lib.lib().sb_partition_level(self._p, k, info, C.byref(A), C.byref(g), C.byref(rg), C.byref(xg),
                                             C.byref(m0), C.byref(m1), C.byref(par)))
-        n_glob, lo, hi, ng, c_lo, c_hi, nrg, nxg, rep = list(info)
+        n_glob, lo, hi, ng, c_lo, c_hi, nrg, nxg, rep, wb, wa = list(info)
 
         def arr(ptr, n, dt):
             return np.ctypeslib.as_array(ptr, shape=(int(n),)).copy() if n else np.zeros(0, dt)
 
         nc_own = c_hi - c_lo
-        return dict(n_glob=n_glob, lo=lo, hi=hi, replicated=bool(rep), A=_from_abi(A),
+        # A's columns: window layout (wb > 0 or ghosts kept as c - lo) -> index x_ext[col + wb]
+        # where x_ext = [wb rows below | own | wa rows above]; compact layout: wb = 0, [own | ghost]
+        return dict(n_glob=n_glob, lo=lo, hi=hi, replicated=bool(rep), A=_from_abi(A), wb=wb, wa=wa,
                     ghost=arr(g, ng, np.int64), rghost=arr(rg, nrg, np.int64), xcghost=arr(xg, nxg, np.int64),
                     c_lo=c_lo, c_hi=c_hi,
                     mem0=arr(m0, nc_own if not rep else 0, np.int32), mem1=arr(m1, nc_own if not rep else 0, np.int32),
@@ -60,9 +62,9 @@ class Partition:
         """which: 0 x halo, 1 residual partners, 2 coarse parents."""
         cnt = (C.c_int64 * 4)()
         sp_, so, si = C.POINTER(C.c_int)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_int32)()
-        rp_, ro = C.POINTER(C.c_int)(), C.POINTER(C.c_int64)()
+        rp_, ro, rd = C.POINTER(C.c_int)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
         check(_lib.lib().sb_partition_exchange(self._p, k, which, cnt, C.byref(sp_), C.byref(so), C.byref(si),
-                                               C.byref(rp_), C.byref(ro)))
+                                               C.byref(rp_), C.byref(ro), C.byref(rd)))
         ns, nr, ts, tr = list(cnt)
 
         def arr(ptr, n, dt):
@@ -70,7 +72,7 @@ class Partition:
 
         return dict(send_peers=arr(sp_, ns, np.int32), send_off=arr(so, ns + 1, np.int64),
                     send_idx=arr(si, ts, np.int32), recv_peers=arr(rp_, nr, np.int32),
-                    recv_off=arr(ro, nr + 1, np.int64))
+                    recv_off=arr(ro, nr + 1, np.int64), recv_dst=arr(rd, nr, np.int64))
 
 
 class DistSolver:

@@ -88,19 +88,42 @@ def exchange(plan, own, tag):
     return out
 
 
+def halo_ext(pl, plan, v, tag):
+    """x vector of a partitioned level with its halo: [wb rows below | own | wa rows
+    above]; each peer's chunk lands at wb + recv_dst (window layout: ghosts at
+    their global offsets; compact layout: wb = 0, ghosts packed after own)."""
+    wb, wa, n = int(pl["wb"]), int(pl["wa"]), v.size
+    xe = np.zeros(wb + n + wa)
+    xe[wb:wb + n] = v
+    g = exchange(plan, v, tag)
+    for j in range(len(plan["recv_peers"])):
+        a, b = int(plan["recv_off"][j]), int(plan["recv_off"][j + 1])
+        d = wb + int(plan["recv_dst"][j])
+        xe[d:d + (b - a)] = g[a:b]
+    return xe
+
+
+def shifted(sp, pl):
+    """the local matrix with columns indexing halo_ext()'s vector"""
+    A = pl["A"]
+    return sp.CsrMatrix(A.nrows(), int(pl["wb"]) + A.nrows() + int(pl["wa"]), A.row_ptr(),
+                        A.col_idx() + int(pl["wb"]), A.values(), _validate=False)
+
+
 def vcycle_dist(part, levels, k, f_own, pre, post, coarse, tagbase):
     pl = part.level(k)
     if pl["replicated"]:
         return vcycle_global(levels, k, f_own, pre, post, coarse)
-    A = pl["A"]  # columns [own | ghost]
+    from paper_2007_00056_b200 import sparsh as sp
+    A = shifted(sp, pl)  # columns index the halo-extended vector
     n = A.nrows()
-    d = diag_of(A)
+    d = diag_of(pl["A"])
     halo = part.exchange(k, 0)
     tag = [tagbase]
 
     def ext(v):
         tag[0] += 1
-        return np.concatenate([v, exchange(halo, v, tag[0])])
+        return halo_ext(pl, halo, v, tag[0])
 
     x = np.zeros(n)
     for s in range(pre):
@@ -161,8 +184,8 @@ def _worker(rank, ws, port, results):
             # distributed SpMV + allreduced dot
             import torch
             pl = part.level(0)
-            xe = np.concatenate([f[lo:hi], exchange(part.exchange(0, 0), f[lo:hi], 99999)])
-            y = rowsum(pl["A"], xe)
+            xe = halo_ext(pl, part.exchange(0, 0), f[lo:hi], 99999)
+            y = rowsum(shifted(sp, pl), xe)
             assert np.array_equal(y, rowsum(A, f)[lo:hi])
             t = torch.tensor([float(np.dot(y, f[lo:hi]))], dtype=torch.float64)
             dist.all_reduce(t)
