@@ -285,6 +285,13 @@ int sb_gen_stencil27(int64_t nx, int64_t ny, int64_t nz, double diag, double off
 int sb_setup_stencil27(int64_t nx, int64_t ny, int64_t nz, double diag, double off, const sb_setup_opts *opts,
                        sb_hier *out);
 void sb_free_csr(sb_csr *m);
+/* read_matrix_market(path) — inc/mm_io.hpp:35-111 (coordinate real general |
+ * symmetric; duplicates summed as the reference's from_triplets, csr.hpp:57-95).
+ * I/O and format errors -> SB_ERUNTIME with the reference's messages. Free with
+ * sb_free_csr. */
+int sb_read_matrix_market(const char *path, sb_csr *out);
+/* write_matrix_market(A, path) — inc/mm_io.hpp:114-135 (general, 1-based, %.17g). */
+int sb_write_matrix_market(const char *path, const sb_csr *A);
 /* rhs_random(n, seed) — inc/problems.hpp:69-75 (std::mt19937, U[0,1)), bit-identical. */
 int sb_gen_rhs_random(int64_t n, unsigned seed, double *out);
 

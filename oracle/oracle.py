@@ -265,6 +265,8 @@ class Ref:
         L.ref_coarse_solve.argtypes = [P, _D, _D]
         L.ref_krylov.argtypes = [C.c_int, P, P, _D, _D, C.c_double, C.c_int, C.POINTER(Report)]
         L.ref_amg_solve.argtypes = [P, _D, _D, C.c_double, C.c_int, C.POINTER(Report)]
+        L.ref_read_mm.argtypes = [C.c_char_p, C.POINTER(P)]
+        L.ref_write_mm.argtypes = [P, C.c_char_p]
         self.L = L
 
     def check(self, rc):
@@ -283,6 +285,16 @@ class Ref:
                                       np.ascontiguousarray(A.col_idx()).ctypes.data_as(_I),
                                       _d(A.values()).ctypes.data_as(_D), C.byref(h)))
         return RefMatrix(self, h)
+
+    def read_matrix_market(self, path):
+        """the reference's read_matrix_market (inc/mm_io.hpp) -> (rp, ci, v)"""
+        h = C.c_void_p()
+        self.check(self.L.ref_read_mm(str(path).encode(), C.byref(h)))
+        return RefMatrix(self, h).arrays()
+
+    def write_matrix_market(self, A, path):
+        m = self.matrix(A)  # keep the handle alive across the call
+        self.check(self.L.ref_write_mm(m.h, str(path).encode()))
 
     def convdiff2d(self, nx, ny, bx, by, c):
         h = C.c_void_p()

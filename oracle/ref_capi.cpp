@@ -102,6 +102,13 @@ int ref_convdiff2d(int32_t nx, int32_t ny, double bx, double by, double c, void 
     return guard([&] { *out = new CsrMatrix(convdiff2d(nx, ny, bx, by, c)); });
 }
 void ref_csr_free(void *m) { delete static_cast<CsrMatrix *>(m); }
+// read_matrix_market / write_matrix_market (inc/mm_io.hpp)
+int ref_read_mm(const char *path, void **out) {
+    return guard([&] { *out = new CsrMatrix(read_matrix_market(path)); });
+}
+int ref_write_mm(void *m, const char *path) {
+    return guard([&] { write_matrix_market(*static_cast<CsrMatrix *>(m), std::string(path)); });
+}
 void ref_csr_info(void *m, int32_t *nrows, int32_t *ncols, int64_t *nnz) {
     auto *A = static_cast<CsrMatrix *>(m);
     *nrows = A->nrows();

@@ -85,6 +85,7 @@ EXPORTS = [
     "sb_partition_level", "sb_partition_exchange", "sb_nccl_unique_id", "sb_dist_create",
     "sb_dist_create_local", "sb_dist_destroy", "sb_dist_rows", "sb_dist_pcg", "sb_dist_pbicgstab",
     "sb_dist_vcycle", "sb_dist_last_solve_ms", "sb_dist_last_launches", "sb_galerkin_gpu", "sb_host_bytes", "sb_setup_stencil27",
+    "sb_read_matrix_market", "sb_write_matrix_market",
 ]
 
 _P = C.c_void_p
@@ -124,6 +125,8 @@ _SIGS = {
     "sb_setup_stencil27": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
                                      C.POINTER(sb_setup_opts), C.POINTER(_P)]),
     "sb_free_csr": (None, [C.POINTER(sb_csr)]),
+    "sb_read_matrix_market": (C.c_int, [C.c_char_p, C.POINTER(sb_csr)]),
+    "sb_write_matrix_market": (C.c_int, [C.c_char_p, C.POINTER(sb_csr)]),
     "sb_galerkin_gpu": (C.c_int, [C.POINTER(sb_csr), C.POINTER(C.c_int32), C.c_int64, C.c_int, C.POINTER(sb_csr)]),
     "sb_gen_rhs_random": (C.c_int, [C.c_int64, C.c_uint, _D]),
     "sb_last_solve_ms": (C.c_double, [_P]),

@@ -10,6 +10,9 @@
 // Build with -ffp-contract=off (the reference is compiled without FMA).
 
 #include <algorithm>
+#include <cctype>
+#include <fstream>
+#include <sstream>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -401,6 +404,109 @@ static void emit(HostCsr &M, sb_csr *out) {
     std::memcpy(v, M.v.data(), sizeof(double) * M.v.size());
     out->col_idx = ci;
     out->values = v;
+}
+
+// read_matrix_market / write_matrix_market — inc/mm_io.hpp:35-135 restated:
+// coordinate real general|symmetric, 1-based indices, symmetric entries
+// mirrored, then the reference's from_triplets (inc/csr.hpp:57-95: std::sort
+// by (row, col), duplicates summed from 0.0 in the sorted order).
+int sb_read_matrix_market(const char *path, sb_csr *out) {
+    return guard([&] {
+        if (!path || !out) throw invalid_argument("sb_read_matrix_market: null argument");
+        const std::string p(path);
+        std::ifstream in(p);
+        if (!in) throw runtime_error("read_matrix_market: cannot open '" + p + "'");
+        auto lower = [](std::string s) {
+            for (char &ch : s) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+            return s;
+        };
+        std::string banner;
+        if (!std::getline(in, banner)) throw runtime_error("read_matrix_market: '" + p + "' is empty");
+        std::istringstream hdr(banner);
+        std::string tag, object, format, field, symmetry;
+        hdr >> tag >> object >> format >> field >> symmetry;
+        if (lower(tag) != "%%matrixmarket" || lower(object) != "matrix")
+            throw runtime_error("read_matrix_market: '" + p + "': malformed header '" + banner + "'");
+        if (lower(format) != "coordinate")
+            throw runtime_error("read_matrix_market: '" + p + "': only coordinate format is supported");
+        if (lower(field) != "real")
+            throw runtime_error("read_matrix_market: '" + p + "': field '" + field + "' is not real");
+        const std::string sym = lower(symmetry);
+        if (sym != "general" && sym != "symmetric")
+            throw runtime_error("read_matrix_market: '" + p + "': symmetry '" + symmetry +
+                                "' is not general or symmetric");
+        std::string line;
+        auto next_data_line = [&](std::string &o) {
+            while (std::getline(in, o)) {
+                const auto pos = o.find_first_not_of(" \t\r\n");
+                if (pos == std::string::npos || o[pos] == '%') continue;
+                return true;
+            }
+            return false;
+        };
+        if (!next_data_line(line)) throw runtime_error("read_matrix_market: '" + p + "': missing size line");
+        long long nrows = 0, ncols = 0, nnz = 0;
+        {
+            std::istringstream sz(line);
+            if (!(sz >> nrows >> ncols >> nnz) || nrows < 0 || ncols < 0 || nnz < 0)
+                throw runtime_error("read_matrix_market: '" + p + "': malformed size line '" + line + "'");
+        }
+        struct Trip {
+            int32_t row, col;
+            double value;
+        };
+        std::vector<Trip> ent;
+        ent.reserve(static_cast<size_t>(sym == "symmetric" ? 2 * nnz : nnz));
+        for (long long e = 0; e < nnz; ++e) {
+            if (!next_data_line(line))
+                throw runtime_error("read_matrix_market: '" + p + "': expected " + std::to_string(nnz) +
+                                    " entries, found " + std::to_string(e));
+            std::istringstream es(line);
+            long long i = 0, j = 0;
+            double v = 0.0;
+            if (!(es >> i >> j >> v)) throw runtime_error("read_matrix_market: '" + p + "': malformed entry '" + line + "'");
+            if (i < 1 || i > nrows || j < 1 || j > ncols)
+                throw runtime_error("read_matrix_market: '" + p + "': index (" + std::to_string(i) + ", " +
+                                    std::to_string(j) + ") out of bounds for " + std::to_string(nrows) + "x" +
+                                    std::to_string(ncols));
+            ent.push_back({static_cast<int32_t>(i - 1), static_cast<int32_t>(j - 1), v});
+            if (sym == "symmetric" && i != j) ent.push_back({static_cast<int32_t>(j - 1), static_cast<int32_t>(i - 1), v});
+        }
+        std::sort(ent.begin(), ent.end(),
+                  [](const Trip &a, const Trip &b) { return a.row != b.row ? a.row < b.row : a.col < b.col; });
+        HostCsr M;
+        M.n = nrows;
+        M.ncols = ncols;
+        M.rp.assign(static_cast<size_t>(nrows) + 1, 0);
+        size_t k = 0;
+        while (k < ent.size()) {
+            const int32_t r = ent[k].row, cc = ent[k].col;
+            double sum = 0.0;
+            while (k < ent.size() && ent[k].row == r && ent[k].col == cc) sum += ent[k++].value;
+            M.ci.push_back(cc);
+            M.v.push_back(sum);
+            M.rp[static_cast<size_t>(r) + 1] = static_cast<int64_t>(M.ci.size());
+        }
+        for (long long r = 0; r < nrows; ++r)
+            M.rp[static_cast<size_t>(r) + 1] = std::max(M.rp[static_cast<size_t>(r) + 1], M.rp[static_cast<size_t>(r)]);
+        emit(M, out);
+    });
+}
+
+int sb_write_matrix_market(const char *path, const sb_csr *A) {
+    return guard([&] {
+        if (!path || !A) throw invalid_argument("sb_write_matrix_market: null argument");
+        const HostCsr M = csr_from_abi(*A);
+        std::ofstream out(path);
+        if (!out) throw runtime_error(std::string("write_matrix_market: cannot open '") + path + "'");
+        out << "%%MatrixMarket matrix coordinate real general\n";
+        out << M.n << " " << M.ncols << " " << M.nnz() << "\n";
+        out.precision(17);
+        for (int64_t i = 0; i < M.n; ++i)
+            for (int64_t e = M.rp[static_cast<size_t>(i)]; e < M.rp[static_cast<size_t>(i) + 1]; ++e)
+                out << (i + 1) << " " << (M.ci[static_cast<size_t>(e)] + 1) << " " << M.v[static_cast<size_t>(e)] << "\n";
+        if (!out) throw runtime_error(std::string("write_matrix_market: write to '") + path + "' failed");
+    });
 }
 
 int sb_galerkin_gpu(const sb_csr *A, const int32_t *f2c, int64_t n_coarse, int device, sb_csr *out) {

@@ -466,6 +466,17 @@ class Hierarchy:
         return x
 
 
+def read_matrix_market(path) -> CsrMatrix:
+    """mm_io.hpp:35-111 (reference semantics and messages)."""
+    return _gen(_lib.lib().sb_read_matrix_market, str(path).encode())
+
+
+def write_matrix_market(A: CsrMatrix, path) -> None:
+    """mm_io.hpp:114-135."""
+    a = A._abi()
+    check(_lib.lib().sb_write_matrix_market(str(path).encode(), C.byref(a)))
+
+
 def galerkin_product_gpu(A: CsrMatrix, agg: "Aggregation", device: int = 0) -> CsrMatrix:
     """galerkin_product(A, agg) (inc/aggregation.hpp:92-152) computed on the GPU;
     bit-identical to the reference."""
