@@ -15,6 +15,15 @@
 // f64 rdiag[np] | int32 off[np][W] | uint8 len[np] (padded to 16).
 
 constexpr int kPatThreads = 256;
+
+// base + off (doubles) as ONE 32x32->64 multiply-add (IMAD.WIDE): the
+// compiler otherwise re-associates (row + off) into 64-bit index arithmetic
+// (4 instructions per gather)
+__device__ __forceinline__ const double *at_off(const double *base, int off) {
+    const double *r;
+    asm("mad.wide.s32 %0, %1, 8, %2;" : "=l"(r) : "r"(off), "l"(base));
+    return r;
+}
 // rows per thread per iteration (their gathers in flight together)
 #ifndef SB_PAT_ROWS
 #define SB_PAT_ROWS 2
@@ -87,7 +96,7 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
                     double xv[SB_PAT_CHUNK];
 #pragma unroll
                     for (int k = 0; k < SB_PAT_CHUNK; ++k)
-                        if (c0 + k < W) xv[k] = __ldg(xr + soff[p * W + c0 + k]);
+                        if (c0 + k < W) xv[k] = __ldg(at_off(xr, soff[p * W + c0 + k]));
 #pragma unroll
                     for (int k = 0; k < SB_PAT_CHUNK; ++k)
                         if (c0 + k < W) sum = __dadd_rn(sum, __dmul_rn(sval[p * W + c0 + k], xv[k]));
@@ -128,7 +137,7 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
                     const int off = soff[p[q] * W + k];
-                    if constexpr (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV) xv[q][k] = __ldg(xr + off);
+                    if constexpr (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV) xv[q][k] = __ldg(at_off(xr, off));
                     else xv[q][k] = xval<MODE, false>(rq + off, x, f, aux, omega);
                 }
                 fv[q] = (MODE == M_SPMV) ? 0.0 : __ldg(f + rq);
@@ -178,7 +187,7 @@ __device__ __forceinline__ double pat_resid_row(int m, int p, const double *sval
                                                 const double *__restrict__ f) {
     double xv[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) xv[k] = __ldg(x + m + soff[p * W + k]);
+    for (int k = 0; k < W; ++k) xv[k] = __ldg(at_off(x + m, soff[p * W + k]));
     const double fm = f[m];
     double sum = 0.0;
 #pragma unroll
