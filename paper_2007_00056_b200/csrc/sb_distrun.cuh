@@ -439,7 +439,7 @@ static void dist_pcg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
         each([&](RankDev &r, int64_t n) {
             launch_k(r.c, k_copy_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
                      static_cast<const double *>(r.c->kv[KZ]), r.c->kv[KP], static_cast<double *>(nullptr),
-                     static_cast<const double *>(r.c->kv[KR]), red_partial(r.c, 1));
+                     static_cast<const double *>(r.c->kv[KR]), red_partial(r.c, 1), X0{});
         });
         allreduce_logic(d, EP_PCG_RZ0);
         for (int j = 0; j < max_iters; ++j) {
@@ -452,8 +452,7 @@ static void dist_pcg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
             each([&](RankDev &r, int64_t n) {
                 launch_k(r.c, k_pcg_update, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n, r.c->kv[KX],
                          r.c->kv[KR], static_cast<const double *>(r.c->kv[KP]),
-                         static_cast<const double *>(r.c->kv[KAP]), red_partial(r.c, 1),
-                         static_cast<const double *>(nullptr), static_cast<double *>(nullptr), 0.0);
+                         static_cast<const double *>(r.c->kv[KAP]), red_partial(r.c, 1), X0{});
             });
             allreduce_logic(d, EP_PCG_RN);
             if (read_done(d)) break;
@@ -515,7 +514,7 @@ static void dist_bicg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
         each([&](RankDev &r, int64_t n) {
             launch_k(r.c, k_copy_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
                      static_cast<const double *>(r.c->kv[KR]), r.c->kv[KRBAR], r.c->kv[KP],
-                     static_cast<const double *>(r.c->kv[KR]), red_partial(r.c, 1));
+                     static_cast<const double *>(r.c->kv[KR]), red_partial(r.c, 1), X0{});
         });
         allreduce_logic(d, EP_BI_RHO0);
         for (int j = 0; j < max_iters && !read_done(d); ++j) {
@@ -529,7 +528,7 @@ static void dist_bicg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
             each([&](RankDev &r, int64_t n) {
                 launch_k(r.c, k_bi_s, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
                          static_cast<const double *>(r.c->kv[KR]), static_cast<const double *>(r.c->kv[KAPT]),
-                         r.c->kv[KS], red_partial(r.c, 1));
+                         r.c->kv[KS], red_partial(r.c, 1), X0{});
             });
             allreduce_logic(d, EP_BI_SN);
             half();
@@ -552,7 +551,7 @@ static void dist_bicg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
             each([&](RankDev &r, int64_t n) {
                 launch_k(r.c, k_bi_p, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
                          static_cast<const double *>(r.c->kv[KR]), r.c->kv[KP],
-                         static_cast<const double *>(r.c->kv[KAPT]), static_cast<const DevState *>(r.c->st));
+                         static_cast<const double *>(r.c->kv[KAPT]), static_cast<const DevState *>(r.c->st), X0{});
             });
         }
     }

@@ -1187,6 +1187,19 @@ __global__ void k_coarse_lu_exact(int n, const double *__restrict__ lu, const in
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < (n);      \
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
 
+// Optional by-product of a Krylov vector kernel: the next preconditioner's
+// first Jacobi sweep from 0 on level 0, x0_i = 0 + (w v_i)/a_ii for the vector
+// v the kernel produces (smoother.hpp:112-119), so that V-cycle skips its
+// zero-sweep kernel (harmless when the loop stops instead: x0 is unused).
+struct X0 {
+    const double *diag = nullptr;
+    double *x0 = nullptr;
+    double omega = 0.0;
+    __device__ __forceinline__ void put(int64_t i, double v) const {
+        if (x0) x0[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, v), diag[i]));
+    }
+};
+
 // x = 0, r = b, ||b||^2 (krylov.hpp:70-79, cycle.hpp:105-111)
 __global__ void k_init(int64_t n, const double *__restrict__ b, double *__restrict__ x,
                        double *__restrict__ r, Red red) {
@@ -1204,7 +1217,7 @@ __global__ void k_init(int64_t n, const double *__restrict__ b, double *__restri
 
 // dst = src; sum src*w  (PCG: p = z, rz = (r, z); BiCGStab: rbar = p = r, rho = (r, rbar))
 __global__ void k_copy_dot(int64_t n, const double *__restrict__ src, double *__restrict__ dst,
-                           double *__restrict__ dst2, const double *__restrict__ w, Red red) {
+                           double *__restrict__ dst2, const double *__restrict__ w, Red red, X0 z0) {
     pdl_wait();  // launched with PDL on the partitioned path
     double a[1] = {0.0};
     GRID_LOOP(i, n) {
@@ -1212,6 +1225,7 @@ __global__ void k_copy_dot(int64_t n, const double *__restrict__ src, double *__
         dst[i] = s;
         if (dst2) dst2[i] = s;
         a[0] += s * w[i];
+        z0.put(i, s);
     }
     finish_reduction<1>(red, a);
 }
@@ -1226,14 +1240,9 @@ __global__ void k_dot(int64_t n, const double *__restrict__ u, const double *__r
     finish_reduction<1>(red, a);
 }
 
-// PCG update (krylov.hpp:96-98): x += alpha p; r += (-alpha) Ap; ||r||^2
-// x0 != nullptr: also the next preconditioner's first Jacobi sweep from 0 on
-// level 0, x0 = 0 + (w r)/a_ii (smoother.hpp:112-119), so the V-cycle skips
-// its zero-sweep kernel (harmless when the loop stops here: x0 is unused).
+// PCG update (krylov.hpp:96-98): x += alpha p; r += (-alpha) Ap; ||r||^2 (+ x0 of z = M r)
 __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
-                             const double *__restrict__ p, const double *__restrict__ Ap, Red red,
-                             const double *__restrict__ diag = nullptr, double *__restrict__ x0 = nullptr,
-                             double omega = 0.0) {
+                             const double *__restrict__ p, const double *__restrict__ Ap, Red red, X0 z0) {
     pdl_wait();  // launched with PDL on the partitioned path
     double a[1] = {0.0};
     const DevState *st = red.st;
@@ -1244,7 +1253,7 @@ __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restri
             const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
             r[i] = ri;
             a[0] += ri * ri;
-            if (x0) x0[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, ri), diag[i]));
+            z0.put(i, ri);
         }
     }
     finish_reduction<1>(red, a);
@@ -1260,7 +1269,7 @@ __global__ void k_xpay(int64_t n, const double *__restrict__ z, double *__restri
 
 // BiCGStab s = r + (-alpha) Ap~; ||s||^2 (krylov.hpp:164-166)
 __global__ void k_bi_s(int64_t n, const double *__restrict__ r, const double *__restrict__ Apt,
-                       double *__restrict__ s, Red red) {
+                       double *__restrict__ s, Red red, X0 z0) {
     pdl_wait();  // launched with PDL on the partitioned path
     double a[1] = {0.0};
     const DevState *st = red.st;
@@ -1270,6 +1279,7 @@ __global__ void k_bi_s(int64_t n, const double *__restrict__ r, const double *__
             const double si = __dadd_rn(r[i], __dmul_rn(nalpha, Apt[i]));
             s[i] = si;
             a[0] += si * si;
+            z0.put(i, si);
         }
     }
     finish_reduction<1>(red, a);
@@ -1308,12 +1318,15 @@ __global__ void k_bi_update(int64_t n, double *__restrict__ x, double *__restric
 
 // p = r + beta (p - omega Ap~)  (krylov.hpp:204-205)
 __global__ void k_bi_p(int64_t n, const double *__restrict__ r, double *__restrict__ p,
-                       const double *__restrict__ Apt, const DevState *__restrict__ st) {
+                       const double *__restrict__ Apt, const DevState *__restrict__ st, X0 z0) {
     pdl_wait();  // launched with PDL on the partitioned path
     if (st->done) return;
     const double beta = st->beta, omega = st->omega;
-    GRID_LOOP(i, n)
-    p[i] = __dadd_rn(r[i], __dmul_rn(beta, __dsub_rn(p[i], __dmul_rn(omega, Apt[i]))));
+    GRID_LOOP(i, n) {
+        const double pi = __dadd_rn(r[i], __dmul_rn(beta, __dsub_rn(p[i], __dmul_rn(omega, Apt[i]))));
+        p[i] = pi;
+        z0.put(i, pi);
+    }
 }
 
 __global__ void k_fill(int64_t n, double *x, double v) {
@@ -1791,14 +1804,14 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
         precond(s1, r, z, false);
         cudaGraphConditionalHandle h_loop = new_handle(s1);
         k_copy_dot<<<vb, kVecThreads, 0, s1>>>(n, z, p, nullptr, r,
-                                              make_red(c, EP_PCG_RZ0, 1, nullptr, nullptr, conds({h_loop})));
+                                              make_red(c, EP_PCG_RZ0, 1, nullptr, nullptr, conds({h_loop})), X0{});
         CK(cudaGetLastError());
         add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
             launch_csr<M_SPMV, 1>(c, l0, s2, p, nullptr, Ap, 0.0, &c->st->done, make_red(c, EP_PCG_PAP, 1, p));
             cudaGraphConditionalHandle h_vc = new_handle(s2);
             k_pcg_update<<<vb, kVecThreads, 0, s2>>>(
                 n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})),
-                static_cast<const double *>(l0.diag), x0, cp ? cp->omega : 0.0);
+                X0{static_cast<const double *>(l0.diag), x0, cp ? cp->omega : 0.0});
             CK(cudaGetLastError());
             add_cond(c, s2, d2, h_vc, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
                 const Red rz = make_red(c, EP_PCG_RZ, 1, r);
@@ -1828,8 +1841,14 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
     double *r = c->kv[KR], *rbar = c->kv[KRBAR], *p = c->kv[KP], *pt = c->kv[KPT], *Apt = c->kv[KAPT],
            *sv = c->kv[KS], *stv = c->kv[KST], *Ast = c->kv[KAST];
     cudaStream_t s = c->stream;
-    auto precond = [c, cp, n](cudaStream_t ss, const double *in, double *out) {
-        if (cp) emit_vcycle(c, ss, *cp, 0, in, out, true);
+    // the kernels producing p and s also write the first level-0 sweep of the
+    // V-cycles that precondition them (X0)
+    const int L = static_cast<int>(c->L.size());
+    const bool fuse0 = cp && cp->pre >= 1 && L >= 2 && c->tail_from != 0;
+    const X0 x0p = fuse0 ? X0{static_cast<const double *>(l0.diag), zero_sweep_dest(c, *cp, 0, pt), cp->omega} : X0{};
+    const X0 x0s = fuse0 ? X0{static_cast<const double *>(l0.diag), zero_sweep_dest(c, *cp, 0, stv), cp->omega} : X0{};
+    auto precond = [c, cp, n, fuse0](cudaStream_t ss, const double *in, double *out) {
+        if (cp) emit_vcycle(c, ss, *cp, 0, in, out, true, fuse0);
         else CK(cudaMemcpyAsync(out, in, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToDevice, ss));
     };
     cudaGraph_t g = begin_capture(c);
@@ -1839,7 +1858,7 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
     add_cond(c, s, 0, h_pro, cudaGraphCondTypeIf, [&](cudaStream_t s1, int d1) {
         cudaGraphConditionalHandle h_loop = new_handle(s1);
         k_copy_dot<<<vb, kVecThreads, 0, s1>>>(n, r, rbar, p, r,
-                                              make_red(c, EP_BI_RHO0, 1, nullptr, nullptr, conds({h_loop})));
+                                              make_red(c, EP_BI_RHO0, 1, nullptr, nullptr, conds({h_loop})), x0p);
         CK(cudaGetLastError());
         add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
             // (the loop is only entered / re-entered with done == 0)
@@ -1847,7 +1866,7 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
             launch_csr<M_SPMV, 1>(c, l0, s2, pt, nullptr, Apt, 0.0, nullptr, make_red(c, EP_BI_DENOM, 1, rbar));
             cudaGraphConditionalHandle h_v2 = new_handle(s2);
             k_bi_s<<<vb, kVecThreads, 0, s2>>>(n, r, Apt, sv,
-                                              make_red(c, EP_BI_SN, 1, nullptr, nullptr, conds({h_v2})));
+                                              make_red(c, EP_BI_SN, 1, nullptr, nullptr, conds({h_v2})), x0s);
             CK(cudaGetLastError());
             k_bi_half<<<vb, kVecThreads, 0, s2>>>(n, x, pt, c->st);
             CK(cudaGetLastError());
@@ -1858,7 +1877,7 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
                 k_bi_update<<<vb, kVecThreads, 0, s3>>>(n, x, r, pt, stv, sv, Ast, rbar,
                                                        make_red(c, EP_BI_RN_RHO, 2));
                 CK(cudaGetLastError());
-                k_bi_p<<<vb, kVecThreads, 0, s3>>>(n, r, p, Apt, c->st);
+                k_bi_p<<<vb, kVecThreads, 0, s3>>>(n, r, p, Apt, c->st, x0p);
                 CK(cudaGetLastError());
             });
             k_set_cond<<<1, 1, 0, s2>>>(c->st, conds({h_loop}));
