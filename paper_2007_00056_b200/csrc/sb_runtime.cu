@@ -1798,18 +1798,18 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
     double *x0 = (cp && cp->pre >= 1 && L >= 2 && c->tail_from != 0) ? zero_sweep_dest(c, *cp, 0, z) : nullptr;
     cudaGraph_t g = begin_capture(c);
     cudaGraphConditionalHandle h_pro = new_handle(s);
-    k_init<<<vb, kVecThreads, 0, s>>>(n, b, x, r, make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_pro})));
+    launch_k(c, k_init, dim3(vb), dim3(kVecThreads), 0, s, n, b, x, r, make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_pro})));
     CK(cudaGetLastError());
     add_cond(c, s, 0, h_pro, cudaGraphCondTypeIf, [&](cudaStream_t s1, int d1) {
         precond(s1, r, z, false);
         cudaGraphConditionalHandle h_loop = new_handle(s1);
-        k_copy_dot<<<vb, kVecThreads, 0, s1>>>(n, z, p, nullptr, r,
+        launch_k(c, k_copy_dot, dim3(vb), dim3(kVecThreads), 0, s1, n, z, p, nullptr, r,
                                               make_red(c, EP_PCG_RZ0, 1, nullptr, nullptr, conds({h_loop})), X0{});
         CK(cudaGetLastError());
         add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
             launch_csr<M_SPMV, 1>(c, l0, s2, p, nullptr, Ap, 0.0, &c->st->done, make_red(c, EP_PCG_PAP, 1, p));
             cudaGraphConditionalHandle h_vc = new_handle(s2);
-            k_pcg_update<<<vb, kVecThreads, 0, s2>>>(
+            launch_k(c, k_pcg_update, dim3(vb), dim3(kVecThreads), 0, s2, 
                 n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})),
                 X0{static_cast<const double *>(l0.diag), x0, cp ? cp->omega : 0.0});
             CK(cudaGetLastError());
@@ -1820,10 +1820,10 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
                 precond(s3, r, z, x0 != nullptr);
                 c->final_red = nullptr;
                 if (!c->final_red_used) {
-                    k_dot<<<vb, kVecThreads, 0, s3>>>(n, r, z, nullptr, rz);
+                    launch_k(c, k_dot, dim3(vb), dim3(kVecThreads), 0, s3, n, r, z, nullptr, rz);
                     CK(cudaGetLastError());
                 }
-                k_xpay<<<vb, kVecThreads, 0, s3>>>(n, z, p, c->st);
+                launch_k(c, k_xpay, dim3(vb), dim3(kVecThreads), 0, s3, n, z, p, c->st);
                 CK(cudaGetLastError());
             });
         });
@@ -1853,11 +1853,11 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
     };
     cudaGraph_t g = begin_capture(c);
     cudaGraphConditionalHandle h_pro = new_handle(s);
-    k_init<<<vb, kVecThreads, 0, s>>>(n, b, x, r, make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_pro})));
+    launch_k(c, k_init, dim3(vb), dim3(kVecThreads), 0, s, n, b, x, r, make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_pro})));
     CK(cudaGetLastError());
     add_cond(c, s, 0, h_pro, cudaGraphCondTypeIf, [&](cudaStream_t s1, int d1) {
         cudaGraphConditionalHandle h_loop = new_handle(s1);
-        k_copy_dot<<<vb, kVecThreads, 0, s1>>>(n, r, rbar, p, r,
+        launch_k(c, k_copy_dot, dim3(vb), dim3(kVecThreads), 0, s1, n, r, rbar, p, r,
                                               make_red(c, EP_BI_RHO0, 1, nullptr, nullptr, conds({h_loop})), x0p);
         CK(cudaGetLastError());
         add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
@@ -1865,19 +1865,19 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
             precond(s2, p, pt);
             launch_csr<M_SPMV, 1>(c, l0, s2, pt, nullptr, Apt, 0.0, nullptr, make_red(c, EP_BI_DENOM, 1, rbar));
             cudaGraphConditionalHandle h_v2 = new_handle(s2);
-            k_bi_s<<<vb, kVecThreads, 0, s2>>>(n, r, Apt, sv,
+            launch_k(c, k_bi_s, dim3(vb), dim3(kVecThreads), 0, s2, n, r, Apt, sv,
                                               make_red(c, EP_BI_SN, 1, nullptr, nullptr, conds({h_v2})), x0s);
             CK(cudaGetLastError());
-            k_bi_half<<<vb, kVecThreads, 0, s2>>>(n, x, pt, c->st);
+            launch_k(c, k_bi_half, dim3(vb), dim3(kVecThreads), 0, s2, n, x, pt, c->st);
             CK(cudaGetLastError());
             add_cond(c, s2, d2, h_v2, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
                 precond(s3, sv, stv);
                 launch_csr<M_SPMV, 2>(c, l0, s3, stv, nullptr, Ast, 0.0, nullptr,
                                       make_red(c, EP_BI_AS, 2, nullptr, sv));
-                k_bi_update<<<vb, kVecThreads, 0, s3>>>(n, x, r, pt, stv, sv, Ast, rbar,
+                launch_k(c, k_bi_update, dim3(vb), dim3(kVecThreads), 0, s3, n, x, r, pt, stv, sv, Ast, rbar,
                                                        make_red(c, EP_BI_RN_RHO, 2));
                 CK(cudaGetLastError());
-                k_bi_p<<<vb, kVecThreads, 0, s3>>>(n, r, p, Apt, c->st, x0p);
+                launch_k(c, k_bi_p, dim3(vb), dim3(kVecThreads), 0, s3, n, r, p, Apt, c->st, x0p);
                 CK(cudaGetLastError());
             });
             k_set_cond<<<1, 1, 0, s2>>>(c->st, conds({h_loop}));
@@ -1896,7 +1896,7 @@ static cudaGraph_t build_amg(sb_ctx c, const Cyc &cp, const double *b, double *x
     cudaStream_t s = c->stream;
     cudaGraph_t g = begin_capture(c);
     cudaGraphConditionalHandle h_loop = new_handle(s);
-    k_init<<<vb, kVecThreads, 0, s>>>(n, b, x, nullptr,
+    launch_k(c, k_init, dim3(vb), dim3(kVecThreads), 0, s, n, b, x, nullptr,
                                       make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_loop})));
     CK(cudaGetLastError());
     add_cond(c, s, 0, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s1, int) {
