@@ -11,8 +11,9 @@
 // bound by x / f / x_new (24 B/row) instead of the matrix.
 //
 // Table layout (bytes, built on the host, copied into shared memory by every
-// CTA before the dependency wait): f64 val[np][W] | f64 diag[np] |
-// f64 rdiag[np] | int32 off[np][W] | uint8 len[np] (padded to 16).
+// CTA before the dependency wait): f64 val[np][WV] | f64 diag[np] |
+// f64 rdiag[np] | int32 off[np][WO] | uint8 len[np] (padded to 16); WV = W
+// rounded up to 2, WO = W rounded up to 4 (16-byte rows).
 
 constexpr int kPatThreads = 256;
 
@@ -31,28 +32,56 @@ __device__ __forceinline__ const double *at_off(const double *base, int off) {
 template <int W> struct PatRows { static constexpr int value = W <= 8 ? SB_PAT_ROWS : 1; };
 
 __host__ __device__ __forceinline__ size_t pat_table_bytes(int np, int w) {
-    return (static_cast<size_t>(np) * w * 12 + static_cast<size_t>(np) * 16 + static_cast<size_t>(np) + 15) & ~size_t(15);
+    const size_t wv = (w + 1) & ~1, wo = (w + 3) & ~3;
+    return (static_cast<size_t>(np) * (wv * 8 + wo * 4) + static_cast<size_t>(np) * 17 + 15) & ~size_t(15);
 }
 
 #ifndef SB_PAT_MINB_WIDE
 #define SB_PAT_MINB_WIDE 2
 #endif
-#ifndef SB_PAT_CHUNK
-#define SB_PAT_CHUNK 28
-#endif
 #ifndef SB_PAT_MINB
 #define SB_PAT_MINB 4
 #endif
-// wide rows (27-point levels) keep all W gathers in flight: more registers, 3 CTAs/SM
-template <int MODE, int NV, int W>
-__global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MINB_WIDE)
-    k_rowpat(int n, const uint8_t *__restrict__ pid, int np, const unsigned char *__restrict__ table,
-             const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
-             const int *skip, Aux aux, Red red) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double acc[NV > 0 ? NV : 1];
+// Pattern table view over the shared-memory copy. (Passing the table as a
+// kernel parameter, read with constant-cache loads, measured 5-15% slower: the
+// lanes of a warp index different patterns at grid boundaries.)
+template <int W> struct SmemTab {
+    static constexpr int WV = (W + 1) & ~1;  // value row stride (doubles): 16-byte rows
+    static constexpr int WO = (W + 3) & ~3;  // offset row stride (int32): 16-byte rows
+    const double *val, *dg, *ry;
+    const int32_t *off;
+    const uint8_t *len;
+    __device__ __forceinline__ double v(int p, int k) const { return val[p * WV + k]; }
+    __device__ __forceinline__ int o(int p, int k) const { return off[p * WO + k]; }
+    __device__ __forceinline__ double d(int p) const { return dg[p]; }
+    __device__ __forceinline__ double r(int p) const { return ry[p]; }
+    __device__ __forceinline__ int l(int p) const { return len[p]; }
+    // a whole row of offsets / values with 16-byte shared-memory loads (one
+    // wavefront per load when the warp's rows share the pattern)
+    __device__ __forceinline__ void offs(int p, int (&o)[W]) const {
+        const int32_t *b = off + p * WO;
 #pragma unroll
-    for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
+        for (int k = 0; k < W; k += 4) {
+            const int4 t = *reinterpret_cast<const int4 *>(b + k);
+            o[k] = t.x;
+            if (k + 1 < W) o[k + 1 < W ? k + 1 : 0] = t.y;
+            if (k + 2 < W) o[k + 2 < W ? k + 2 : 0] = t.z;
+            if (k + 3 < W) o[k + 3 < W ? k + 3 : 0] = t.w;
+        }
+    }
+    __device__ __forceinline__ void vals(int p, double (&v)[W]) const {
+        const double *b = val + p * WV;
+#pragma unroll
+        for (int k = 0; k < W; k += 2) {
+            const double2 t = *reinterpret_cast<const double2 *>(b + k);
+            v[k] = t.x;
+            if (k + 1 < W) v[k + 1 < W ? k + 1 : 0] = t.y;
+        }
+    }
+};
+
+template <int W>
+__device__ __forceinline__ SmemTab<W> smem_tab(unsigned char *smem, const unsigned char *table, int np) {
     const int tb = static_cast<int>(pat_table_bytes(np, W));
     {  // constant table: before the dependency wait (overlaps the predecessor's tail)
         const uint4 *src = reinterpret_cast<const uint4 *>(table);
@@ -60,12 +89,25 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
         for (int i = threadIdx.x; i < tb / 16; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
+    SmemTab<W> T;
+    T.val = reinterpret_cast<const double *>(smem);
+    T.dg = T.val + static_cast<size_t>(np) * SmemTab<W>::WV;
+    T.ry = T.dg + np;
+    T.off = reinterpret_cast<const int32_t *>(T.ry + np);
+    T.len = reinterpret_cast<const uint8_t *>(T.off + static_cast<size_t>(np) * SmemTab<W>::WO);
+    return T;
+}
+
+// wide rows (27-point levels) keep all W gathers in flight: more registers, 3 CTAs/SM
+template <int MODE, int NV, int W>
+__device__ __forceinline__ void rowpat_body(const SmemTab<W> &T, int n, const uint8_t *__restrict__ pid,
+                                            const double *__restrict__ x, const double *__restrict__ f,
+                                            double *__restrict__ out, double omega, const int *skip, Aux aux,
+                                            Red red) {
+    double acc[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
     constexpr int kPatRows = PatRows<W>::value;
-    const double *sval = reinterpret_cast<const double *>(smem);
-    const double *sdg = sval + static_cast<size_t>(np) * W;
-    const double *sry = sdg + np;
-    const int32_t *soff = reinterpret_cast<const int32_t *>(sry + np);
-    const uint8_t *slen = reinterpret_cast<const uint8_t *>(soff + static_cast<size_t>(np) * W);
     const int stride = gridDim.x * kPatThreads * kPatRows;
     // the pattern bytes of the next iteration are loaded one iteration ahead,
     // so the x gathers do not wait behind a dependent DRAM load; the first
@@ -78,8 +120,8 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
     }
     pdl_wait();
     if constexpr (W > 8 && (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV)) {
-        // wide rows (27-point levels): one row per thread, the gathers in chunks
-        // of SB_PAT_CHUNK (registers for more resident warps), sums in slot order
+        // wide rows (27-point levels): one row per thread, all W gathers in
+        // flight, sums in slot order
         if (!(skip && *skip)) {
             for (int base = blockIdx.x * kPatThreads; base < n; base += stride) {
                 if (base + stride >= n) pdl_trigger();
@@ -91,26 +133,27 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
                 const double fi = (MODE == M_SPMV) ? 0.0 : __ldg(f + rq);
                 const double xi = __ldg(xr);
                 double sum = 0.0;
+                {
+                    int o[W];
+                    T.offs(p, o);
+                    double xv[W];
 #pragma unroll
-                for (int c0 = 0; c0 < W; c0 += SB_PAT_CHUNK) {
-                    double xv[SB_PAT_CHUNK];
+                    for (int k = 0; k < W; ++k) xv[k] = __ldg(at_off(xr, o[k]));
+                    double v[W];
+                    T.vals(p, v);
 #pragma unroll
-                    for (int k = 0; k < SB_PAT_CHUNK; ++k)
-                        if (c0 + k < W) xv[k] = __ldg(at_off(xr, soff[p * W + c0 + k]));
-#pragma unroll
-                    for (int k = 0; k < SB_PAT_CHUNK; ++k)
-                        if (c0 + k < W) sum = __dadd_rn(sum, __dmul_rn(sval[p * W + c0 + k], xv[k]));
+                    for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], xv[k]));
                 }
-                const int len = slen[p];
+                const int len = T.l(p);
                 if (len < W && !isfinite(xi)) {  // exact replay for a non-finite own x (see below)
                     sum = 0.0;
-                    for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(sval[p * W + k], __ldg(xr + soff[p * W + k])));
+                    for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(T.v(p, k), __ldg(xr + T.o(p, k))));
                 }
                 if (row < n) {
                     double o;
                     if constexpr (MODE == M_SPMV) o = sum;
                     else if constexpr (MODE == M_RESID) o = __dsub_rn(fi, sum);
-                    else o = __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), sdg[p], sry[p]));
+                    else o = __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), T.d(p), T.r(p)));
                     out[row] = o;
                     if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fi : red.w0[row]) : o);
                     if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
@@ -134,9 +177,11 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
             for (int q = 0; q < kPatRows; ++q) {
                 const int rq = row[q] < n ? row[q] : n - 1;
                 const double *xr = x + rq;
+                int o[W];
+                T.offs(p[q], o);
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
-                    const int off = soff[p[q] * W + k];
+                    const int off = o[k];
                     if constexpr (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV) xv[q][k] = __ldg(at_off(xr, off));
                     else xv[q][k] = xval<MODE, false>(rq + off, x, f, aux, omega);
                 }
@@ -146,18 +191,20 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
 #pragma unroll
             for (int q = 0; q < kPatRows; ++q) {
                 if (row[q] >= n) continue;
-                const int len = slen[p[q]];
+                const int len = T.l(p[q]);
                 // Padding slots hold value +0.0 at offset 0 (the row itself): 0 * x_i
                 // is +-0 and sum + (+-0) == sum bit for bit (sum is never -0), so
                 // the unmasked sum equals the reference's unless x_i is inf / NaN
                 // (0 * inf = NaN); only then replay the row with masked slots.
+                double v[W];
+                T.vals(p[q], v);
                 double sum = 0.0;
 #pragma unroll
-                for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(sval[p[q] * W + k], xv[q][k]));
+                for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], xv[q][k]));
                 if (len < W && !isfinite(xv[q][W - 1])) {
                     sum = 0.0;
 #pragma unroll
-                    for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(sval[p[q] * W + k], xv[q][k]), k < len);
+                    for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(v[k], xv[q][k]), k < len);
                 }
                 double o;
                 if constexpr (MODE == M_SPMV) {
@@ -165,7 +212,7 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
                 } else if constexpr (MODE == M_RESID) {
                     o = __dsub_rn(fv[q], sum);
                 } else {
-                    o = __dadd_rn(xo[q], div_rn(__dmul_rn(omega, __dsub_rn(fv[q], sum)), sdg[p[q]], sry[p[q]]));
+                    o = __dadd_rn(xo[q], div_rn(__dmul_rn(omega, __dsub_rn(fv[q], sum)), T.d(p[q]), T.r(p[q])));
                 }
                 out[row[q]] = o;
                 if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fv[q] : red.w0[row[q]]) : o);
@@ -176,27 +223,40 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
 }
 
+template <int MODE, int NV, int W>
+__global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MINB_WIDE)
+    k_rowpat(int n, const uint8_t *__restrict__ pid, int np, const unsigned char *__restrict__ table,
+             const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
+             const int *skip, Aux aux, Red red) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const SmemTab<W> T = smem_tab<W>(smem, table, np);
+    rowpat_body<MODE, NV, W>(T, n, pid, x, f, out, omega, skip, aux, red);
+}
+
 // Residual + restriction fused for a row-pattern level (one launch and no r
 // vector): thread c evaluates r_m = f_m - A_m x for the members m0 < m1 of
 // coarse row c in the reference's order and writes f_c = (0 + r_m0) + r_m1
 // (csr.hpp:267-274 then the unit-P spmv_transpose, csr.hpp:232-239); with
 // xc0, also the coarse level's first sweep from 0, x0_c = 0 + (w f_c) / a_cc.
 template <int W>
-__device__ __forceinline__ double pat_resid_row(int m, int p, const double *sval, const int32_t *soff,
-                                                const uint8_t *slen, const double *__restrict__ x,
+__device__ __forceinline__ double pat_resid_row(int m, int p, const SmemTab<W> &T, const double *__restrict__ x,
                                                 const double *__restrict__ f) {
+    int o[W];
+    T.offs(p, o);
     double xv[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) xv[k] = __ldg(at_off(x + m, soff[p * W + k]));
+    for (int k = 0; k < W; ++k) xv[k] = __ldg(at_off(x + m, o[k]));
     const double fm = f[m];
+    double v[W];
+    T.vals(p, v);
     double sum = 0.0;
 #pragma unroll
-    for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(sval[p * W + k], xv[k]));
-    const int len = slen[p];
+    for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], xv[k]));
+    const int len = T.l(p);
     if (len < W && !isfinite(xv[W - 1])) {  // see k_rowpat: exact replay for a non-finite own x
         sum = 0.0;
 #pragma unroll
-        for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(sval[p * W + k], xv[k]), k < len);
+        for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(v[k], xv[k]), k < len);
     }
     return __dsub_rn(fm, sum);
 }
@@ -208,19 +268,7 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
                          const double *__restrict__ f, double *__restrict__ fc, const double *__restrict__ dc,
                          double *__restrict__ xc0, double omega) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int tb = static_cast<int>(pat_table_bytes(np, W));
-    {
-        const uint4 *src = reinterpret_cast<const uint4 *>(table);
-        uint4 *dst = reinterpret_cast<uint4 *>(smem);
-        for (int i = threadIdx.x; i < tb / 16; i += blockDim.x) dst[i] = src[i];
-    }
-    __syncthreads();
-    const double *sval = reinterpret_cast<const double *>(smem);
-    const double *sdg = sval + static_cast<size_t>(np) * W;
-    const double *sry = sdg + np;
-    const int32_t *soff = reinterpret_cast<const int32_t *>(sry + np);
-    const uint8_t *slen = reinterpret_cast<const uint8_t *>(soff + static_cast<size_t>(np) * W);
-    (void)sdg;
+    const SmemTab<W> T = smem_tab<W>(smem, table, np);
     const int c0 = blockIdx.x * blockDim.x + threadIdx.x;
     int2 mm = make_int2(0, -1);
     int p0 = 0, p1 = 0;
@@ -239,8 +287,8 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
             if (mm.y >= 0) p1 = pid[mm.y];
             if (xc0) d = dc[c];
         }
-        double s = __dadd_rn(0.0, pat_resid_row<W>(mm.x, p0, sval, soff, slen, x, f));
-        if (mm.y >= 0) s = __dadd_rn(s, pat_resid_row<W>(mm.y, p1, sval, soff, slen, x, f));
+        double s = __dadd_rn(0.0, pat_resid_row<W>(mm.x, p0, T, x, f));
+        if (mm.y >= 0) s = __dadd_rn(s, pat_resid_row<W>(mm.y, p1, T, x, f));
         fc[c] = s;
         if (xc0) xc0[c] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), d));
     }

@@ -2024,23 +2024,24 @@ static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
     const int np = static_cast<int>(rep.size());
     const size_t tb = pat_table_bytes(np, w);
     std::vector<unsigned char> tab(tb, 0);
+    const int wv = (w + 1) & ~1, wo = (w + 3) & ~3;  // 16-byte table rows (SmemTab)
     auto *val = reinterpret_cast<double *>(tab.data());
-    auto *dg = val + static_cast<size_t>(np) * w;
+    auto *dg = val + static_cast<size_t>(np) * wv;
     auto *ry = dg + np;
     auto *off = reinterpret_cast<int32_t *>(ry + np);
-    auto *len = reinterpret_cast<uint8_t *>(off + static_cast<size_t>(np) * w);
+    auto *len = reinterpret_cast<uint8_t *>(off + static_cast<size_t>(np) * wo);
     for (int q = 0; q < np; ++q) {
         const int64_t r = rep[static_cast<size_t>(q)];
         const int lq = static_cast<int>(A.rp[r + 1] - A.rp[r]);
         len[q] = static_cast<uint8_t>(lq);
         dg[q] = 0.0;
         for (int e = 0; e < w; ++e) {
-            off[q * w + e] = 0;  // padding: the row itself, value +0.0 (see k_rowpat)
-            val[q * w + e] = 0.0;
+            off[q * wo + e] = 0;  // padding: the row itself, value +0.0 (see k_rowpat)
+            val[q * wv + e] = 0.0;
             if (e < lq) {
-                off[q * w + e] = static_cast<int32_t>(static_cast<int64_t>(A.ci[A.rp[r] + e]) - r);
-                val[q * w + e] = A.v[A.rp[r] + e];
-                if (off[q * w + e] == 0) dg[q] = val[q * w + e];
+                off[q * wo + e] = static_cast<int32_t>(static_cast<int64_t>(A.ci[A.rp[r] + e]) - r);
+                val[q * wv + e] = A.v[A.rp[r] + e];
+                if (off[q * wo + e] == 0) dg[q] = val[q * wv + e];
             }
         }
         const double ad = std::fabs(dg[q]);
