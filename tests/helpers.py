@@ -46,3 +46,28 @@ def random_sparse(sp, n, seed, density=0.2, mirror=True):
 def rel(a, b):
     nb = np.linalg.norm(b)
     return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+def stencil27_varied(sp, nx, ny, nz, seed=0):
+    """27-point operator on an nx*ny*nz grid whose 26 off-diagonal values differ by
+    direction (and the diagonal dominates), neighbours outside the grid dropped."""
+    rng = np.random.default_rng(seed)
+    w = -rng.uniform(0.5, 1.5, (3, 3, 3))
+    w[1, 1, 1] = 30.0
+    n = nx * ny * nz
+    iz, iy, ix = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    rows, cols, vals = [], [], []
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                jx, jy, jz = ix + dx, iy + dy, iz + dz
+                ok = (jx >= 0) & (jx < nx) & (jy >= 0) & (jy < ny) & (jz >= 0) & (jz < nz)
+                rows.append(((iz * ny + iy) * nx + ix)[ok])
+                cols.append(((jz * ny + jy) * nx + jx)[ok])
+                vals.append(np.full(ok.sum(), w[dz + 1, dy + 1, dx + 1]))
+    r, c, v = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+    order = np.lexsort((c, r))
+    r, c, v = r[order], c[order], v[order]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, r + 1, 1)
+    return sp.CsrMatrix(n, n, np.cumsum(rp), c.astype(np.int32), v)

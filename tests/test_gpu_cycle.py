@@ -103,3 +103,19 @@ def test_vcycle_bitexact_with_exact_coarse(sp, port, tail_rows, monkeypatch):
     o = port.hierarchy(A, 500, 40)
     f = sp.rhs_random(A.nrows(), 3)
     assert np.array_equal(sp.vcycle(h, 0, f, np.zeros(A.nrows()), _cp(sp)), o.vcycle(f, np.zeros(A.nrows())))
+
+
+@pytest.mark.parametrize("tail_rows", ["0", "8192"])
+def test_vcycle_27point_varied_bitexact(sp, port, tail_rows, monkeypatch):
+    # direction-weighted 27-point operator (wide row patterns on every level);
+    # with the reference-order coarse solve the whole cycle is bitwise the
+    # reference's
+    from helpers import stencil27_varied
+    monkeypatch.setenv("SB_TAIL_ROWS", tail_rows)
+    for dims in [(96, 6, 5), (128, 4, 4)]:
+        A = stencil27_varied(sp, *dims, seed=3)
+        h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40, coarse_target=64), coarse_exact=True)
+        o = port.hierarchy(A, 64, 40)
+        f = sp.rhs_random(A.nrows(), 5)
+        assert np.array_equal(sp.vcycle(h, 0, f, np.zeros(A.nrows()), _cp(sp)), o.vcycle(f, np.zeros(A.nrows())))
+        assert np.array_equal(sp.make_amg_preconditioner(h, _cp(sp)).apply(f), o.vcycle(f, np.zeros(A.nrows())))

@@ -140,3 +140,19 @@ def test_spmv_nonfinite_inputs(sp, oracle_best, rpat, monkeypatch):
         assert np.array_equal(got, want, equal_nan=True)
         assert np.array_equal(np.signbit(got), np.signbit(want))
         assert np.array_equal(sp.residual(A, x, f), oracle_best.residual(A, x, f), equal_nan=True)
+
+
+@pytest.mark.parametrize("dims", [(100, 4, 3), (128, 5, 4), (96, 3, 2)])
+def test_27point_varied_bitexact(sp, oracle_best, dims):
+    # 27-point rows (the wide row-pattern path, W = 28) with a different value
+    # per direction: any slip in slot order or value/column pairing changes bits
+    from helpers import stencil27_varied
+    A = stencil27_varied(sp, *dims, seed=sum(dims))
+    x = np.random.default_rng(11).uniform(-1, 1, A.ncols())
+    f = np.random.default_rng(12).uniform(-1, 1, A.nrows())
+    assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x))
+    assert np.array_equal(sp.residual(A, x, f), oracle_best.residual(A, x, f))
+    jac = sp.SmootherKind.weighted_jacobi()
+    assert np.array_equal(sp.smooth(jac, A, x, f, 3), oracle_best.jacobi(A, 2.0 / 3.0, x, f, 3))
+    x[[40, 41, 200]] = [np.inf, np.nan, -np.inf]  # non-finite values inside interior rows
+    assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x), equal_nan=True)

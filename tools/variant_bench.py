@@ -12,7 +12,7 @@ sys.path.insert(0, %r)
 import numpy as np, torch
 from paper_2007_00056_b200 import sparsh as sp, _lib
 wl = os.environ.get("VB_WL", "C2")
-A = {"C2": lambda: sp.poisson3d(128), "C1": lambda: sp.poisson2d(1024, 1024), "C3": lambda: sp.aniso3d(256), "C4": lambda: sp.convdiff3d(256, 256, 256, 1.0, 100.0, 1.0, 1.0), "P27": lambda: sp.poisson3d_27(128)}[wl]()
+A = {"C2": lambda: sp.poisson3d(128), "C1": lambda: sp.poisson2d(1024, 1024), "C3": lambda: sp.aniso3d(256), "C4": lambda: sp.convdiff3d(256, 256, 256, 1.0, 100.0, 1.0, 1.0), "P27": lambda: sp.poisson3d_27(128), "P27_256": lambda: sp.poisson3d_27(256)}[wl]()
 cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40)
 h = sp.Hierarchy(A, cfg); ctx = h.ctx(); L = _lib.lib()
 cp = sp.CycleParams.from_config(cfg)._abi()
