@@ -129,7 +129,9 @@ def run_c5(args, wl):
                        "parallelism": "single GPU"},
             "roofline": {"bound": "hbm", "kernel": "k_rowpat<JACOBI> (L0 Jacobi sweep)", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "algorithmic_bytes_per_launch": jac_bytes, "launch_ms": avg.value},
+                         # C5p's operator is the 27-point 256^3 of profiles/ncu_summary_P27_256.json
+                         "traffic": load_traffic("P27_256") if wl == "C5p" else None,
+                         "algorithmic_bytes_per_launch": jac_bytes, "launch_ms": avg.value},
             "e2e": {"value": statistics.mean(e2e), "unit": "s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
             "cpu_baseline": {"value": None, "unit": "s", "cores": 0, "kind": "reference",
                              "sample": "unavailable: the reference's int32 CSR offsets cannot hold nnz = 3.6e9"},
