@@ -98,9 +98,69 @@ __device__ __forceinline__ SmemTab<W> smem_tab(unsigned char *smem, const unsign
     return T;
 }
 
+// The level's most frequent pattern, passed by value as a kernel parameter:
+// a warp whose rows all have it reads offsets and values as constant-bank
+// operands (no shared-memory loads; the table reads otherwise cost as many L1
+// wavefronts as the x gathers on 27-point levels).
+template <int W> struct MainPat {
+    double v[W];
+    double d, r;
+    int o[W];
+    int p, len;
+};
+template <int W> struct SrcMain {  // row source: the main pattern (kernel parameter)
+    const MainPat<W> &m;
+    __device__ __forceinline__ void offs(int (&o)[W]) const {
+#pragma unroll
+        for (int k = 0; k < W; ++k) o[k] = m.o[k];
+    }
+    __device__ __forceinline__ void vals(double (&v)[W]) const {
+#pragma unroll
+        for (int k = 0; k < W; ++k) v[k] = m.v[k];
+    }
+    __device__ __forceinline__ double v1(int k) const { return m.v[k]; }
+    __device__ __forceinline__ int o1(int k) const { return m.o[k]; }
+    __device__ __forceinline__ double d() const { return m.d; }
+    __device__ __forceinline__ double r() const { return m.r; }
+    __device__ __forceinline__ int l() const { return m.len; }
+};
+template <int W> struct SrcTab {  // row source: pattern p of the shared-memory table
+    const SmemTab<W> &T;
+    int p;
+    __device__ __forceinline__ void offs(int (&o)[W]) const { T.offs(p, o); }
+    __device__ __forceinline__ void vals(double (&v)[W]) const { T.vals(p, v); }
+    __device__ __forceinline__ double v1(int k) const { return T.v(p, k); }
+    __device__ __forceinline__ int o1(int k) const { return T.o(p, k); }
+    __device__ __forceinline__ double d() const { return T.d(p); }
+    __device__ __forceinline__ double r() const { return T.r(p); }
+    __device__ __forceinline__ int l() const { return T.l(p); }
+};
+
+// sum_k v_k x[i + o_k] of one wide row in slot order (padding slots add +0.0;
+// replayed with masked slots when the row's own x is not finite, see below)
+template <int W, typename S>
+__device__ __forceinline__ double wide_row_sum(const S &src, const double *__restrict__ xr, double xi) {
+    int o[W];
+    src.offs(o);
+    double xv[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) xv[k] = __ldg(at_off(xr, o[k]));
+    double v[W];
+    src.vals(v);
+    double sum = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], xv[k]));
+    const int len = src.l();
+    if (len < W && !isfinite(xi)) {
+        sum = 0.0;
+        for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(src.v1(k), __ldg(xr + src.o1(k))));
+    }
+    return sum;
+}
+
 // wide rows (27-point levels) keep all W gathers in flight: more registers, 3 CTAs/SM
 template <int MODE, int NV, int W>
-__device__ __forceinline__ void rowpat_body(const SmemTab<W> &T, int n, const uint8_t *__restrict__ pid,
+__device__ __forceinline__ void rowpat_body(const SmemTab<W> &T, const MainPat<W> &mp, int n, const uint8_t *__restrict__ pid,
                                             const double *__restrict__ x, const double *__restrict__ f,
                                             double *__restrict__ out, double omega, const int *skip, Aux aux,
                                             Red red) {
@@ -132,28 +192,21 @@ __device__ __forceinline__ void rowpat_body(const SmemTab<W> &T, int n, const ui
                 const double *xr = x + rq;
                 const double fi = (MODE == M_SPMV) ? 0.0 : __ldg(f + rq);
                 const double xi = __ldg(xr);
-                double sum = 0.0;
-                {
-                    int o[W];
-                    T.offs(p, o);
-                    double xv[W];
-#pragma unroll
-                    for (int k = 0; k < W; ++k) xv[k] = __ldg(at_off(xr, o[k]));
-                    double v[W];
-                    T.vals(p, v);
-#pragma unroll
-                    for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], xv[k]));
-                }
-                const int len = T.l(p);
-                if (len < W && !isfinite(xi)) {  // exact replay for a non-finite own x (see below)
-                    sum = 0.0;
-                    for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(T.v(p, k), __ldg(xr + T.o(p, k))));
+                double sum, dg, ry;
+                if (__all_sync(0xffffffffu, p == mp.p)) {
+                    sum = wide_row_sum<W>(SrcMain<W>{mp}, xr, xi);
+                    dg = mp.d;
+                    ry = mp.r;
+                } else {
+                    sum = wide_row_sum<W>(SrcTab<W>{T, p}, xr, xi);
+                    dg = T.d(p);
+                    ry = T.r(p);
                 }
                 if (row < n) {
                     double o;
                     if constexpr (MODE == M_SPMV) o = sum;
                     else if constexpr (MODE == M_RESID) o = __dsub_rn(fi, sum);
-                    else o = __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), T.d(p), T.r(p)));
+                    else o = __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), dg, ry));
                     out[row] = o;
                     if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fi : red.w0[row]) : o);
                     if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
@@ -172,52 +225,61 @@ __device__ __forceinline__ void rowpat_body(const SmemTab<W> &T, int n, const ui
                 const int r = row[q] + stride;
                 pn[q] = pid[r < n ? r : n - 1];
             }
-            double fv[kPatRows], xo[kPatRows];  // rhs and own iterate, loaded with the gathers
+            // one iteration with the rows' table source: the main pattern for
+            // a warp whose rows all have it, else the shared-memory table
+            auto iter = [&](auto src) {
+                double fv[kPatRows], xo[kPatRows];  // rhs and own iterate, loaded with the gathers
 #pragma unroll
-            for (int q = 0; q < kPatRows; ++q) {
-                const int rq = row[q] < n ? row[q] : n - 1;
-                const double *xr = x + rq;
-                int o[W];
-                T.offs(p[q], o);
+                for (int q = 0; q < kPatRows; ++q) {
+                    const int rq = row[q] < n ? row[q] : n - 1;
+                    const double *xr = x + rq;
+                    int o[W];
+                    src(q).offs(o);
 #pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    const int off = o[k];
-                    if constexpr (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV) xv[q][k] = __ldg(at_off(xr, off));
-                    else xv[q][k] = xval<MODE, false>(rq + off, x, f, aux, omega);
+                    for (int k = 0; k < W; ++k) {
+                        const int off = o[k];
+                        if constexpr (MODE == M_JACOBI || MODE == M_RESID || MODE == M_SPMV) xv[q][k] = __ldg(at_off(xr, off));
+                        else xv[q][k] = xval<MODE, false>(rq + off, x, f, aux, omega);
+                    }
+                    fv[q] = (MODE == M_SPMV) ? 0.0 : __ldg(f + rq);
+                    xo[q] = (MODE >= M_JACOBI) ? xval<MODE, false>(rq, x, f, aux, omega) : 0.0;
                 }
-                fv[q] = (MODE == M_SPMV) ? 0.0 : __ldg(f + rq);
-                xo[q] = (MODE >= M_JACOBI) ? xval<MODE, false>(rq, x, f, aux, omega) : 0.0;
-            }
 #pragma unroll
-            for (int q = 0; q < kPatRows; ++q) {
-                if (row[q] >= n) continue;
-                const int len = T.l(p[q]);
-                // Padding slots hold value +0.0 at offset 0 (the row itself): 0 * x_i
-                // is +-0 and sum + (+-0) == sum bit for bit (sum is never -0), so
-                // the unmasked sum equals the reference's unless x_i is inf / NaN
-                // (0 * inf = NaN); only then replay the row with masked slots.
-                double v[W];
-                T.vals(p[q], v);
-                double sum = 0.0;
+                for (int q = 0; q < kPatRows; ++q) {
+                    if (row[q] >= n) continue;
+                    const int len = src(q).l();
+                    // Padding slots hold value +0.0 at offset 0 (the row itself): 0 * x_i
+                    // is +-0 and sum + (+-0) == sum bit for bit (sum is never -0), so
+                    // the unmasked sum equals the reference's unless x_i is inf / NaN
+                    // (0 * inf = NaN); only then replay the row with masked slots.
+                    double v[W];
+                    src(q).vals(v);
+                    double sum = 0.0;
 #pragma unroll
-                for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], xv[q][k]));
-                if (len < W && !isfinite(xv[q][W - 1])) {
-                    sum = 0.0;
+                    for (int k = 0; k < W; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], xv[q][k]));
+                    if (len < W && !isfinite(xv[q][W - 1])) {
+                        sum = 0.0;
 #pragma unroll
-                    for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(v[k], xv[q][k]), k < len);
+                        for (int k = 0; k < W; ++k) add_if(sum, __dmul_rn(v[k], xv[q][k]), k < len);
+                    }
+                    double o;
+                    if constexpr (MODE == M_SPMV) {
+                        o = sum;
+                    } else if constexpr (MODE == M_RESID) {
+                        o = __dsub_rn(fv[q], sum);
+                    } else {
+                        o = __dadd_rn(xo[q], div_rn(__dmul_rn(omega, __dsub_rn(fv[q], sum)), src(q).d(), src(q).r()));
+                    }
+                    out[row[q]] = o;
+                    if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fv[q] : red.w0[row[q]]) : o);
+                    if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row[q]] : o);
                 }
-                double o;
-                if constexpr (MODE == M_SPMV) {
-                    o = sum;
-                } else if constexpr (MODE == M_RESID) {
-                    o = __dsub_rn(fv[q], sum);
-                } else {
-                    o = __dadd_rn(xo[q], div_rn(__dmul_rn(omega, __dsub_rn(fv[q], sum)), T.d(p[q]), T.r(p[q])));
-                }
-                out[row[q]] = o;
-                if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fv[q] : red.w0[row[q]]) : o);
-                if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row[q]] : o);
-            }
+            };
+            bool uni = true;
+#pragma unroll
+            for (int q = 0; q < kPatRows; ++q) uni = uni && p[q] == mp.p;
+            if (__all_sync(0xffffffffu, uni)) iter([&](int) { return SrcMain<W>{mp}; });
+            else iter([&](int q) { return SrcTab<W>{T, p[q]}; });
         }
     }
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
@@ -226,11 +288,11 @@ __device__ __forceinline__ void rowpat_body(const SmemTab<W> &T, int n, const ui
 template <int MODE, int NV, int W>
 __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MINB_WIDE)
     k_rowpat(int n, const uint8_t *__restrict__ pid, int np, const unsigned char *__restrict__ table,
-             const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
-             const int *skip, Aux aux, Red red) {
+             const __grid_constant__ MainPat<W> mp, const double *__restrict__ x, const double *__restrict__ f,
+             double *__restrict__ out, double omega, const int *skip, Aux aux, Red red) {
     extern __shared__ __align__(16) unsigned char smem[];
     const SmemTab<W> T = smem_tab<W>(smem, table, np);
-    rowpat_body<MODE, NV, W>(T, n, pid, x, f, out, omega, skip, aux, red);
+    rowpat_body<MODE, NV, W>(T, mp, n, pid, x, f, out, omega, skip, aux, red);
 }
 
 // Residual + restriction fused for a row-pattern level (one launch and no r

@@ -1363,6 +1363,12 @@ struct DevLevel {
     double *rdict = nullptr;
     // row-pattern layout (pat = 1): one pattern index per row + the pattern table
     int pat = 0, pat_np = 0, pat_w = 0, pat_grid = 0;
+    // the most frequent pattern (k_rowpat's MainPat parameter): id, len, a_ii,
+    // RN(1/a_ii), values and offsets (W slots, padding included)
+    int main_p = -1, main_len = 0;
+    double main_d = 0.0, main_r = 0.0;
+    std::vector<double> main_v;
+    std::vector<int> main_o;
     size_t pat_tb = 0;
     const uint8_t *pat_id = nullptr;
     const unsigned char *pat_table = nullptr;
@@ -1481,6 +1487,11 @@ static CondSet conds(std::initializer_list<cudaGraphConditionalHandle> hs) {
 
 // ---- launchers (each counts the kernels it emits) -------------------------------
 
+static const bool c_main_off = [] {  // SB_MAIN_PAT=0: every warp reads the shared-memory table (A/B only)
+    const char *e = std::getenv("SB_MAIN_PAT");
+    return e && std::atoi(e) == 0;
+}();
+
 // Launch with programmatic dependent launch (the kernel calls pdl_wait()
 // before touching its predecessor's outputs) when the context enables it.
 template <typename... KArgs, typename... Args>
@@ -1543,11 +1554,25 @@ static void launch_sell_f(sb_ctx c, const DevLevel &l, cudaStream_t s, const dou
     }
 }
 
+template <int W> static MainPat<W> main_pat(const DevLevel &l) {
+    MainPat<W> m;
+    std::memset(&m, 0, sizeof(m));
+    m.p = c_main_off ? -1 : l.main_p;
+    m.len = l.main_len;
+    m.d = l.main_d;
+    m.r = l.main_r;
+    for (int k = 0; k < W && k < static_cast<int>(l.main_v.size()); ++k) {
+        m.v[k] = l.main_v[static_cast<size_t>(k)];
+        m.o[k] = l.main_o[static_cast<size_t>(k)];
+    }
+    return m;
+}
+
 template <int MODE, int NV, int W>
 static void launch_pat_w(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
                          double *out, double omega, const int *skip, const Red &red, Aux aux) {
     launch_k(c, k_rowpat<MODE, NV, W>, dim3(l.pat_grid), dim3(kPatThreads), l.pat_tb, s, static_cast<int>(l.n),
-             l.pat_id, l.pat_np, l.pat_table, x, f, out, omega, skip, aux, red);
+             l.pat_id, l.pat_np, l.pat_table, main_pat<W>(l), x, f, out, omega, skip, aux, red);
 }
 
 template <int MODE, int NV>
@@ -2046,6 +2071,17 @@ static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
         }
         const double ad = std::fabs(dg[q]);
         ry[q] = (ad >= std::ldexp(1.0, -100) && ad <= std::ldexp(1.0, 100)) ? 1.0 / dg[q] : 0.0;
+    }
+    {  // the most frequent pattern goes to the kernels as a parameter (MainPat)
+        std::vector<int64_t> cnt(static_cast<size_t>(np), 0);
+        for (uint8_t q : pid) ++cnt[q];
+        const int q = static_cast<int>(std::max_element(cnt.begin(), cnt.end()) - cnt.begin());
+        D.main_p = q;
+        D.main_len = len[q];
+        D.main_d = dg[q];
+        D.main_r = ry[q];
+        D.main_v.assign(val + static_cast<size_t>(q) * wv, val + static_cast<size_t>(q) * wv + w);
+        D.main_o.assign(off + static_cast<size_t>(q) * wo, off + static_cast<size_t>(q) * wo + w);
     }
     auto *dp = dalloc<uint8_t>(c, A.n + 16);
     CK(cudaMemcpy(dp, pid.data(), pid.size(), cudaMemcpyHostToDevice));
