@@ -37,7 +37,7 @@ __host__ __device__ __forceinline__ size_t pat_table_bytes(int np, int w) {
 }
 
 #ifndef SB_PAT_MINB_WIDE
-#define SB_PAT_MINB_WIDE 2
+#define SB_PAT_MINB_WIDE 3
 #endif
 #ifndef SB_PAT_MINB
 #define SB_PAT_MINB 4

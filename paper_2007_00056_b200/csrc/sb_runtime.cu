@@ -2836,8 +2836,18 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
         }
         if (l.pat) {
             occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowpat<M_JACOBI, 0, 8>, kPatThreads, l.pat_tb));
-            const int64_t need = (l.n + kPatThreads * 2 - 1) / (kPatThreads * 2);
+            // resident CTAs of this level's kernel (wide rows: fewer, 1 row per thread)
+            auto occ_of = [&](auto kern) {
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPatThreads, l.pat_tb));
+            };
+            switch (l.pat_w) {
+            case 16: occ_of(k_rowpat<M_JACOBI, 0, 16>); break;
+            case 28: occ_of(k_rowpat<M_JACOBI, 0, 28>); break;
+            case 32: occ_of(k_rowpat<M_JACOBI, 0, 32>); break;
+            default: occ_of(k_rowpat<M_JACOBI, 0, 8>);
+            }
+            const int rows_it = kPatThreads * (l.pat_w <= 8 ? 2 : 1);
+            const int64_t need = (l.n + rows_it - 1) / rows_it;
             l.pat_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
         }
     }
