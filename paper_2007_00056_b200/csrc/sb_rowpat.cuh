@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
         if (xc0) d = dc[c0];
     }
     pdl_wait();
+    pdl_trigger_single(nc);
     for (int c = c0; c < nc; c += gridDim.x * blockDim.x) {
         if (c != c0) {
             mm = mem[c];

@@ -85,6 +85,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 // (no-op when launched without the attribute) / allow the successor to launch.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// grid-stride kernels: a CTA with at most one iteration over n items lets the
+// dependent grid launch now (it still waits for this grid's completion); CTAs
+// with more iterations trigger implicitly at exit
+__device__ __forceinline__ void pdl_trigger_single(int64_t n) {
+    if ((blockIdx.x + static_cast<int64_t>(gridDim.x)) * blockDim.x >= n) pdl_trigger();
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -1104,6 +1110,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
 __global__ void k_jacobi_zero(int64_t n, const double *__restrict__ f,
                               const double *__restrict__ diag, double *__restrict__ x, double omega) {
     pdl_wait();
+    pdl_trigger_single(n);
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         x[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, f[i]), diag[i]));
@@ -1117,6 +1124,7 @@ __global__ void k_restrict(int64_t nc, const int2 *__restrict__ mem, const doubl
                            double *__restrict__ fc, const double *__restrict__ dc, double *__restrict__ xc0,
                            double omega) {
     pdl_wait();
+    pdl_trigger_single(nc);
     for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < nc;
          c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int2 m = mem[c];
@@ -1131,6 +1139,7 @@ __global__ void k_restrict(int64_t nc, const int2 *__restrict__ mem, const doubl
 __global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const double *xin,
                           const double *__restrict__ xc, double *xout) {
     pdl_wait();
+    pdl_trigger_single(n);
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         xout[i] = __dadd_rn(xin[i], __dadd_rn(0.0, xc[agg[i]]));
@@ -1204,6 +1213,7 @@ struct X0 {
 __global__ void k_init(int64_t n, const double *__restrict__ b, double *__restrict__ x,
                        double *__restrict__ r, Red red) {
     pdl_wait();  // launched with PDL on the partitioned path
+    pdl_trigger_single(n);
     if (blockIdx.x == 0 && threadIdx.x == 0) red.st->t0 = globaltimer();
     double a[1] = {0.0};
     GRID_LOOP(i, n) {
@@ -1219,6 +1229,7 @@ __global__ void k_init(int64_t n, const double *__restrict__ b, double *__restri
 __global__ void k_copy_dot(int64_t n, const double *__restrict__ src, double *__restrict__ dst,
                            double *__restrict__ dst2, const double *__restrict__ w, Red red, X0 z0) {
     pdl_wait();  // launched with PDL on the partitioned path
+    pdl_trigger_single(n);
     double a[1] = {0.0};
     GRID_LOOP(i, n) {
         const double s = src[i];
@@ -1233,6 +1244,7 @@ __global__ void k_copy_dot(int64_t n, const double *__restrict__ src, double *__
 __global__ void k_dot(int64_t n, const double *__restrict__ u, const double *__restrict__ v,
                       const int *skip, Red red) {
     pdl_wait();  // launched with PDL on the partitioned path
+    pdl_trigger_single(n);
     double a[1] = {0.0};
     if (!(skip && *skip)) {
         GRID_LOOP(i, n) a[0] += u[i] * v[i];
@@ -1244,6 +1256,7 @@ __global__ void k_dot(int64_t n, const double *__restrict__ u, const double *__r
 __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
                              const double *__restrict__ p, const double *__restrict__ Ap, Red red, X0 z0) {
     pdl_wait();  // launched with PDL on the partitioned path
+    pdl_trigger_single(n);
     double a[1] = {0.0};
     const DevState *st = red.st;
     if (!st->done) {
@@ -1263,6 +1276,7 @@ __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restri
 __global__ void k_xpay(int64_t n, const double *__restrict__ z, double *__restrict__ p,
                        const DevState *__restrict__ st) {
     pdl_wait();  // launched with PDL on the partitioned path
+    pdl_trigger_single(n);
     const double beta = st->beta;
     GRID_LOOP(i, n) p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
 }
@@ -1271,6 +1285,7 @@ __global__ void k_xpay(int64_t n, const double *__restrict__ z, double *__restri
 __global__ void k_bi_s(int64_t n, const double *__restrict__ r, const double *__restrict__ Apt,
                        double *__restrict__ s, Red red, X0 z0) {
     pdl_wait();  // launched with PDL on the partitioned path
+    pdl_trigger_single(n);
     double a[1] = {0.0};
     const DevState *st = red.st;
     if (!st->done) {
@@ -1289,6 +1304,7 @@ __global__ void k_bi_s(int64_t n, const double *__restrict__ r, const double *__
 __global__ void k_bi_half(int64_t n, double *__restrict__ x, const double *__restrict__ pt,
                           const DevState *__restrict__ st) {
     pdl_wait();  // launched with PDL on the partitioned path
+    pdl_trigger_single(n);
     if (!st->half) return;
     const double alpha = st->alpha;
     GRID_LOOP(i, n) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pt[i]));
@@ -1300,6 +1316,7 @@ __global__ void k_bi_update(int64_t n, double *__restrict__ x, double *__restric
                             const double *__restrict__ s, const double *__restrict__ Ast,
                             const double *__restrict__ rbar, Red red) {
     pdl_wait();  // launched with PDL on the partitioned path
+    pdl_trigger_single(n);
     double a[2] = {0.0, 0.0};
     const DevState *st = red.st;
     if (!st->done) {
@@ -1320,6 +1337,7 @@ __global__ void k_bi_update(int64_t n, double *__restrict__ x, double *__restric
 __global__ void k_bi_p(int64_t n, const double *__restrict__ r, double *__restrict__ p,
                        const double *__restrict__ Apt, const DevState *__restrict__ st, X0 z0) {
     pdl_wait();  // launched with PDL on the partitioned path
+    pdl_trigger_single(n);
     if (st->done) return;
     const double beta = st->beta, omega = st->omega;
     GRID_LOOP(i, n) {
