@@ -205,6 +205,9 @@ int sb_tail_info(sb_ctx ctx, int *tail_from, int *ctas, int *smem_bytes);
  * int16 column deltas?, slice width}; *matrix_bytes = HBM bytes one matrix pass
  * streams (entries incl. padding + per-row metadata); *nnz = stored nonzeros. */
 int sb_level_format(sb_ctx ctx, int level, int *fmt, int64_t *matrix_bytes, int64_t *nnz);
+/* Plane-marching sweep of a row-pattern level (sb_march.cuh, opt-in with
+ * SB_MARCH=1): *geo = -1 (none) or 0 (27-point box); *stride = plane stride. */
+int sb_level_march(sb_ctx ctx, int level, int *geo, int *stride);
 /* Kernels launched by one V-cycle from level 0 (graph node count). */
 int sb_vcycle_launches(sb_ctx ctx, const sb_cycle *cp);
 

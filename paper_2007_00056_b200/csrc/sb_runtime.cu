@@ -825,6 +825,7 @@ __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
 }
 
 #include "sb_rowpat.cuh"
+#include "sb_march.cuh"
 
 // ===========================================================================
 // Cluster-resident tail: the deepest levels (each CTA's slice of every tail
@@ -1388,6 +1389,12 @@ struct DevLevel {
     std::vector<double> main_v;
     std::vector<int> main_o;
     size_t pat_tb = 0;
+    // marching sweep (k_march, sb_march.cuh): geometry of the main pattern
+    // (-1: none), march stride, offset range, table, tiles of 32 rows x K steps
+    int march_geo = -1, march_S = 0, march_N = 0, march_nqf = 0, march_nxb = 0, march_nyb = 0, march_ntiles = 0;
+    int march_grid = 0;
+    size_t march_tb = 0;
+    const unsigned char *march_table = nullptr;
     const uint8_t *pat_id = nullptr;
     const unsigned char *pat_table = nullptr;
     int2 *mem = nullptr;
@@ -1593,10 +1600,36 @@ static void launch_pat_w(sb_ctx c, const DevLevel &l, cudaStream_t s, const doub
              l.pat_id, l.pat_np, l.pat_table, main_pat<W>(l), x, f, out, omega, skip, aux, red);
 }
 
+template <int MODE, int NV, int G, int WP>
+static void launch_march_g(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
+                           double *out, double omega, const int *skip, const Red &red) {
+    MarchPat<Geo<G>::W> m;
+    std::memset(&m, 0, sizeof(m));
+    for (int k = 0; k < Geo<G>::W; ++k) m.v[k] = l.main_v[static_cast<size_t>(k)];
+    m.d = l.main_d;
+    m.r = l.main_r;
+    m.p = c_main_off ? -1 : l.main_p;
+    m.P = l.march_S;
+    m.N = l.march_N;
+    m.NY = l.march_S / l.march_N;
+    m.nqf = l.march_nqf;
+    m.nxb = l.march_nxb;
+    m.nyb = l.march_nyb;
+    m.ntiles = l.march_ntiles;
+    auto kern = ((l.march_S | l.march_N) & 1) ? k_march<MODE, NV, G, WP, false> : k_march<MODE, NV, G, WP, true>;
+    launch_k(c, kern, dim3(l.march_grid), dim3(kMarchThreads), march_smem_bytes(l.pat_tb, l.march_tb), s, static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table,
+             static_cast<int>(l.pat_tb), l.march_table, static_cast<int>(l.march_tb), m, x, f, out, omega, skip, red);
+}
+
 template <int MODE, int NV>
 static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *x, const double *f,
                        double *out, double omega, const int *skip, const Red &red, Aux aux = Aux{}) {
     if (l.n == 0) return;
+    if constexpr (MODE == M_JACOBI || MODE == M_SPMV || MODE == M_RESID) {
+        if (l.pat && l.march_geo >= 0) {
+            return launch_march_g<MODE, NV, 0, 28>(c, l, s, x, f, out, omega, skip, red);
+        }
+    }
     if (l.pat) {
         switch (l.pat_w) {
         case 5: return launch_pat_w<MODE, NV, 5>(c, l, s, x, f, out, omega, skip, red, aux);
@@ -1971,6 +2004,66 @@ static void make_tiles(const HostCsr &A, std::vector<int32_t> &tiles, int &cap) 
     }
 }
 
+// Plane-marching sweep (sb_march.cuh) for a row-pattern level whose main
+// pattern is a 27-point box: validate the box geometry of the main offsets,
+// embed every pattern whose offsets are a subsequence of the main ones (values
+// at the main slots, +0.0 elsewhere), upload the table. Opt-in (SB_MARCH=1);
+// SB_MARCH_MIN: smallest level (rows) that gets it.
+template <int G>
+static bool march_geo_ok(const DevLevel &D, int &P, int &N) {
+    constexpr int W = Geo<G>::W;
+    if (D.main_len != W || static_cast<int>(D.main_o.size()) < W) return false;
+    int kp = -1, kn = -1;  // slots (1, 0, 0) and (0, 1, 0)
+    for (int k = 0; k < W; ++k) {
+        if (Geo<G>::dz(k) == 1 && Geo<G>::dy(k) == 0 && Geo<G>::dx(k) == 0) kp = k;
+        if (Geo<G>::dz(k) == 0 && Geo<G>::dy(k) == 1 && Geo<G>::dx(k) == 0) kn = k;
+    }
+    P = D.main_o[static_cast<size_t>(kp)];
+    N = D.main_o[static_cast<size_t>(kn)];
+    if (N < 32 || P % N != 0 || P / N < 2) return false;  // a tile row spans one line
+    for (int k = 0; k < W; ++k)
+        if (D.main_o[static_cast<size_t>(k)] != Geo<G>::dz(k) * P + Geo<G>::dy(k) * N + Geo<G>::dx(k)) return false;
+    return true;
+}
+
+static void build_march(sb_ctx c, DevLevel &D, int np, int w, const double *val, const int32_t *off,
+                        const uint8_t *len) {
+    const char *e = std::getenv("SB_MARCH");  // opt-in: measured slower than k_rowpat
+    if (!e || std::atoi(e) == 0) return;
+    const char *em = std::getenv("SB_MARCH_MIN");
+    const int64_t nmin = em ? std::atoll(em) : 65536;
+    if (D.n < nmin) return;
+    int geo = -1, P = 0, N = 0;
+    if (w == 28 && march_geo_ok<0>(D, P, N)) geo = 0;  // (7-point levels: the row-pattern kernel measured faster)
+    if (geo < 0 || D.n / P < 3) return;
+    const int W = D.main_len, WE = (W + 1) & ~1;
+    const int wv = (w + 1) & ~1, wo = (w + 3) & ~3;
+    const size_t mtb = march_table_bytes(np, W);
+    std::vector<unsigned char> mt(mtb, 0);
+    auto *ev = reinterpret_cast<double *>(mt.data());
+    auto *emb = reinterpret_cast<uint8_t *>(ev + static_cast<size_t>(np) * WE);
+    for (int q = 0; q < np; ++q) {
+        int k = 0;
+        for (int j = 0; j < W; ++j) {
+            ev[q * WE + j] = 0.0;
+            if (k < len[q] && off[q * wo + k] == D.main_o[static_cast<size_t>(j)]) ev[q * WE + j] = val[q * wv + k++];
+        }
+        emb[q] = (k == len[q]) ? 1 : 0;
+    }
+    auto *dt = dalloc<unsigned char>(c, static_cast<int64_t>(mtb));
+    CK(cudaMemcpy(dt, mt.data(), mtb, cudaMemcpyHostToDevice));
+    D.march_geo = geo;
+    D.march_S = P;
+    D.march_N = N;
+    D.march_nqf = static_cast<int>(D.n / P);
+    D.march_nxb = (N + 31) / 32;
+    D.march_nyb = (P / N + kMarchLines - 1) / kMarchLines;
+    const int nqb = (D.march_nqf - 2 + kMarchK - 1) / kMarchK;
+    D.march_ntiles = D.march_nxb * D.march_nyb * nqb;
+    D.march_tb = mtb;
+    D.march_table = dt;
+}
+
 // Row-pattern format (§3.1): one byte per row when the level has <= 256
 // distinct rows (offsets + value bits, CSR order) of length <= 32. Threads
 // hash their rows, first occurrences become patterns, and every row is
@@ -2101,6 +2194,7 @@ static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
         D.main_v.assign(val + static_cast<size_t>(q) * wv, val + static_cast<size_t>(q) * wv + w);
         D.main_o.assign(off + static_cast<size_t>(q) * wo, off + static_cast<size_t>(q) * wo + w);
     }
+    build_march(c, D, np, w, val, off, len);
     auto *dp = dalloc<uint8_t>(c, A.n + 16);
     CK(cudaMemcpy(dp, pid.data(), pid.size(), cudaMemcpyHostToDevice));
     auto *dt = dalloc<unsigned char>(c, static_cast<int64_t>(tb));
@@ -2373,6 +2467,10 @@ template <int MODE, int NV, int VF, int CF> static void set_sg_attr(int b) {
 template <int MODE, int NV> static void set_smem_attr(size_t smem) {
     if (smem <= 48 * 1024) return;
     const int b = static_cast<int>(smem);
+    if constexpr (MODE == M_JACOBI || MODE == M_SPMV || MODE == M_RESID) {
+        CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    }
     CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
@@ -2830,7 +2928,8 @@ static sb_ctx ctx_begin(const sb_device_opts &o) {
 static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t n_vec, int tail_min,
                        int64_t vec_headroom = 0) {
     size_t max_smem = 0;
-    for (auto &l : c->L) max_smem = std::max({max_smem, l.smem, l.sell_smem, l.pat_tb});
+    for (auto &l : c->L) max_smem = std::max({max_smem, l.smem, l.sell_smem, l.pat_tb,
+                                               l.march_geo >= 0 ? march_smem_bytes(l.pat_tb, l.march_tb) : 0});
     if (max_smem > 200 * 1024) throw invalid_argument("sb_create: tile staging exceeds shared memory");
     set_smem_attr<M_SPMV, 0>(max_smem);
     set_smem_attr<M_SPMV, 1>(max_smem);
@@ -2867,6 +2966,16 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
             const int rows_it = kPatThreads * (l.pat_w <= 8 ? 2 : 1);
             const int64_t need = (l.n + rows_it - 1) / rows_it;
             l.pat_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
+        }
+        if (l.march_geo >= 0) {
+            occ = 0;
+            const size_t sm = march_smem_bytes(l.pat_tb, l.march_tb);
+            auto occ_m = [&](auto kern) {
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMarchThreads, sm));
+            };
+            occ_m(k_march<M_JACOBI, 0, 0, 28, true>);
+            const int64_t need = std::max<int64_t>(l.march_ntiles, 1);
+            l.march_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
         }
     }
     c->nc = h.nc;
@@ -3019,6 +3128,14 @@ int sb_level_format(sb_ctx c, int k, int *fmt, int64_t *matrix_bytes, int64_t *n
             *matrix_bytes = l.nnz * (vb + cb) + 4 * (l.n + 1);
         }
         *nnz = l.nnz;
+    });
+}
+
+int sb_level_march(sb_ctx c, int k, int *geo, int *stride) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, k);
+        *geo = l.march_geo;
+        *stride = l.march_S;
     });
 }
 
