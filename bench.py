@@ -45,7 +45,22 @@ WORKLOADS = {
     # BASELINE.json's stated target: "3D 7-point Poisson 256^3 AMG-PCG solved to 1e-8"
     "T256": dict(desc="Target: 3D 7-pt Poisson 256^3 (16.8M DOFs) AMG-PCG to 1e-8",
                  solver="pcg", gen=lambda sp: sp.poisson3d(256)),
+    # a general-valued operator (every row distinct, irregular coarse levels):
+    # the SELL-G / CSR format path instead of the row-pattern one
+    "G128": dict(desc="G128: 3D 7-pt graph Laplacian 128^3, random edge weights U[0.5,1.5) + 0.01 I (general "
+                      "format path) AMG-PCG",
+                 solver="pcg", gen=lambda sp: sp.graph_laplacian3d(128, seed=7)),
 }
+
+
+
+def placement(h, args):
+    """Level placement of the run: all levels device-resident, or the paper's hybrid
+    scheme (levels >= host_levels_from in pinned host memory, read zero-copy)."""
+    if args.host_levels_from < 0:
+        return {"mode": "device", "device_gb": round(h.device_bytes() / 1e9, 3)}
+    return {"mode": "hybrid", "host_levels_from": args.host_levels_from,
+            "device_gb": round(h.device_bytes() / 1e9, 3), "host_gb": round(h.host_bytes() / 1e9, 3)}
 
 
 def run_c5(args, wl):
@@ -62,7 +77,8 @@ def run_c5(args, wl):
     L = _lib.lib()
     cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40, coarse_target=500)
     t0 = time.perf_counter()
-    h = sp.Hierarchy.from_stencil27(nside, nside, nside, 26.0, -1.0, cfg, galerkin_gpu=args.galerkin_gpu)
+    h = sp.Hierarchy.from_stencil27(nside, nside, nside, 26.0, -1.0, cfg, galerkin_gpu=args.galerkin_gpu,
+                                    host_levels_from=args.host_levels_from)
     t_setup = time.perf_counter() - t0
     t0 = time.perf_counter()
     ctx = h.ctx()
@@ -126,7 +142,7 @@ def run_c5(args, wl):
                        "tol": "1e-8*||b||", "true_rel_residual": rep.true_residual / float(np.sqrt(n)),
                        "setup_s": round(t_setup, 1), "upload_s": round(t_upload, 1),
                        "level_rows": [v[0] for v in lv], "level_formats": [v[3][0] for v in lv],
-                       "parallelism": "single GPU"},
+                       "placement": placement(h, args), "parallelism": "single GPU"},
             "roofline": {"bound": "hbm", "kernel": "k_rowpat<JACOBI> (L0 Jacobi sweep)", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          # C5p's operator is the 27-point 256^3 of profiles/ncu_summary_P27_256.json
@@ -440,6 +456,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS) + ["C5", "C5p"])
+    ap.add_argument("--host-levels-from", type=int, default=-1,
+                    help="hybrid placement: matrices of levels >= K in pinned host memory (paper MI scheme)")
     ap.add_argument("--galerkin-gpu", action="store_true", help="Galerkin products on the GPU during setup")
     ap.add_argument("--ref-sample-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -473,7 +491,7 @@ def main():
     n = A.nrows()
     cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40, coarse_target=500)
     t0 = time.perf_counter()
-    h = sp.Hierarchy(A, cfg, device=local)
+    h = sp.Hierarchy(A, cfg, device=local, host_levels_from=args.host_levels_from)
     setup_s = time.perf_counter() - t0  # host setup (aggregation, Galerkin products, coarse inverse)
     t0 = time.perf_counter()
     ctx = h.ctx()
@@ -593,6 +611,7 @@ def main():
                        "coarse_target": 500, "max_levels": 40,
                        "l2": "hierarchy (%.0f MB) > 126 MB L2 and L2 flushed (256 MB write) before every step"
                              % (h.device_bytes() / 1e6),
+                       "placement": placement(h, args),
                        "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
                        "setup_s": round(setup_s, 3), "upload_s": round(upload_s, 3),
                        "true_rel_residual": true_rel},

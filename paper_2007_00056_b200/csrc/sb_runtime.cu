@@ -21,6 +21,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <vector>
@@ -2758,7 +2759,9 @@ static void setup_tail(sb_ctx c, const Hier &H) {
     d.img = dimg;
     c->tail = dalloc<TailDesc>(c, 1, false);
     CK(cudaMemcpy(c->tail, &d, sizeof(d), cudaMemcpyHostToDevice));
-    CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes));
+    // the attribute is process-wide: leave it at the budget (never below what
+    // another context's tail needs)
+    CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
     c->tail_ctas = ctas;
     c->tail_from = k0;
     c->tail_smem = d.smem_bytes;
@@ -2931,6 +2934,14 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
     for (auto &l : c->L) max_smem = std::max({max_smem, l.smem, l.sell_smem, l.pat_tb,
                                                l.march_geo >= 0 ? march_smem_bytes(l.pat_tb, l.march_tb) : 0});
     if (max_smem > 200 * 1024) throw invalid_argument("sb_create: tile staging exceeds shared memory");
+    {  // function attributes are process-wide: only ever raise them (a later
+       // context with smaller tiles must not break an earlier one's launches)
+        static std::mutex mu;
+        static size_t raised = 0;
+        std::lock_guard<std::mutex> lk(mu);
+        max_smem = std::max(max_smem, raised);
+        raised = max_smem;
+    }
     set_smem_attr<M_SPMV, 0>(max_smem);
     set_smem_attr<M_SPMV, 1>(max_smem);
     set_smem_attr<M_SPMV, 2>(max_smem);

@@ -33,7 +33,7 @@ __all__ = [
     "SolveResult", "InvalidArgument", "CudaError", "make_amg_preconditioner", "vcycle",
     "vcycle_in_place", "amg_solve", "pcg", "pbicgstab", "cg", "bicgstab", "spmv",
     "residual", "smooth", "smooth_in_place", "stats", "convdiff2d", "poisson2d",
-    "poisson3d", "aniso3d", "convdiff3d", "poisson3d_27", "rhs_ones", "rhs_random", "zeros",
+    "poisson3d", "aniso3d", "convdiff3d", "poisson3d_27", "graph_laplacian3d", "rhs_ones", "rhs_random", "zeros",
 ]
 
 
@@ -340,10 +340,11 @@ class Hierarchy:
 
     @classmethod
     def from_stencil27(cls, nx: int, ny: int, nz: int, diag: float, off: float, cfg: SolverConfig = None,
-                       device: int = 0, galerkin_gpu: bool = False) -> "Hierarchy":
+                       device: int = 0, galerkin_gpu: bool = False, host_levels_from: int = -1) -> "Hierarchy":
         """Hierarchy of the 3D 27-point operator generated straight into the setup's
         host storage (sb_setup_stencil27): no Python-side copy of the fine matrix,
-        int64 row offsets (config 5: 512^3, nnz 3.6e9)."""
+        int64 row offsets (config 5: 512^3, nnz 3.6e9). host_levels_from: hybrid
+        placement of the coarse levels (as in __init__)."""
         cfg = cfg or SolverConfig()
         cfg.validate()
         self = cls.__new__(cls)
@@ -352,7 +353,7 @@ class Hierarchy:
         check(_lib.lib().sb_setup_stencil27(int(nx), int(ny), int(nz), float(diag), float(off), C.byref(opts),
                                             C.byref(h)))
         self._h, self._ctx, self._device, self._coarse_exact = h, None, device, False
-        self._host_from, self._levels, self._A0, self.config = -1, None, None, cfg
+        self._host_from, self._levels, self._A0, self.config = int(host_levels_from), None, None, cfg
         return self
 
     def __del__(self):
@@ -675,6 +676,34 @@ def aniso3d(n, eps=1e-3) -> CsrMatrix:
 
 def convdiff3d(nx, ny, nz, bx, by, bz, c) -> CsrMatrix:
     return _gen(_lib.lib().sb_gen_convdiff3d, nx, ny, nz, bx, by, bz, c)
+
+
+def graph_laplacian3d(m, seed=7, shift=0.01) -> CsrMatrix:
+    """SPD graph Laplacian of the m^3 7-point grid with random edge weights
+    U[0.5, 1.5) plus shift*I: no two rows share their values, so no level has
+    row patterns and the hierarchy is irregular (node-HEM on random weights)."""
+    n = m ** 3
+    rng = np.random.default_rng(seed)
+    idx = np.arange(n, dtype=np.int64).reshape(m, m, m)  # [z, y, x]
+    rows, cols, vals = [], [], []
+    diag = np.full(n, shift)
+    for ax in range(3):
+        a = np.take(idx, np.arange(m - 1), axis=2 - ax).ravel()
+        b = np.take(idx, np.arange(1, m), axis=2 - ax).ravel()
+        w = rng.uniform(0.5, 1.5, a.size)
+        rows += [a, b]
+        cols += [b, a]
+        vals += [-w, -w]
+        np.add.at(diag, a, w)
+        np.add.at(diag, b, w)
+    r = np.concatenate(rows + [np.arange(n)])
+    c = np.concatenate(cols + [np.arange(n)])
+    v = np.concatenate(vals + [diag])
+    order = np.lexsort((c, r))
+    r, c, v = r[order], c[order], v[order]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, r + 1, 1)
+    return CsrMatrix(n, n, np.cumsum(rp), c.astype(np.int32), v)
 
 
 def poisson3d_27(n) -> CsrMatrix:

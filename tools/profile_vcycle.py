@@ -17,7 +17,8 @@ what = sys.argv[2] if len(sys.argv) > 2 else "both"
 gen = {"C2": lambda: sp.poisson3d(128), "C1": lambda: sp.poisson2d(1024, 1024),
        "C3": lambda: sp.aniso3d(256), "M64": lambda: sp.poisson3d(64), "T256": lambda: sp.poisson3d(256),
        "C4": lambda: sp.convdiff3d(256, 256, 256, 1.0, 100.0, 1.0, 1.0), "P27": lambda: sp.poisson3d_27(128),
-       "P27_256": lambda: sp.poisson3d_27(256)}[wl]
+       "P27_256": lambda: sp.poisson3d_27(256),
+       "G128": lambda: sp.graph_laplacian3d(128, seed=7)}[wl]
 A = gen()
 cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40)
 h = sp.Hierarchy(A, cfg)
