@@ -419,6 +419,54 @@ __device__ __forceinline__ double row_eval(int row, int rs, int re, const E &e, 
     else return __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
 }
 
+// Rows longer than this are evaluated by a whole warp (k_csr_tile).
+constexpr int kLongRow = 32;
+
+// row_eval of one long row by a warp: lane l multiplies entries k0 + l (the
+// products are the reference's, __dmul_rn), then every lane adds the 32
+// products in CSR order from the shuffles (the same dependent chain of
+// __dadd_rn as row_eval; the gathers of 32 entries are in flight together).
+template <int MODE, typename E>
+__device__ __forceinline__ double warp_row_eval(int row, int rs, int re, const E &e, const double *x,
+                                                const double *f, double fi, const Aux &aux, double omega, int lane) {
+    double sum = 0.0, d = 0.0;
+#pragma unroll 1
+    for (int k0 = rs; k0 < re; k0 += 32) {
+        const int k = k0 + lane;
+        double p = 0.0;
+        bool isd = false;
+        double a = 0.0;
+        if (k < re) {
+            const int c = e.col(k, row);
+            a = e.val(k);
+            p = __dmul_rn(a, xval<MODE, false>(c, x, f, aux, omega));
+            isd = c == row;
+        }
+        const int cnt = min(32, re - k0);
+        if (cnt == 32) {  // full chunk: shuffles issue 8 ahead of the dependent adds
+#pragma unroll
+            for (int j0 = 0; j0 < 32; j0 += 8) {
+                double q[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) q[j] = __shfl_sync(0xffffffffu, p, j0 + j);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) sum = __dadd_rn(sum, q[j]);
+            }
+        } else {
+#pragma unroll 1
+            for (int j = 0; j < cnt; ++j) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, p, j));
+        }
+        const unsigned dm = __ballot_sync(0xffffffffu, isd);
+        if (MODE >= M_JACOBI && dm) d = __shfl_sync(0xffffffffu, a, 31 - __clz(dm));
+    }
+    if constexpr (MODE == M_SPMV) return sum;
+    else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
+    else {
+        const double xi = xval<MODE, false>(row, x, f, aux, omega);
+        return __dadd_rn(xi, __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), d));
+    }
+}
+
 // Persistent, double-buffered CSR tile pipeline. Tiles of <= 256 consecutive
 // rows (tile_ptr, built at setup) are dealt round-robin to a grid sized to the
 // SM count; for each tile one elected thread issues two TMA bulk copies
@@ -463,6 +511,11 @@ __global__ void __launch_bounds__(kTileRows, 3)
 #pragma unroll
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
 
+    auto emit_row = [&](int row, double o) {
+        out[row] = o;
+        if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row] : o);
+        if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
+    };
     constexpr int VB = VF ? 1 : 8;  // bytes per value / column entry
     constexpr int CB = CF ? 2 : 4;
     constexpr int VA = 16 / VB, CA = 16 / CB;  // entries per 16-byte granule
@@ -540,25 +593,26 @@ __global__ void __launch_bounds__(kTileRows, 3)
             const int r0 = h.x, r1 = h.y;
             const int row = r0 + static_cast<int>(threadIdx.x);
             const unsigned char *st = smem + s * sb;
-            if (row < r1) {
-                const int32_t *srp = reinterpret_cast<const int32_t *>(st + o_rp) - (r0 & ~3);
-                const int rs = srp[row], re = srp[row + 1];
-                double fi = 0.0;
-                if (MODE != M_SPMV) {
-                    const bool f_staged = it >= kStages - 1 && row < (r1 & ~1);
-                    fi = f_staged ? reinterpret_cast<const double *>(st + o_f)[row - (r0 & ~1)] : f[row];
-                }
-                const bool staged = (h.w - h.z) <= cap;
-                Ent<VF, CF> e;
-                e.vals = staged ? static_cast<const void *>(st - static_cast<size_t>(h.z & ~(VA - 1)) * VB)
-                                : vals;
-                e.cols = staged ? static_cast<const void *>(st + o_c - static_cast<size_t>(h.z & ~(CA - 1)) * CB)
-                                : cols;
-                e.dict = sdict;
-                const double o = row_eval<MODE, false>(row, rs, re, e, x, f, fi, aux, omega);
-                out[row] = o;
-                if (NV >= 1) acc[0] += o * (red.w0 ? red.w0[row] : o);
-                if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? red.w1[row] : o);
+            const bool staged = (h.w - h.z) <= cap;
+            Ent<VF, CF> e;
+            e.vals = staged ? static_cast<const void *>(st - static_cast<size_t>(h.z & ~(VA - 1)) * VB) : vals;
+            e.cols = staged ? static_cast<const void *>(st + o_c - static_cast<size_t>(h.z & ~(CA - 1)) * CB) : cols;
+            e.dict = sdict;
+            const int32_t *srp = reinterpret_cast<const int32_t *>(st + o_rp) - (r0 & ~3);
+            auto rhs_of = [&](int rr) {  // f_row: staged window or global
+                if (MODE == M_SPMV) return 0.0;
+                const bool f_staged = it >= kStages - 1 && rr < (r1 & ~1);
+                return f_staged ? reinterpret_cast<const double *>(st + o_f)[rr - (r0 & ~1)] : f[rr];
+            };
+            // rows longer than kLongRow go to the whole warp (below)
+            const unsigned lm = __ballot_sync(0xffffffffu, row < r1 && srp[row + 1] - srp[row] > kLongRow);
+            if (row < r1 && !((lm >> lane) & 1u))
+                emit_row(row, row_eval<MODE, false>(row, srp[row], srp[row + 1], e, x, f, rhs_of(row), aux, omega));
+            for (unsigned m = lm; m; m &= m - 1) {  // gathers 32 entries at a time, sum in CSR order
+                const int src = __ffs(m) - 1;
+                const int lr = row - lane + src;
+                const double o = warp_row_eval<MODE>(lr, srp[lr], srp[lr + 1], e, x, f, rhs_of(lr), aux, omega, lane);
+                if (lane == src) emit_row(lr, o);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
@@ -2619,6 +2673,13 @@ static void setup_tail(sb_ctx c, const Hier &H) {
         const int k = k0 - 1;
         if (c->L[static_cast<size_t>(k)].n > tail_rows || L - k > kTailMaxLevels) break;
         if ((H.levels[static_cast<size_t>(k)].A.n + ctas - 1) / ctas > 32768) break;
+        {  // the tail sums a row per thread: levels with long (hub) rows stay on
+           // the kernels, whose CSR tiles give such rows a whole warp
+            const HostCsr &A = H.levels[static_cast<size_t>(k)].A;
+            int64_t wmax = 0;
+            for (int64_t i = 0; i < A.n; ++i) wmax = std::max<int64_t>(wmax, A.rp[i + 1] - A.rp[i]);
+            if (wmax > kLongRow) break;
+        }
         const int64_t add = level_bytes(k);
         if (total + add > budget) break;
         total += add;
