@@ -257,11 +257,17 @@ def bytes_model(h, pre=6, post=6, matrix_bytes=None):
 
 
 KERNEL_OF_FORMAT = {2: "k_rowpat<JACOBI>", 1: "k_sellg<JACOBI>", 0: "k_csr_tile<JACOBI>"}
-BYTES_OF_FORMAT = {
-    2: "matrix pass = 1 B pattern index per row + the pattern table",
-    1: "matrix pass = grouped sliced-ELL slice blocks incl. padding (1 B value index + 2 B column delta "
-       "per slot, 2 B/row length + diagonal index, 16 B/slice header)",
-    0: "matrix pass = CSR (12 B/nonzero + 4 B/row)"}
+def bytes_of_format(fmt):
+    """What one matrix pass streams for a level format (sb_level_format: kind, vf, cf, width)."""
+    kind, vf, cf = fmt[0], fmt[1], fmt[2]
+    v = "1 B value index" if vf else "8 B value"
+    c = "2 B column delta" if cf else "4 B column"
+    if kind == 2:
+        return "matrix pass = 1 B pattern index per row + the pattern table"
+    if kind == 1:
+        return (f"matrix pass = grouped sliced-ELL slice blocks incl. padding ({v} + {c} per slot, "
+                "2 B/row length + diagonal index, 16 B/slice header)")
+    return f"matrix pass = CSR tiles ({v} + {c} per nonzero + 4 B/row)"
 
 
 def load_traffic(wl):
@@ -620,7 +626,7 @@ def main():
                          "frac": achieved / peak, "traffic": load_traffic(wl),
                          "algorithmic_bytes_per_launch": bm["l0_jacobi"],
                          "bytes_definition": "bytes the shipped lossless format must stream per sweep: "
-                                             + BYTES_OF_FORMAT[fmts[0][0]] + " + 24 B/row (x, f, x_new); "
+                                             + bytes_of_format(fmts[0]) + " + 24 B/row (x, f, x_new); "
                                              "SURVEY §8d CSR-equivalent figures below",
                          "launch_ms": jac_ms, "l0_format": fmts[0],
                          "csr_equiv_bytes_per_launch": bm_csr["l0_jacobi"],
