@@ -143,7 +143,7 @@ def run_c5(args, wl):
                        "setup_s": round(t_setup, 1), "upload_s": round(t_upload, 1),
                        "level_rows": [v[0] for v in lv], "level_formats": [v[3][0] for v in lv],
                        "placement": placement(h, args), "parallelism": "single GPU"},
-            "roofline": {"bound": "hbm", "kernel": "k_rowpat<JACOBI> (L0 Jacobi sweep)", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": sweep_kernel(L, ctx) + " (L0 Jacobi sweep)", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "frac_of_spec_8000": achieved / SPEC_HBM_GBS,
                          # C5p's operator is the 27-point 256^3 of profiles/ncu_summary_P27_256.json
@@ -260,7 +260,13 @@ def bytes_model(h, pre=6, post=6, matrix_bytes=None):
     return dict(vcycle=vc, pcg_iter=pcg_it, bicg_iter=bicg_it, l0_jacobi=jac(0), l0_spmv=spmv)
 
 
-KERNEL_OF_FORMAT = {2: "k_rowpat<JACOBI>", 1: "k_sellg<JACOBI>", 0: "k_csr_tile<JACOBI>"}
+def sweep_kernel(L, ctx, level=0):
+    """The kernel a Jacobi sweep of `level` launches (sb_level_sweep_kernel)."""
+    import ctypes as C
+    buf = C.create_string_buffer(64)
+    from paper_2007_00056_b200 import _lib
+    _lib.check(L.sb_level_sweep_kernel(ctx, level, buf, 64))
+    return buf.value.decode() + "<JACOBI>"
 def bytes_of_format(fmt):
     """What one matrix pass streams for a level format (sb_level_format: kind, vf, cf, width)."""
     kind, vf, cf = fmt[0], fmt[1], fmt[2]
@@ -625,7 +631,7 @@ def main():
                        "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
                        "setup_s": round(setup_s, 3), "upload_s": round(upload_s, 3),
                        "true_rel_residual": true_rel},
-            "roofline": {"bound": "hbm", "kernel": KERNEL_OF_FORMAT[fmts[0][0]] + " (L0 Jacobi sweep)",
+            "roofline": {"bound": "hbm", "kernel": sweep_kernel(L, ctx) + " (L0 Jacobi sweep)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "frac_of_spec_8000": achieved / SPEC_HBM_GBS,
                          "traffic": load_traffic(wl),

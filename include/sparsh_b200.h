@@ -208,6 +208,9 @@ int sb_level_format(sb_ctx ctx, int level, int *fmt, int64_t *matrix_bytes, int6
 /* Plane-marching sweep of a row-pattern level (sb_march.cuh, opt-in with
  * SB_MARCH=1): *geo = -1 (none) or 0 (27-point box); *stride = plane stride. */
 int sb_level_march(sb_ctx ctx, int level, int *geo, int *stride);
+/* Name of the kernel a Jacobi sweep of `level` launches (k_boxpair, k_march,
+ * k_rowpat, k_sellg or k_csr_tile), NUL-terminated into buf[cap]. */
+int sb_level_sweep_kernel(sb_ctx ctx, int level, char *buf, int cap);
 /* Kernels launched by one V-cycle from level 0 (graph node count). */
 int sb_vcycle_launches(sb_ctx ctx, const sb_cycle *cp);
 

@@ -356,3 +356,127 @@ __global__ void __launch_bounds__(kPatThreads, W <= 8 ? SB_PAT_MINB : SB_PAT_MIN
         if (xc0) xc0[c] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), d));
     }
 }
+
+// Row pairs on 27-point box levels (k_boxpair). A thread owns rows 2q, 2q + 1
+// (P and N even, so for every run (dz, dy) of three consecutive columns the
+// base r + dz P + dy N is even): the six x values both rows need from a run,
+// x[r + d - 1 .. r + d + 2] (and d - 2 for alignment), come from three
+// 16-byte loads instead of six 8-byte gathers, the rhs / output / pattern
+// bytes of the pair in one vector access each, and the two rows' sums are two
+// independent dependent chains (ILP 2 for the reference's sequential order).
+// Warps whose 64 rows are not all the main pattern, or whose reads would leave
+// [0, n), run the row-pattern per-row path. L1 wavefronts per 32 rows: ~58 vs
+// ~79 for k_rowpat's wide path, which is L1-bound (ncu: 87% of peak).
+#ifndef SB_BOX_THREADS
+#define SB_BOX_THREADS 128  // measured: 128 x 5 CTAs/SM (<= 102 registers) 176 us vs 212 at 256 x 2 (27-pt 256^3 L0)
+#endif
+#ifndef SB_BOX_MINB
+#define SB_BOX_MINB 5
+#endif
+constexpr int kBoxThreads = SB_BOX_THREADS;
+template <int MODE, int NV>
+__global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
+    k_boxpair(int n, const uint8_t *__restrict__ pid, int np, const unsigned char *__restrict__ table,
+              const uint32_t *__restrict__ rmask, const __grid_constant__ MainPat<28> mp,
+              const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
+              const int *skip, Red red) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const SmemTab<28> T = smem_tab<28>(smem, table, np);
+    double acc[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
+    const int npairs = n >> 1;
+    const int stride = gridDim.x * kBoxThreads;
+    const int lo = -mp.o[0] + 2, hi = n - (mp.o[26] + 3);  // pairs starting in [lo, hi) read inside [0, n)
+    auto emit = [&](int row, double o, double fi, double xi) {
+        out[row] = o;
+        if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fi : red.w0 == x ? xi : red.w0[row]) : o);
+        if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? (red.w1 == x ? xi : red.w1[row]) : o);
+    };
+    auto fin = [&](double xi, double fi, double sum, double dg, double ry) -> double {
+        if constexpr (MODE == M_SPMV) return sum;
+        else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
+        else return __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), dg, ry));
+    };
+    pdl_wait();
+    if (!(skip && *skip)) {
+        for (int q = blockIdx.x * kBoxThreads + threadIdx.x, base = blockIdx.x * kBoxThreads; base < npairs;
+             q += stride, base += stride) {
+            if (base + stride >= npairs) pdl_trigger();
+            const bool in = q < npairs;
+            const unsigned inm = __ballot_sync(0xffffffffu, in);
+            if (!inm) continue;
+            // lanes past the end shadow the warp's first pair (in bounds, not stored)
+            const int r0w = __shfl_sync(0xffffffffu, 2 * q, __ffs(inm) - 1);
+            const int r = in ? 2 * q : r0w;
+            const uint16_t pp = *reinterpret_cast<const uint16_t *>(pid + r);
+            const int p0 = pp & 0xff, p1 = pp >> 8;
+            // restriction masks: the pattern is the main one with some slots absent
+            // and the same values elsewhere (0: not a restriction)
+            const uint32_t m0 = __ldg(rmask + p0), m1 = __ldg(rmask + p1);
+            const bool fast = m0 && m1 && r >= lo && r < hi;
+            if (__all_sync(0xffffffffu, fast)) {
+                const double2 fv = (MODE == M_SPMV) ? make_double2(0.0, 0.0) : __ldg(reinterpret_cast<const double2 *>(f + r));
+                double s0 = 0.0, s1 = 0.0, xi0 = 0.0, xi1 = 0.0;
+                double2 A[9], B[9], Cc[9];
+#pragma unroll
+                for (int j = 0; j < 9; ++j) {  // run j: slots 3j .. 3j+2, base offset o[3j+1] (even)
+                    const double2 *b = reinterpret_cast<const double2 *>(at_off(x + r, mp.o[3 * j + 1]));
+                    A[j] = __ldg(b - 1);
+                    B[j] = __ldg(b);
+                    Cc[j] = __ldg(b + 1);
+                }
+                // an absent slot adds +0.0 (no product: inf / NaN there never enter),
+                // sum + (+0) == sum bit for bit, so the sums are the rows' own CSR sums
+                if (__all_sync(0xffffffffu, (m0 & m1) == 0x7ffffffu)) {
+#pragma unroll
+                    for (int j = 0; j < 9; ++j) {
+                        s0 = __dadd_rn(s0, __dmul_rn(mp.v[3 * j], A[j].y));
+                        s1 = __dadd_rn(s1, __dmul_rn(mp.v[3 * j], B[j].x));
+                        s0 = __dadd_rn(s0, __dmul_rn(mp.v[3 * j + 1], B[j].x));
+                        s1 = __dadd_rn(s1, __dmul_rn(mp.v[3 * j + 1], B[j].y));
+                        s0 = __dadd_rn(s0, __dmul_rn(mp.v[3 * j + 2], B[j].y));
+                        s1 = __dadd_rn(s1, __dmul_rn(mp.v[3 * j + 2], Cc[j].x));
+                    }
+                } else {
+                    auto t = [&](uint32_t m, int k, double v, double xv) {
+                        return ((m >> k) & 1u) ? __dmul_rn(v, xv) : 0.0;
+                    };
+#pragma unroll
+                    for (int j = 0; j < 9; ++j) {
+                        s0 = __dadd_rn(s0, t(m0, 3 * j, mp.v[3 * j], A[j].y));
+                        s1 = __dadd_rn(s1, t(m1, 3 * j, mp.v[3 * j], B[j].x));
+                        s0 = __dadd_rn(s0, t(m0, 3 * j + 1, mp.v[3 * j + 1], B[j].x));
+                        s1 = __dadd_rn(s1, t(m1, 3 * j + 1, mp.v[3 * j + 1], B[j].y));
+                        s0 = __dadd_rn(s0, t(m0, 3 * j + 2, mp.v[3 * j + 2], B[j].y));
+                        s1 = __dadd_rn(s1, t(m1, 3 * j + 2, mp.v[3 * j + 2], Cc[j].x));
+                    }
+                }
+                xi0 = B[4].x;
+                xi1 = B[4].y;
+                if (in) {
+                    const double o0 = fin(xi0, fv.x, s0, mp.d, mp.r), o1 = fin(xi1, fv.y, s1, mp.d, mp.r);
+                    if constexpr (NV == 0) {
+                        *reinterpret_cast<double2 *>(out + r) = make_double2(o0, o1);
+                    } else {
+                        emit(r, o0, fv.x, xi0);
+                        emit(r + 1, o1, fv.y, xi1);
+                    }
+                }
+            } else if (in) {  // the row-pattern per-row path for both rows
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    const int row = r + h, p = h ? p1 : p0;
+                    const double *xr = x + row;
+                    const double xi = __ldg(xr);
+                    const double fi = (MODE == M_SPMV) ? 0.0 : __ldg(f + row);
+                    const double sum = (p == mp.p) ? wide_row_sum<28>(SrcMain<28>{mp}, xr, xi)
+                                                   : wide_row_sum<28>(SrcTab<28>{T, p}, xr, xi);
+                    const double dg = (p == mp.p) ? mp.d : T.d(p), ry = (p == mp.p) ? mp.r : T.r(p);
+                    emit(row, fin(xi, fi, sum, dg, ry), fi, xi);
+                }
+            }
+        }
+    }
+    if constexpr (NV > 0) finish_reduction<NV>(red, acc);
+}

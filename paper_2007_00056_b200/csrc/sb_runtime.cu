@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <cstdio>
 #include <map>
 #include <mutex>
 #include <memory>
@@ -1449,6 +1450,9 @@ struct DevLevel {
     int march_geo = -1, march_S = 0, march_N = 0, march_nqf = 0, march_nxb = 0, march_nyb = 0, march_ntiles = 0;
     int march_grid = 0;
     size_t march_tb = 0;
+    // row pairs on 27-point box levels with even strides (k_boxpair)
+    int box_pair = 0, box_grid = 0;
+    const uint32_t *box_rmask = nullptr;
     const unsigned char *march_table = nullptr;
     const uint8_t *pat_id = nullptr;
     const unsigned char *pat_table = nullptr;
@@ -1681,6 +1685,12 @@ static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double
                        double *out, double omega, const int *skip, const Red &red, Aux aux = Aux{}) {
     if (l.n == 0) return;
     if constexpr (MODE == M_JACOBI || MODE == M_SPMV || MODE == M_RESID) {
+        auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        if (l.pat && l.box_pair && a16(x) && a16(out) && (MODE == M_SPMV || a16(f))) {
+            launch_k(c, k_boxpair<MODE, NV>, dim3(l.box_grid), dim3(kBoxThreads), l.pat_tb, s, static_cast<int>(l.n),
+                     l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<28>(l), x, f, out, omega, skip, red);
+            return;
+        }
         if (l.pat && l.march_geo >= 0) {
             return launch_march_g<MODE, NV, 0, 28>(c, l, s, x, f, out, omega, skip, red);
         }
@@ -2250,6 +2260,32 @@ static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
         D.main_o.assign(off + static_cast<size_t>(q) * wo, off + static_cast<size_t>(q) * wo + w);
     }
     build_march(c, D, np, w, val, off, len);
+    {  // k_boxpair: main pattern a 27-point box with even line / plane strides, n even
+        const char *bp = std::getenv("SB_BOXPAIR");
+        int P = 0, N = 0;
+        if (!(bp && std::atoi(bp) == 0) && w == 28 && A.n % 2 == 0 && A.n >= 2 && march_geo_ok<0>(D, P, N) &&
+            P % 2 == 0 && N % 2 == 0) {
+            // restriction masks: pattern q = the main pattern with slots removed
+            // (same offsets in order, same value bits where present), else 0
+            const int wv = (w + 1) & ~1, wo = (w + 3) & ~3;
+            std::vector<uint32_t> rm(static_cast<size_t>(np), 0u);
+            for (int q = 0; q < np; ++q) {
+                uint32_t m = 0u;
+                int k = 0;
+                for (int j = 0; j < 27; ++j)
+                    if (k < len[q] && off[q * wo + k] == D.main_o[static_cast<size_t>(j)]) {
+                        if (std::memcmp(&val[q * wv + k], &D.main_v[static_cast<size_t>(j)], 8) != 0) break;
+                        m |= 1u << j;
+                        ++k;
+                    }
+                rm[static_cast<size_t>(q)] = (k == len[q]) ? m : 0u;
+            }
+            auto *dm = dalloc<uint32_t>(c, np);
+            CK(cudaMemcpy(dm, rm.data(), sizeof(uint32_t) * rm.size(), cudaMemcpyHostToDevice));
+            D.box_rmask = dm;
+            D.box_pair = 1;
+        }
+    }
     auto *dp = dalloc<uint8_t>(c, A.n + 16);
     CK(cudaMemcpy(dp, pid.data(), pid.size(), cudaMemcpyHostToDevice));
     auto *dt = dalloc<unsigned char>(c, static_cast<int64_t>(tb));
@@ -2523,6 +2559,7 @@ template <int MODE, int NV> static void set_smem_attr(size_t smem) {
     if (smem <= 48 * 1024) return;
     const int b = static_cast<int>(smem);
     if constexpr (MODE == M_JACOBI || MODE == M_SPMV || MODE == M_RESID) {
+        CK(cudaFuncSetAttribute(k_boxpair<MODE, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     }
@@ -3039,6 +3076,12 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
             const int64_t need = (l.n + rows_it - 1) / rows_it;
             l.pat_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
         }
+        if (l.box_pair) {
+            occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_boxpair<M_JACOBI, 0>, kBoxThreads, l.pat_tb));
+            const int64_t need = (l.n / 2 + kBoxThreads - 1) / kBoxThreads;
+            l.box_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
+        }
         if (l.march_geo >= 0) {
             occ = 0;
             const size_t sm = march_smem_bytes(l.pat_tb, l.march_tb);
@@ -3200,6 +3243,16 @@ int sb_level_format(sb_ctx c, int k, int *fmt, int64_t *matrix_bytes, int64_t *n
             *matrix_bytes = l.nnz * (vb + cb) + 4 * (l.n + 1);
         }
         *nnz = l.nnz;
+    });
+}
+
+int sb_level_sweep_kernel(sb_ctx c, int k, char *buf, int cap) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, k);
+        if (!buf || cap < 1) throw invalid_argument("sb_level_sweep_kernel: no buffer");
+        const char *name = l.pat ? (l.box_pair ? "k_boxpair" : l.march_geo >= 0 ? "k_march" : "k_rowpat")
+                                 : l.sell ? "k_sellg" : "k_csr_tile";
+        std::snprintf(buf, static_cast<size_t>(cap), "%s", name);
     });
 }
 

@@ -47,6 +47,7 @@ def _cases(sp):
 
 @pytest.mark.parametrize("idx", range(8))
 def test_march_kernels_bitexact(sp, oracle_best, idx, monkeypatch):
+    monkeypatch.setenv("SB_BOXPAIR", "0")
     monkeypatch.setenv("SB_MARCH", "1")
     monkeypatch.setenv("SB_MARCH_MIN", "0")
     name, make, geo = _cases(sp)[idx]
@@ -63,11 +64,13 @@ def test_march_kernels_bitexact(sp, oracle_best, idx, monkeypatch):
         assert np.array_equal(sp.smooth(jac, A, x, f, sweeps), oracle_best.jacobi(A, 2.0 / 3.0, x, f, sweeps)), name
 
 
+@pytest.mark.parametrize("kern", ["march", "boxpair"])
 @pytest.mark.parametrize("idx", [0, 1, 2, 3])
-def test_march_nonfinite_absent_slots(sp, oracle_best, idx, monkeypatch):
+def test_march_nonfinite_absent_slots(sp, oracle_best, idx, kern, monkeypatch):
     # inf / NaN at x positions that boundary rows read only through absent
-    # (embedded +0.0) slots: 0 * inf would be NaN, the row must be replayed
-    monkeypatch.setenv("SB_MARCH", "1")
+    # (embedded +0.0 / masked) slots: 0 * inf would be NaN
+    monkeypatch.setenv("SB_BOXPAIR", "1" if kern == "boxpair" else "0")
+    monkeypatch.setenv("SB_MARCH", "1" if kern == "march" else "0")
     monkeypatch.setenv("SB_MARCH_MIN", "0")
     _, make, _ = _cases(sp)[idx]
     A = make()
@@ -93,6 +96,7 @@ def test_march_nonfinite_absent_slots(sp, oracle_best, idx, monkeypatch):
 
 
 def _solve(sp, A, march, monkeypatch):
+    monkeypatch.setenv("SB_BOXPAIR", "0")
     monkeypatch.setenv("SB_MARCH", "1" if march else "0")
     monkeypatch.setenv("SB_MARCH_MIN", "0")
     cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40)
@@ -116,3 +120,55 @@ def test_march_vcycle_pcg_identical(sp, dims, monkeypatch):
     # per-thread order (deterministic, rounding-level differences)
     assert r1.report.iterations == r0.report.iterations
     assert np.linalg.norm(r1.x - r0.x) <= 1e-12 * np.linalg.norm(r0.x)
+
+
+# ---- k_boxpair (sb_rowpat.cuh): row pairs with 16-byte loads on 27-point box
+# levels whose line / plane strides are even (the default kernel there) -------
+
+def _sweep_kernel(sp, A_or_h, level=0):
+    from paper_2007_00056_b200 import _lib
+    h = A_or_h._device() if isinstance(A_or_h, sp.CsrMatrix) else A_or_h
+    buf = C.create_string_buffer(64)
+    _lib.check(_lib.lib().sb_level_sweep_kernel(h.ctx(), level, buf, 64))
+    return buf.value.decode()
+
+
+@pytest.mark.parametrize("case", ["p27", "varied", "varied-odd", "poisson7"])
+def test_boxpair_kernels_bitexact(sp, oracle_best, case, monkeypatch):
+    monkeypatch.setenv("SB_BOXPAIR", "1")
+    A, want_k = {"p27": (lambda: _p27(sp, 40, 10, 40), "k_boxpair"),
+                 "varied": (lambda: stencil27_varied(sp, 64, 6, 9, seed=8), "k_boxpair"),
+                 "varied-odd": (lambda: stencil27_varied(sp, 33, 17, 12, seed=9), "k_rowpat"),  # odd N
+                 "poisson7": (lambda: sp.poisson3d(34, 12, 20), "k_rowpat")}[case]
+    A = A()
+    assert _sweep_kernel(sp, A) == want_k
+    n = A.nrows()
+    rng = np.random.default_rng(21)
+    x = rng.uniform(-1, 1, n)
+    f = rng.uniform(-1, 1, n)
+    assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x))
+    assert np.array_equal(sp.residual(A, x, f), oracle_best.residual(A, x, f))
+    jac = sp.SmootherKind.weighted_jacobi()
+    for sweeps in (1, 4):
+        assert np.array_equal(sp.smooth(jac, A, x, f, sweeps), oracle_best.jacobi(A, 2.0 / 3.0, x, f, sweeps))
+    x[[n // 2, n // 3, 5]] = [np.inf, np.nan, -np.inf]  # interior (pair path) and boundary rows
+    assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x), equal_nan=True)
+
+
+def test_boxpair_vcycle_pcg_identical(sp, monkeypatch):
+    A = _p27(sp, 48, 16, 40)
+    cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40)
+    b = sp.rhs_ones(A.nrows())
+    cp = sp.CycleParams.from_config(cfg)
+    out = {}
+    for on in ("1", "0"):
+        monkeypatch.setenv("SB_BOXPAIR", on)
+        h = sp.Hierarchy(A, cfg, device=0)
+        ks = [_sweep_kernel(sp, h, k) for k in range(h.nlevels() - 1)]
+        v = sp.vcycle(h, 0, b, np.zeros(A.nrows()), cp)
+        r = sp.pcg(A, b, sp.make_amg_preconditioner(h, cp), 1e-8 * float(np.linalg.norm(b)), 200)
+        out[on] = (ks, v, r)
+    assert "k_boxpair" in out["1"][0] and "k_boxpair" not in out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert out["1"][2].report.iterations == out["0"][2].report.iterations
+    assert np.linalg.norm(out["1"][2].x - out["0"][2].x) <= 1e-12 * np.linalg.norm(out["0"][2].x)
