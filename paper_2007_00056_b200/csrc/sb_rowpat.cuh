@@ -480,3 +480,116 @@ __global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
     }
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
 }
+
+// Row pairs on 7-point (W = 7: -P, -N, -1, 0, 1, N, P) and 5-point (W = 5:
+// -N, -1, 0, 1, N) cross levels with even strides: k_boxpair's scheme for the
+// cross. Per pair: one 16-byte load for each of the +-P / +-N neighbour pairs,
+// three for the -1 .. +2 run, one for the rhs, one store; the two rows' sums
+// are independent chains; restriction masks (W bits) keep boundary rows on the
+// vector path (absent slot: +0.0, no product).
+#ifndef SB_CROSS_THREADS
+#define SB_CROSS_THREADS 256
+#endif
+#ifndef SB_CROSS_MINB
+#define SB_CROSS_MINB 6  // measured (C2 / 256^3 L0 sweeps): 256 x 6 best of 256 x 4,5,6, 128 x 8,10,12, 512 x 2
+#endif
+constexpr int kCrossThreads = SB_CROSS_THREADS;
+template <int MODE, int NV, int W>
+__global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
+    k_crosspair(int n, const uint8_t *__restrict__ pid, int np, const unsigned char *__restrict__ table,
+                const uint32_t *__restrict__ rmask, const __grid_constant__ MainPat<W> mp,
+                const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
+                const int *skip, Red red) {
+    static_assert(W == 7 || W == 5, "cross geometries");
+    constexpr int C = W / 2;  // centre slot (offset 0)
+    extern __shared__ __align__(16) unsigned char smem[];
+    const SmemTab<W> T = smem_tab<W>(smem, table, np);
+    double acc[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
+    const int npairs = n >> 1;
+    const int stride = gridDim.x * kCrossThreads;
+    const int lo = -mp.o[0] + 2, hi = n - (mp.o[W - 1] + 3);
+    auto emit = [&](int row, double o, double fi, double xi) {
+        out[row] = o;
+        if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fi : red.w0 == x ? xi : red.w0[row]) : o);
+        if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? (red.w1 == x ? xi : red.w1[row]) : o);
+    };
+    auto fin = [&](double xi, double fi, double sum, double dg, double ry) -> double {
+        if constexpr (MODE == M_SPMV) return sum;
+        else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
+        else return __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), dg, ry));
+    };
+    pdl_wait();
+    if (!(skip && *skip)) {
+        for (int q = blockIdx.x * kCrossThreads + threadIdx.x, base = blockIdx.x * kCrossThreads; base < npairs;
+             q += stride, base += stride) {
+            if (base + stride >= npairs) pdl_trigger();
+            const bool in = q < npairs;
+            const unsigned inm = __ballot_sync(0xffffffffu, in);
+            if (!inm) continue;
+            const int r0w = __shfl_sync(0xffffffffu, 2 * q, __ffs(inm) - 1);
+            const int r = in ? 2 * q : r0w;
+            const uint16_t pp = *reinterpret_cast<const uint16_t *>(pid + r);
+            const int p0 = pp & 0xff, p1 = pp >> 8;
+            const uint32_t m0 = __ldg(rmask + p0), m1 = __ldg(rmask + p1);
+            const bool fast = m0 && m1 && r >= lo && r < hi;
+            if (__all_sync(0xffffffffu, fast)) {
+                const double2 fv = (MODE == M_SPMV) ? make_double2(0.0, 0.0) : __ldg(reinterpret_cast<const double2 *>(f + r));
+                const double *xr = x + r;
+                // x values per slot for row r (a) and row r + 1 (b)
+                double a[W], b[W];
+                {
+                    const double2 A = __ldg(reinterpret_cast<const double2 *>(xr - 2));
+                    const double2 B = __ldg(reinterpret_cast<const double2 *>(xr));
+                    const double2 Cc = __ldg(reinterpret_cast<const double2 *>(xr + 2));
+                    a[C - 1] = A.y; a[C] = B.x; a[C + 1] = B.y;
+                    b[C - 1] = B.x; b[C] = B.y; b[C + 1] = Cc.x;
+                }
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    if (k >= C - 1 && k <= C + 1) continue;
+                    const double2 v2 = __ldg(reinterpret_cast<const double2 *>(at_off(xr, mp.o[k])));
+                    a[k] = v2.x;
+                    b[k] = v2.y;
+                }
+                double s0 = 0.0, s1 = 0.0;
+                if (__all_sync(0xffffffffu, (m0 & m1) == (1u << W) - 1u)) {
+#pragma unroll
+                    for (int k = 0; k < W; ++k) {
+                        s0 = __dadd_rn(s0, __dmul_rn(mp.v[k], a[k]));
+                        s1 = __dadd_rn(s1, __dmul_rn(mp.v[k], b[k]));
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < W; ++k) {
+                        s0 = __dadd_rn(s0, ((m0 >> k) & 1u) ? __dmul_rn(mp.v[k], a[k]) : 0.0);
+                        s1 = __dadd_rn(s1, ((m1 >> k) & 1u) ? __dmul_rn(mp.v[k], b[k]) : 0.0);
+                    }
+                }
+                if (in) {
+                    const double o0 = fin(a[C], fv.x, s0, mp.d, mp.r), o1 = fin(b[C], fv.y, s1, mp.d, mp.r);
+                    if constexpr (NV == 0) {
+                        *reinterpret_cast<double2 *>(out + r) = make_double2(o0, o1);
+                    } else {
+                        emit(r, o0, fv.x, a[C]);
+                        emit(r + 1, o1, fv.y, b[C]);
+                    }
+                }
+            } else if (in) {  // the row-pattern per-row path for both rows
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    const int row = r + h, p = h ? p1 : p0;
+                    const double *xrow = x + row;
+                    const double xi = __ldg(xrow);
+                    const double fi = (MODE == M_SPMV) ? 0.0 : __ldg(f + row);
+                    double sum = 0.0;
+                    const int len = T.l(p);
+                    for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(T.v(p, k), __ldg(xrow + T.o(p, k))));
+                    emit(row, fin(xi, fi, sum, T.d(p), T.r(p)), fi, xi);
+                }
+            }
+        }
+    }
+    if constexpr (NV > 0) finish_reduction<NV>(red, acc);
+}

@@ -1687,8 +1687,18 @@ static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double
     if constexpr (MODE == M_JACOBI || MODE == M_SPMV || MODE == M_RESID) {
         auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
         if (l.pat && l.box_pair && a16(x) && a16(out) && (MODE == M_SPMV || a16(f))) {
-            launch_k(c, k_boxpair<MODE, NV>, dim3(l.box_grid), dim3(kBoxThreads), l.pat_tb, s, static_cast<int>(l.n),
-                     l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<28>(l), x, f, out, omega, skip, red);
+            if (l.box_pair == 1)
+                launch_k(c, k_boxpair<MODE, NV>, dim3(l.box_grid), dim3(kBoxThreads), l.pat_tb, s,
+                         static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<28>(l), x, f,
+                         out, omega, skip, red);
+            else if (l.pat_w == 7)
+                launch_k(c, k_crosspair<MODE, NV, 7>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
+                         static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<7>(l), x, f,
+                         out, omega, skip, red);
+            else
+                launch_k(c, k_crosspair<MODE, NV, 5>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
+                         static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<5>(l), x, f,
+                         out, omega, skip, red);
             return;
         }
         if (l.pat && l.march_geo >= 0) {
@@ -2260,20 +2270,33 @@ static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
         D.main_o.assign(off + static_cast<size_t>(q) * wo, off + static_cast<size_t>(q) * wo + w);
     }
     build_march(c, D, np, w, val, off, len);
-    {  // k_boxpair: main pattern a 27-point box with even line / plane strides, n even
+    {  // row-pair kernels: main pattern a 27-point box (k_boxpair) or a 7/5-point
+       // cross (k_crosspair) with even strides, n even
         const char *bp = std::getenv("SB_BOXPAIR");
-        int P = 0, N = 0;
-        if (!(bp && std::atoi(bp) == 0) && w == 28 && A.n % 2 == 0 && A.n >= 2 && march_geo_ok<0>(D, P, N) &&
-            P % 2 == 0 && N % 2 == 0) {
+        int P = 0, N = 0, kind = 0;
+        const std::vector<int> &mo = D.main_o;
+        if (!(bp && std::atoi(bp) == 0) && A.n % 2 == 0 && A.n >= 2) {
+            if (w == 28 && march_geo_ok<0>(D, P, N) && P % 2 == 0 && N % 2 == 0) kind = 1;
+            if (w == 7 && D.main_len == 7 && mo[0] == -mo[6] && mo[1] == -mo[5] && mo[2] == -1 && mo[3] == 0 &&
+                mo[4] == 1 && mo[5] > 1 && mo[6] > mo[5] && mo[5] % 2 == 0 && mo[6] % 2 == 0)
+                kind = 2;
+            // (the 5-point 2D cross also works, SB_CROSS5=1, but measured slower on
+            // C1's coarse levels: 24.2 vs 22.8 ms)
+            const char *c5 = std::getenv("SB_CROSS5");
+            if (c5 && std::atoi(c5) != 0 && w == 5 && D.main_len == 5 && mo[0] == -mo[4] && mo[1] == -1 &&
+                mo[2] == 0 && mo[3] == 1 && mo[4] > 1 && mo[4] % 2 == 0)
+                kind = 2;
+        }
+        if (kind) {
             // restriction masks: pattern q = the main pattern with slots removed
             // (same offsets in order, same value bits where present), else 0
-            const int wv = (w + 1) & ~1, wo = (w + 3) & ~3;
+            const int wv = (w + 1) & ~1, wo = (w + 3) & ~3, W = D.main_len;
             std::vector<uint32_t> rm(static_cast<size_t>(np), 0u);
             for (int q = 0; q < np; ++q) {
                 uint32_t m = 0u;
                 int k = 0;
-                for (int j = 0; j < 27; ++j)
-                    if (k < len[q] && off[q * wo + k] == D.main_o[static_cast<size_t>(j)]) {
+                for (int j = 0; j < W; ++j)
+                    if (k < len[q] && off[q * wo + k] == mo[static_cast<size_t>(j)]) {
                         if (std::memcmp(&val[q * wv + k], &D.main_v[static_cast<size_t>(j)], 8) != 0) break;
                         m |= 1u << j;
                         ++k;
@@ -2283,7 +2306,7 @@ static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
             auto *dm = dalloc<uint32_t>(c, np);
             CK(cudaMemcpy(dm, rm.data(), sizeof(uint32_t) * rm.size(), cudaMemcpyHostToDevice));
             D.box_rmask = dm;
-            D.box_pair = 1;
+            D.box_pair = kind;
         }
     }
     auto *dp = dalloc<uint8_t>(c, A.n + 16);
@@ -2560,6 +2583,8 @@ template <int MODE, int NV> static void set_smem_attr(size_t smem) {
     const int b = static_cast<int>(smem);
     if constexpr (MODE == M_JACOBI || MODE == M_SPMV || MODE == M_RESID) {
         CK(cudaFuncSetAttribute(k_boxpair<MODE, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_crosspair<MODE, NV, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        CK(cudaFuncSetAttribute(k_crosspair<MODE, NV, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     }
@@ -3078,8 +3103,14 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
         }
         if (l.box_pair) {
             occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_boxpair<M_JACOBI, 0>, kBoxThreads, l.pat_tb));
-            const int64_t need = (l.n / 2 + kBoxThreads - 1) / kBoxThreads;
+            const int th = l.box_pair == 1 ? kBoxThreads : kCrossThreads;
+            if (l.box_pair == 1)
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_boxpair<M_JACOBI, 0>, th, l.pat_tb));
+            else if (l.pat_w == 7)
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_crosspair<M_JACOBI, 0, 7>, th, l.pat_tb));
+            else
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_crosspair<M_JACOBI, 0, 5>, th, l.pat_tb));
+            const int64_t need = (l.n / 2 + th - 1) / th;
             l.box_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
         }
         if (l.march_geo >= 0) {
@@ -3113,8 +3144,9 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
     // Krylov vectors; on a partitioned level 0 in the window layout the halo
     // below own row 0 lives at negative indices (vec_headroom rows)
     for (auto &v : c->kv) v = dalloc<double>(c, vec_headroom + n_vec) + vec_headroom;
-    int maxb = 148 * 8;
-    for (auto &l : c->L) maxb = std::max(maxb, l.ntiles);
+    int maxb = 148 * 8;  // reduction partials: one pair per CTA of any reducing kernel's grid
+    for (auto &l : c->L)
+        maxb = std::max({maxb, l.ntiles, l.grid, l.sell_grid, l.pat_grid, l.box_grid, l.march_grid});
     c->partials = dalloc<double>(c, 2 * static_cast<int64_t>(maxb) + 2, false);
     c->counter = dalloc<unsigned>(c, 4, false);
     c->st = dalloc<DevState>(c, 1, false);
@@ -3250,7 +3282,8 @@ int sb_level_sweep_kernel(sb_ctx c, int k, char *buf, int cap) {
     return guard([&] {
         const DevLevel &l = level_of(c, k);
         if (!buf || cap < 1) throw invalid_argument("sb_level_sweep_kernel: no buffer");
-        const char *name = l.pat ? (l.box_pair ? "k_boxpair" : l.march_geo >= 0 ? "k_march" : "k_rowpat")
+        const char *name = l.pat ? (l.box_pair == 1 ? "k_boxpair" : l.box_pair == 2 ? "k_crosspair"
+                                    : l.march_geo >= 0 ? "k_march" : "k_rowpat")
                                  : l.sell ? "k_sellg" : "k_csr_tile";
         std::snprintf(buf, static_cast<size_t>(cap), "%s", name);
     });

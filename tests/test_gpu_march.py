@@ -133,13 +133,22 @@ def _sweep_kernel(sp, A_or_h, level=0):
     return buf.value.decode()
 
 
-@pytest.mark.parametrize("case", ["p27", "varied", "varied-odd", "poisson7"])
+@pytest.mark.parametrize("case", ["p27", "varied", "varied-odd", "poisson7", "convdiff7", "aniso7-odd",
+                                  "poisson5", "poisson5-odd"])
 def test_boxpair_kernels_bitexact(sp, oracle_best, case, monkeypatch):
+    # k_boxpair (27-point box) / k_crosspair (7- and 5-point cross): row pairs,
+    # 16-byte loads, restriction masks for boundary rows; odd strides keep k_rowpat
     monkeypatch.setenv("SB_BOXPAIR", "1")
+    monkeypatch.setenv("SB_CROSS5", "1")
     A, want_k = {"p27": (lambda: _p27(sp, 40, 10, 40), "k_boxpair"),
                  "varied": (lambda: stencil27_varied(sp, 64, 6, 9, seed=8), "k_boxpair"),
                  "varied-odd": (lambda: stencil27_varied(sp, 33, 17, 12, seed=9), "k_rowpat"),  # odd N
-                 "poisson7": (lambda: sp.poisson3d(34, 12, 20), "k_rowpat")}[case]
+                 "poisson7": (lambda: sp.poisson3d(34, 12, 20), "k_crosspair"),
+                 "convdiff7": (lambda: sp.convdiff3d(36, 10, 14, 1.0, 100.0, 1.0, 1.0), "k_crosspair"),
+                 "aniso7-odd": (lambda: sp.stencil7(45, 13, 21, 4.002, [-1.0, -1.0, -1.0, -1.0, -1e-3, -1e-3]),
+                                "k_rowpat"),
+                 "poisson5": (lambda: sp.poisson2d(46, 30), "k_crosspair"),
+                 "poisson5-odd": (lambda: sp.poisson2d(45, 29), "k_rowpat")}[case]
     A = A()
     assert _sweep_kernel(sp, A) == want_k
     n = A.nrows()
@@ -155,11 +164,14 @@ def test_boxpair_kernels_bitexact(sp, oracle_best, case, monkeypatch):
     assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x), equal_nan=True)
 
 
-def test_boxpair_vcycle_pcg_identical(sp, monkeypatch):
-    A = _p27(sp, 48, 16, 40)
+@pytest.mark.parametrize("which", ["p27", "p7", "p5"])
+def test_boxpair_vcycle_pcg_identical(sp, which, monkeypatch):
+    A = {"p27": lambda: _p27(sp, 48, 16, 40), "p7": lambda: sp.poisson3d(64, 40, 40),
+         "p5": lambda: sp.poisson2d(256, 200)}[which]()
     cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40)
     b = sp.rhs_ones(A.nrows())
     cp = sp.CycleParams.from_config(cfg)
+    monkeypatch.setenv("SB_CROSS5", "1")
     out = {}
     for on in ("1", "0"):
         monkeypatch.setenv("SB_BOXPAIR", on)
@@ -168,7 +180,8 @@ def test_boxpair_vcycle_pcg_identical(sp, monkeypatch):
         v = sp.vcycle(h, 0, b, np.zeros(A.nrows()), cp)
         r = sp.pcg(A, b, sp.make_amg_preconditioner(h, cp), 1e-8 * float(np.linalg.norm(b)), 200)
         out[on] = (ks, v, r)
-    assert "k_boxpair" in out["1"][0] and "k_boxpair" not in out["0"][0]
+    pair = "k_boxpair" if which == "p27" else "k_crosspair"
+    assert pair in out["1"][0] and pair not in out["0"][0]
     assert np.array_equal(out["1"][1], out["0"][1])
     assert out["1"][2].report.iterations == out["0"][2].report.iterations
     assert np.linalg.norm(out["1"][2].x - out["0"][2].x) <= 1e-12 * np.linalg.norm(out["0"][2].x)

@@ -5,7 +5,7 @@
 mkdir -p gpurun_out
 for W in ${@:-C2 C1 C3 C4 T256 P27_256}; do
   timeout 900 ncu --nvtx --nvtx-include 'prof/' --set full --import-source on --clock-control none \
-     -k regex:k_rowpat --launch-skip 0 --launch-count 1 \
+     -k regex:'k_rowpat|k_crosspair|k_boxpair|k_sellg' --launch-skip 0 --launch-count 1 \
      -o gpurun_out/l0_$W -f python tools/profile_vcycle.py $W vcycle > gpurun_out/prof_l0_$W.log 2>&1
   tail -1 gpurun_out/prof_l0_$W.log
 done
