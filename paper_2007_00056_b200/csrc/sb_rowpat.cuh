@@ -593,3 +593,85 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
     }
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
 }
+
+// Residual + restriction (k_pat_resid_restrict) on 7-point cross levels with
+// even strides when coarse row c's members are a row pair (2k, 2k + 1): node-HEM
+// on a grid pairs each row with its right neighbour, so at the fine levels of
+// C2-C4 every aggregate is one. The pair's two residuals come from
+// k_crosspair's 16-byte loads; f_c = (0 + r_m0) + r_m1 and the coarse level's
+// first sweep x0_c = 0 + (w f_c) / a_cc exactly as k_pat_resid_restrict
+// (csr.hpp:267-274, 232-239). Warps with another aggregate or pattern shape
+// take the per-member path. Bitwise equal, but measured slower than
+// k_pat_resid_restrict (C2 solve 14.07 vs 13.70 ms): opt-in, SB_CROSS_RR=1.
+template <int W>
+__global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
+    k_cross_rr(int nc, const int2 *__restrict__ mem, int n, const uint8_t *__restrict__ pid, int np,
+               const unsigned char *__restrict__ table, const uint32_t *__restrict__ rmask,
+               const __grid_constant__ MainPat<W> mp, const double *__restrict__ x, const double *__restrict__ f,
+               double *__restrict__ fc, const double *__restrict__ dc, double *__restrict__ xc0, double omega) {
+    constexpr int C = W / 2;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const SmemTab<W> T = smem_tab<W>(smem, table, np);
+    const int lo = -mp.o[0] + 2, hi = n - (mp.o[W - 1] + 3);
+    const int stride = gridDim.x * kCrossThreads;
+    auto resid = [&](int m, int p) {  // r_m = f_m - A_m x, the reference's order
+        double sum = 0.0;
+        const int len = T.l(p);
+        for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(T.v(p, k), __ldg(x + m + T.o(p, k))));
+        return __dsub_rn(__ldg(f + m), sum);
+    };
+    pdl_wait();
+    for (int c = blockIdx.x * kCrossThreads + threadIdx.x, base = blockIdx.x * kCrossThreads; base < nc;
+         c += stride, base += stride) {
+        if (base + stride >= nc) pdl_trigger();
+        const bool in = c < nc;
+        const unsigned inm = __ballot_sync(0xffffffffu, in);
+        if (!inm) continue;
+        const int cw = __shfl_sync(0xffffffffu, c, __ffs(inm) - 1);
+        const int2 mm = __ldg(mem + (in ? c : cw));
+        const int r = mm.x;
+        bool fast = mm.y == r + 1 && (r & 1) == 0 && r >= lo && r < hi;
+        uint32_t m0 = 0u, m1 = 0u;
+        if (fast) {
+            const uint16_t pp = *reinterpret_cast<const uint16_t *>(pid + r);
+            m0 = __ldg(rmask + (pp & 0xff));
+            m1 = __ldg(rmask + (pp >> 8));
+            fast = m0 && m1;
+        }
+        double s;
+        if (__all_sync(0xffffffffu, fast)) {
+            const double *xr = x + r;
+            double a[W], b[W];
+            {
+                const double2 A = __ldg(reinterpret_cast<const double2 *>(xr - 2));
+                const double2 B = __ldg(reinterpret_cast<const double2 *>(xr));
+                const double2 Cc = __ldg(reinterpret_cast<const double2 *>(xr + 2));
+                a[C - 1] = A.y; a[C] = B.x; a[C + 1] = B.y;
+                b[C - 1] = B.x; b[C] = B.y; b[C + 1] = Cc.x;
+            }
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                if (k >= C - 1 && k <= C + 1) continue;
+                const double2 v2 = __ldg(reinterpret_cast<const double2 *>(at_off(xr, mp.o[k])));
+                a[k] = v2.x;
+                b[k] = v2.y;
+            }
+            const double2 fv = __ldg(reinterpret_cast<const double2 *>(f + r));
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                s0 = __dadd_rn(s0, ((m0 >> k) & 1u) ? __dmul_rn(mp.v[k], a[k]) : 0.0);
+                s1 = __dadd_rn(s1, ((m1 >> k) & 1u) ? __dmul_rn(mp.v[k], b[k]) : 0.0);
+            }
+            s = __dadd_rn(__dadd_rn(0.0, __dsub_rn(fv.x, s0)), __dsub_rn(fv.y, s1));
+        } else {
+            if (!in) continue;
+            s = __dadd_rn(0.0, resid(mm.x, pid[mm.x]));
+            if (mm.y >= 0) s = __dadd_rn(s, resid(mm.y, pid[mm.y]));
+        }
+        if (in) {
+            fc[c] = s;
+            if (xc0) xc0[c] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), __ldg(dc + c)));
+        }
+    }
+}

@@ -1571,6 +1571,11 @@ static CondSet conds(std::initializer_list<cudaGraphConditionalHandle> hs) {
 
 // ---- launchers (each counts the kernels it emits) -------------------------------
 
+static const bool c_cross_rr_off = [] {  // opt-in (SB_CROSS_RR=1): measured slower than k_pat_resid_restrict
+    const char *e = std::getenv("SB_CROSS_RR");   // (C2 14.07 vs 13.70 ms, T256 98.0 vs 97.6 ms)
+    return !(e && std::atoi(e) != 0);
+}();
+
 static const bool c_main_off = [] {  // SB_MAIN_PAT=0: every warp reads the shared-memory table (A/B only)
     const char *e = std::getenv("SB_MAIN_PAT");
     return e && std::atoi(e) == 0;
@@ -1740,6 +1745,15 @@ static void launch_pat_rr_w(sb_ctx c, const DevLevel &l, const DevLevel &lc, cud
 
 static void launch_pat_rr(sb_ctx c, const DevLevel &l, const DevLevel &lc, cudaStream_t s, const double *x,
                           const double *f, double *x0, double omega) {
+    auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (l.box_pair == 2 && l.pat_w == 7 && a16(x) && a16(f) && !c_cross_rr_off) {
+        const int grid = static_cast<int>(std::max<int64_t>(
+            1, std::min<int64_t>((lc.n + kCrossThreads - 1) / kCrossThreads, static_cast<int64_t>(l.box_grid))));
+        launch_k(c, k_cross_rr<7>, dim3(grid), dim3(kCrossThreads), l.pat_tb, s, static_cast<int>(lc.n),
+                 static_cast<const int2 *>(l.mem), static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask,
+                 main_pat<7>(l), x, f, lc.f, static_cast<const double *>(lc.diag), x0, omega);
+        return;
+    }
     switch (l.pat_w) {
     case 5: return launch_pat_rr_w<5>(c, l, lc, s, x, f, x0, omega);
     case 7: return launch_pat_rr_w<7>(c, l, lc, s, x, f, x0, omega);
@@ -2585,6 +2599,8 @@ template <int MODE, int NV> static void set_smem_attr(size_t smem) {
         CK(cudaFuncSetAttribute(k_boxpair<MODE, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_crosspair<MODE, NV, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_crosspair<MODE, NV, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        if constexpr (MODE == M_RESID && NV == 0)
+            CK(cudaFuncSetAttribute(k_cross_rr<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     }

@@ -185,3 +185,25 @@ def test_boxpair_vcycle_pcg_identical(sp, which, monkeypatch):
     assert np.array_equal(out["1"][1], out["0"][1])
     assert out["1"][2].report.iterations == out["0"][2].report.iterations
     assert np.linalg.norm(out["1"][2].x - out["0"][2].x) <= 1e-12 * np.linalg.norm(out["0"][2].x)
+
+
+def test_cross_rr_vcycle_identical():
+    # k_cross_rr (opt-in, read once per process): residual + restriction from row
+    # pairs gives bitwise the same V-cycle as k_pat_resid_restrict
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from paper_2007_00056_b200 import sparsh as sp; "
+            "A = sp.poisson3d(64, 40, 40); "
+            "cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40); "
+            "h = sp.Hierarchy(A, cfg); b = sp.rhs_random(A.nrows(), 5); "
+            "v = sp.vcycle(h, 0, b, np.zeros(A.nrows()), sp.CycleParams.from_config(cfg)); "
+            "sys.stdout.write(v.tobytes().hex())") % root
+    vs = []
+    for on in ("1", "0"):
+        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SB_CROSS_RR=on), capture_output=True,
+                             text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        vs.append(out.stdout)
+    assert vs[0] and vs[0] == vs[1]
