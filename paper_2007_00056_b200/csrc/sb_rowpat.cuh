@@ -398,6 +398,12 @@ __global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
         else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
         else return __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), dg, ry));
     };
+    // the pattern bytes are constant: the first pair's before the dependency
+    // wait, later ones one iteration ahead
+    auto pair_of = [&](int qq) {
+        return static_cast<uint32_t>(*reinterpret_cast<const uint16_t *>(pid + 2 * min(qq, npairs - 1)));
+    };
+    uint32_t ppn = npairs > 0 ? pair_of(blockIdx.x * kBoxThreads + threadIdx.x) : 0u;
     pdl_wait();
     if (!(skip && *skip)) {
         for (int q = blockIdx.x * kBoxThreads + threadIdx.x, base = blockIdx.x * kBoxThreads; base < npairs;
@@ -405,11 +411,15 @@ __global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
             if (base + stride >= npairs) pdl_trigger();
             const bool in = q < npairs;
             const unsigned inm = __ballot_sync(0xffffffffu, in);
+            const uint32_t ppc = ppn;
+            if (base + stride < npairs) ppn = pair_of(q + stride);
             if (!inm) continue;
             // lanes past the end shadow the warp's first pair (in bounds, not stored)
-            const int r0w = __shfl_sync(0xffffffffu, 2 * q, __ffs(inm) - 1);
+            const int src = __ffs(inm) - 1;
+            const int r0w = __shfl_sync(0xffffffffu, 2 * q, src);
+            const uint32_t pps = __shfl_sync(0xffffffffu, ppc, src);
             const int r = in ? 2 * q : r0w;
-            const uint16_t pp = *reinterpret_cast<const uint16_t *>(pid + r);
+            const uint32_t pp = in ? ppc : pps;
             const int p0 = pp & 0xff, p1 = pp >> 8;
             // restriction masks: the pattern is the main one with some slots absent
             // and the same values elsewhere (0: not a restriction)
@@ -520,6 +530,12 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
         else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
         else return __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), dg, ry));
     };
+    // the pattern bytes are constant: the first pair's before the dependency
+    // wait, later ones one iteration ahead
+    auto pair_of = [&](int qq) {
+        return static_cast<uint32_t>(*reinterpret_cast<const uint16_t *>(pid + 2 * min(qq, npairs - 1)));
+    };
+    uint32_t ppn = npairs > 0 ? pair_of(blockIdx.x * kCrossThreads + threadIdx.x) : 0u;
     pdl_wait();
     if (!(skip && *skip)) {
         for (int q = blockIdx.x * kCrossThreads + threadIdx.x, base = blockIdx.x * kCrossThreads; base < npairs;
@@ -527,10 +543,14 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
             if (base + stride >= npairs) pdl_trigger();
             const bool in = q < npairs;
             const unsigned inm = __ballot_sync(0xffffffffu, in);
+            const uint32_t ppc = ppn;
+            if (base + stride < npairs) ppn = pair_of(q + stride);
             if (!inm) continue;
-            const int r0w = __shfl_sync(0xffffffffu, 2 * q, __ffs(inm) - 1);
+            const int src = __ffs(inm) - 1;
+            const int r0w = __shfl_sync(0xffffffffu, 2 * q, src);
+            const uint32_t pps = __shfl_sync(0xffffffffu, ppc, src);
             const int r = in ? 2 * q : r0w;
-            const uint16_t pp = *reinterpret_cast<const uint16_t *>(pid + r);
+            const uint32_t pp = in ? ppc : pps;
             const int p0 = pp & 0xff, p1 = pp >> 8;
             const uint32_t m0 = __ldg(rmask + p0), m1 = __ldg(rmask + p1);
             const bool fast = m0 && m1 && r >= lo && r < hi;
