@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
 // first sweep x0_c = 0 + (w f_c) / a_cc exactly as k_pat_resid_restrict
 // (csr.hpp:267-274, 232-239). Warps with another aggregate or pattern shape
 // take the per-member path. Bitwise equal, but measured slower than
-// k_pat_resid_restrict (C2 solve 14.07 vs 13.70 ms): opt-in, SB_CROSS_RR=1.
+// k_pat_resid_restrict (C2 solve 13.92 vs 13.61 ms with the prefetch below): opt-in, SB_CROSS_RR=1.
 template <int W>
 __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
     k_cross_rr(int nc, const int2 *__restrict__ mem, int n, const uint8_t *__restrict__ pid, int np,
@@ -640,20 +640,38 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
         for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(T.v(p, k), __ldg(x + m + T.o(p, k))));
         return __dsub_rn(__ldg(f + m), sum);
     };
+    // members and pattern bytes are constant: the first coarse row's before the
+    // dependency wait, later ones one iteration ahead
+    struct Pre {
+        int2 mm;
+        uint32_t pp;
+    };
+    auto pre_of = [&](int cc) {
+        Pre q;
+        q.mm = __ldg(mem + min(cc, nc - 1));
+        const bool pair = q.mm.y == q.mm.x + 1 && (q.mm.x & 1) == 0;
+        q.pp = pair ? static_cast<uint32_t>(*reinterpret_cast<const uint16_t *>(pid + q.mm.x)) : 0xffffffffu;
+        return q;
+    };
+    Pre nx = pre_of(blockIdx.x * kCrossThreads + threadIdx.x);
     pdl_wait();
     for (int c = blockIdx.x * kCrossThreads + threadIdx.x, base = blockIdx.x * kCrossThreads; base < nc;
          c += stride, base += stride) {
         if (base + stride >= nc) pdl_trigger();
         const bool in = c < nc;
         const unsigned inm = __ballot_sync(0xffffffffu, in);
+        const Pre cur = nx;
+        if (base + stride < nc) nx = pre_of(c + stride);
         if (!inm) continue;
-        const int cw = __shfl_sync(0xffffffffu, c, __ffs(inm) - 1);
-        const int2 mm = __ldg(mem + (in ? c : cw));
+        const int src = __ffs(inm) - 1;
+        const int2 mw = make_int2(__shfl_sync(0xffffffffu, cur.mm.x, src), __shfl_sync(0xffffffffu, cur.mm.y, src));
+        const uint32_t pw = __shfl_sync(0xffffffffu, cur.pp, src);
+        const int2 mm = in ? cur.mm : mw;
+        const uint32_t pp = in ? cur.pp : pw;
         const int r = mm.x;
-        bool fast = mm.y == r + 1 && (r & 1) == 0 && r >= lo && r < hi;
+        bool fast = pp != 0xffffffffu && r >= lo && r < hi;
         uint32_t m0 = 0u, m1 = 0u;
         if (fast) {
-            const uint16_t pp = *reinterpret_cast<const uint16_t *>(pid + r);
             m0 = __ldg(rmask + (pp & 0xff));
             m1 = __ldg(rmask + (pp >> 8));
             fast = m0 && m1;
