@@ -2294,10 +2294,12 @@ static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
             if (w == 7 && D.main_len == 7 && mo[0] == -mo[6] && mo[1] == -mo[5] && mo[2] == -1 && mo[3] == 0 &&
                 mo[4] == 1 && mo[5] > 1 && mo[6] > mo[5] && mo[5] % 2 == 0 && mo[6] % 2 == 0)
                 kind = 2;
-            // (the 5-point 2D cross also works, SB_CROSS5=1, but measured slower on
-            // C1's coarse levels: 24.2 vs 22.8 ms)
+            // 5-point 2D cross: faster on large levels (C1 L0 5.3 vs 5.7 us) but slower
+            // on 2D coarse levels (V-cycle 0.364 vs 0.343 ms with every level), so
+            // only levels >= 2^19 rows (SB_CROSS5=1: every level, =0: none)
             const char *c5 = std::getenv("SB_CROSS5");
-            if (c5 && std::atoi(c5) != 0 && w == 5 && D.main_len == 5 && mo[0] == -mo[4] && mo[1] == -1 &&
+            const bool c5_on = c5 ? std::atoi(c5) != 0 : A.n >= (int64_t(1) << 19);
+            if (c5_on && w == 5 && D.main_len == 5 && mo[0] == -mo[4] && mo[1] == -1 &&
                 mo[2] == 0 && mo[3] == 1 && mo[4] > 1 && mo[4] % 2 == 0)
                 kind = 2;
         }
