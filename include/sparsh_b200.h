@@ -100,7 +100,9 @@ typedef struct {
 /* Device-context options. */
 typedef struct {
     int device;          /* CUDA ordinal */
-    int use_graphs;      /* 1: whole-solve CUDA graph with device-side loop control (default) */
+    int use_graphs;      /* 1: whole-solve CUDA graph with device-side loop control (default);
+                            0: eager launches on sb_stream, host-side loop control (same kernels,
+                            same bits; one host sync per conditional decision) */
     int64_t host_levels_from; /* hybrid mode (paper's MI scheme): the matrix storage of levels
                                  >= this index stays in pinned host memory and the device
                                  kernels read it over the host link (zero-copy; no CPU
@@ -190,6 +192,9 @@ int sb_pbicgstab_dev(sb_ctx ctx, const sb_cycle *cp, const double *d_b, double *
 
 /* CUDA-event time (ms) of the last whole-solve graph launch on sb_stream. */
 double sb_last_solve_ms(sb_ctx ctx);
+/* Kernels the last solve executed on the device (graph mode: counted from the
+ * captured graph's structure and the iteration count; eager mode: launched). */
+int64_t sb_last_solve_launches(sb_ctx ctx);
 /* Times `reps` back-to-back launches of one kernel on level `level` with CUDA
  * events on sb_stream; *avg_ms = mean per launch. kind: 0 Jacobi sweep,
  * 1 SpMV, 2 residual, 3 one V-cycle from x = 0 launched eagerly, 4 the same
@@ -197,6 +202,10 @@ double sb_last_solve_ms(sb_ctx ctx);
  * *launches = kernels launched per repetition. */
 int sb_time_kernel(sb_ctx ctx, int kind, int level, const sb_cycle *cp, int reps, double *avg_ms,
                    int *launches);
+/* Same, with a cold L2: before every launch a write of flush_bytes (> the
+ * 126 MB L2) on sb_stream, and one event pair around each launch. */
+int sb_time_kernel_cold(sb_ctx ctx, int kind, int level, const sb_cycle *cp, int reps, int64_t flush_bytes,
+                        double *avg_ms, int *launches);
 /* Diagnostics: tail-kernel phase timestamps (needs SB_TAIL_TRACE=1 at
  * sb_create) and the tail placement (first tail level, cluster CTAs, smem). */
 int sb_tail_trace(sb_ctx ctx, unsigned long long *out, int cap);

@@ -157,8 +157,15 @@ public:
         : Hierarchy() {
         std::vector<sb_csr> ls;
         std::vector<const int32_t *> ag;
+        if (levels.empty() || aggs.size() + 1 != levels.size())
+            throw std::invalid_argument("Hierarchy: need one aggregation per level but the coarsest");
         for (const auto &m : levels) ls.push_back(m.abi());
-        for (const auto &a : aggs) ag.push_back(a.data());
+        for (std::size_t k = 0; k < aggs.size(); ++k) {
+            if (static_cast<std::int64_t>(aggs[k].size()) != levels[k].nrows())
+                throw std::invalid_argument("Hierarchy: aggregation " + std::to_string(k) +
+                                            " does not cover level " + std::to_string(k));
+            ag.push_back(aggs[k].data());
+        }
         sb_hier h = nullptr;
         detail::check(sb_hier_from_levels(static_cast<int>(ls.size()), ls.data(), ag.data(), &h));
         hier_.reset(h);

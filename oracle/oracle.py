@@ -245,6 +245,10 @@ class Ref:
         L.ref_set_threads.argtypes = [C.c_uint]
         L.ref_csr_new.argtypes = [C.c_int32, C.c_int32, _I, _I, _D, C.POINTER(P)]
         L.ref_convdiff2d.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.POINTER(P)]
+        L.ref_stencil7.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_double, _D, C.POINTER(P)]
+        L.ref_convdiff3d.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                     C.c_double, C.POINTER(P)]
+        L.ref_stencil27.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.POINTER(P)]
         L.ref_csr_free.argtypes = [P]
         L.ref_csr_info.argtypes = [P, _I, _I, C.POINTER(C.c_int64)]
         L.ref_csr_copy.argtypes = [P, _I, _I, _D]
@@ -301,6 +305,47 @@ class Ref:
         self.check(self.L.ref_convdiff2d(nx, ny, bx, by, c, C.byref(h)))
         return RefMatrix(self, h)
 
+    # 3D generators (ref_capi.cpp: triplets through the reference's from_triplets)
+    def stencil7(self, nx, ny, nz, diag, off):
+        o = _d(off)
+        h = C.c_void_p()
+        self.check(self.L.ref_stencil7(nx, ny, nz, diag, o.ctypes.data_as(_D), C.byref(h)))
+        return RefMatrix(self, h)
+
+    def poisson3d(self, n):
+        return self.stencil7(n, n, n, 6.0, [-1.0] * 6)
+
+    def aniso3d(self, n, eps=1e-3):
+        return self.stencil7(n, n, n, 4.0 + 2.0 * eps, [-1.0, -1.0, -1.0, -1.0, -eps, -eps])
+
+    def convdiff3d(self, nx, ny, nz, bx, by, bz, c):
+        h = C.c_void_p()
+        self.check(self.L.ref_convdiff3d(nx, ny, nz, bx, by, bz, c, C.byref(h)))
+        return RefMatrix(self, h)
+
+    def stencil27(self, nx, ny, nz, diag=26.0, off=-1.0):
+        h = C.c_void_p()
+        self.check(self.L.ref_stencil27(nx, ny, nz, diag, off, C.byref(h)))
+        return RefMatrix(self, h)
+
+    def problem(self, name):
+        """The BASELINE workloads, generated by the reference build."""
+        if name == "C1":
+            return self.convdiff2d(1024, 1024, 0.0, 0.0, 0.0)
+        if name == "C2":
+            return self.poisson3d(128)
+        if name == "C3":
+            return self.aniso3d(256, 1e-3)
+        if name == "C4":
+            return self.convdiff3d(256, 256, 256, 1.0, 100.0, 1.0, 1.0)
+        if name == "T256":
+            return self.poisson3d(256)
+        if name == "P27_128":
+            return self.stencil27(128, 128, 128)
+        if name == "G128":
+            return self.matrix(ArraysCsr(*graph_laplacian3d_arrays(128, seed=7)))
+        raise ValueError(f"unknown problem {name}")
+
     def spmv(self, A, x):
         return self.matrix(A).spmv(x)
 
@@ -314,7 +359,7 @@ class Ref:
         return self.matrix(A).node_hem()
 
     def hierarchy(self, A, coarse_target=500, max_levels=40):
-        m = self.matrix(A)
+        m = A if isinstance(A, RefMatrix) else self.matrix(A)
         return RefHier(self, m, coarse_target, max_levels)
 
 
@@ -334,6 +379,14 @@ class RefMatrix:
         v = np.empty(z.value)
         self.R.L.ref_csr_copy(self.h, rp.ctypes.data_as(_I), ci.ctypes.data_as(_I), v.ctypes.data_as(_D))
         return rp, ci, v
+
+    def nrows(self):
+        return self._n()[0]
+
+    def nnz(self):
+        n, m, z = C.c_int32(), C.c_int32(), C.c_int64()
+        self.R.L.ref_csr_info(self.h, C.byref(n), C.byref(m), C.byref(z))
+        return z.value
 
     def _n(self):
         n, m, z = C.c_int32(), C.c_int32(), C.c_int64()
@@ -443,3 +496,57 @@ def best_available():
         return Ref()
     except Exception:
         return Port()
+
+
+def graph_laplacian3d_arrays(m, seed=7, shift=0.01):
+    """(rp, ci, v) of bench.py's G128 operator (a 7-point graph Laplacian on m^3
+    with random edge weights U[0.5, 1.5) + shift*I) in plain numpy, so the
+    reference arm builds it without the product library. tests/test_oracle.py
+    asserts it equals paper_2007_00056_b200.sparsh.graph_laplacian3d bit for bit."""
+    n = m ** 3
+    rng = np.random.default_rng(seed)
+    idx = np.arange(n, dtype=np.int64).reshape(m, m, m)
+    rows, cols, vals = [], [], []
+    diag = np.full(n, shift)
+    for ax in range(3):
+        a = np.take(idx, np.arange(m - 1), axis=2 - ax).ravel()
+        b = np.take(idx, np.arange(1, m), axis=2 - ax).ravel()
+        w = rng.uniform(0.5, 1.5, a.size)
+        rows += [a, b]
+        cols += [b, a]
+        vals += [-w, -w]
+        np.add.at(diag, a, w)
+        np.add.at(diag, b, w)
+    r = np.concatenate(rows + [np.arange(n)])
+    c = np.concatenate(cols + [np.arange(n)])
+    v = np.concatenate(vals + [diag])
+    order = np.lexsort((c, r))
+    r, c, v = r[order], c[order], v[order]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, r + 1, 1)
+    return np.cumsum(rp).astype(np.int32), c.astype(np.int32), v
+
+
+class ArraysCsr:
+    """Minimal CSR view (row_ptr/col_idx/values/nrows/ncols) for Ref.matrix()."""
+
+    def __init__(self, rp, ci, v):
+        self._rp, self._ci, self._v = rp, ci, v
+
+    def row_ptr(self):
+        return self._rp
+
+    def col_idx(self):
+        return self._ci
+
+    def values(self):
+        return self._v
+
+    def nrows(self):
+        return self._rp.size - 1
+
+    def ncols(self):
+        return self._rp.size - 1
+
+    def nnz(self):
+        return int(self._rp[-1])

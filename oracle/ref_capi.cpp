@@ -11,6 +11,8 @@
 // Every entry point returns 0 on success, 1 for std::invalid_argument, 2 for
 // std::runtime_error (message via ref_last_error()).
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -100,6 +102,73 @@ int ref_csr_from_triplets(int32_t nrows, int32_t ncols, int64_t ntrip, const int
 }
 int ref_convdiff2d(int32_t nx, int32_t ny, double bx, double by, double c, void **out) {
     return guard([&] { *out = new CsrMatrix(convdiff2d(nx, ny, bx, by, c)); });
+}
+// 3D generators for the BASELINE configs, built the way the
+// reference's own 2D generators are (inc/problems.hpp:28-57): triplets of
+// (row, col, value) into CsrMatrix::from_triplets (inc/csr.hpp:57-95), which
+// sorts the columns and stores 0.0 + value. Node m = (iz*ny + iy)*nx + ix,
+// Dirichlet boundaries (out-of-grid neighbours dropped). These are test
+// infrastructure: bench.py's reference arm and tests/golden/make_config_fixtures.py
+// build their matrices here, so no product library is loaded on that path.
+// off = {x-, x+, y-, y+, z-, z+}.
+int ref_stencil7(int32_t nx, int32_t ny, int32_t nz, double diag, const double *off, void **out) {
+    return guard([&] {
+        if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("stencil7: grid dims must be >= 1");
+        const index_t n = nx * ny * nz;
+        std::vector<Triplet> e;
+        e.reserve(7 * static_cast<std::size_t>(n));
+        for (index_t iz = 0; iz < nz; ++iz)
+            for (index_t iy = 0; iy < ny; ++iy)
+                for (index_t ix = 0; ix < nx; ++ix) {
+                    const index_t m = (iz * ny + iy) * nx + ix;
+                    e.push_back({m, m, diag});
+                    if (ix > 0) e.push_back({m, m - 1, off[0]});
+                    if (ix < nx - 1) e.push_back({m, m + 1, off[1]});
+                    if (iy > 0) e.push_back({m, m - nx, off[2]});
+                    if (iy < ny - 1) e.push_back({m, m + nx, off[3]});
+                    if (iz > 0) e.push_back({m, m - nx * ny, off[4]});
+                    if (iz < nz - 1) e.push_back({m, m + nx * ny, off[5]});
+                }
+        *out = new CsrMatrix(CsrMatrix::from_triplets(n, n, std::move(e)));
+    });
+}
+// -lap(u) + b.grad(u) + c u on (0,1)^3, first-order upwinding scaled by the
+// cell volume: convdiff2d's expressions (inc/problems.hpp:34-41) extended to z.
+int ref_convdiff3d(int32_t nx, int32_t ny, int32_t nz, double bx, double by, double bz, double c,
+                   void **out) {
+    const double hx = 1.0 / (static_cast<double>(nx) + 1.0);
+    const double hy = 1.0 / (static_cast<double>(ny) + 1.0);
+    const double hz = 1.0 / (static_cast<double>(nz) + 1.0);
+    const double ax = hy * hz / hx, ay = hx * hz / hy, az = hx * hy / hz;
+    const double diag = 2.0 * (ax + ay + az) + std::abs(bx) * hy * hz + std::abs(by) * hx * hz +
+                        std::abs(bz) * hx * hy + c * hx * hy * hz;
+    const double off[6] = {-ax - std::max(bx, 0.0) * hy * hz, -ax + std::min(bx, 0.0) * hy * hz,
+                           -ay - std::max(by, 0.0) * hx * hz, -ay + std::min(by, 0.0) * hx * hz,
+                           -az - std::max(bz, 0.0) * hx * hy, -az + std::min(bz, 0.0) * hx * hy};
+    return ref_stencil7(nx, ny, nz, diag, off, out);
+}
+// 27-point box stencil (diag, `off` to all 26 neighbours).
+int ref_stencil27(int32_t nx, int32_t ny, int32_t nz, double diag, double off, void **out) {
+    return guard([&] {
+        if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("stencil27: grid dims must be >= 1");
+        const index_t n = nx * ny * nz;
+        std::vector<Triplet> e;
+        e.reserve(27 * static_cast<std::size_t>(n));
+        for (index_t iz = 0; iz < nz; ++iz)
+            for (index_t iy = 0; iy < ny; ++iy)
+                for (index_t ix = 0; ix < nx; ++ix) {
+                    const index_t m = (iz * ny + iy) * nx + ix;
+                    for (int dz = -1; dz <= 1; ++dz)
+                        for (int dy = -1; dy <= 1; ++dy)
+                            for (int dx = -1; dx <= 1; ++dx) {
+                                const index_t jx = ix + dx, jy = iy + dy, jz = iz + dz;
+                                if (jx < 0 || jy < 0 || jz < 0 || jx >= nx || jy >= ny || jz >= nz) continue;
+                                const index_t col = (jz * ny + jy) * nx + jx;
+                                e.push_back({m, col, col == m ? diag : off});
+                            }
+                }
+        *out = new CsrMatrix(CsrMatrix::from_triplets(n, n, std::move(e)));
+    });
 }
 void ref_csr_free(void *m) { delete static_cast<CsrMatrix *>(m); }
 // read_matrix_market / write_matrix_market (inc/mm_io.hpp)

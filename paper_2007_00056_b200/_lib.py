@@ -80,7 +80,7 @@ EXPORTS = [
     "sb_pcg", "sb_pbicgstab", "sb_amg_solve", "sb_pcg_dev", "sb_pbicgstab_dev", "sb_spmv",
     "sb_smooth", "sb_residual", "sb_restrict", "sb_prolong", "sb_coarse_solve",
     "sb_gen_convdiff2d", "sb_gen_stencil7", "sb_gen_convdiff3d", "sb_gen_stencil27",
-    "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_time_kernel", "sb_vcycle_launches", "sb_tail_trace",
+    "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_last_solve_launches", "sb_time_kernel", "sb_time_kernel_cold", "sb_vcycle_launches", "sb_tail_trace",
     "sb_tail_info", "sb_level_format", "sb_level_march", "sb_level_sweep_kernel", "sb_partition", "sb_partition_free", "sb_partition_info",
     "sb_partition_level", "sb_partition_exchange", "sb_nccl_unique_id", "sb_dist_create",
     "sb_dist_create_local", "sb_dist_destroy", "sb_dist_rows", "sb_dist_pcg", "sb_dist_pbicgstab",
@@ -130,7 +130,10 @@ _SIGS = {
     "sb_galerkin_gpu": (C.c_int, [C.POINTER(sb_csr), C.POINTER(C.c_int32), C.c_int64, C.c_int, C.POINTER(sb_csr)]),
     "sb_gen_rhs_random": (C.c_int, [C.c_int64, C.c_uint, _D]),
     "sb_last_solve_ms": (C.c_double, [_P]),
+    "sb_last_solve_launches": (C.c_int64, [_P]),
     "sb_time_kernel": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(sb_cycle), C.c_int, _D, C.POINTER(C.c_int)]),
+    "sb_time_kernel_cold": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(sb_cycle), C.c_int, C.c_int64, _D,
+                                      C.POINTER(C.c_int)]),
     "sb_vcycle_launches": (C.c_int, [_P, C.POINTER(sb_cycle)]),
     "sb_tail_trace": (C.c_int, [_P, C.POINTER(C.c_ulonglong), C.c_int]),
     "sb_tail_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),

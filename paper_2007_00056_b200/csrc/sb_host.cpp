@@ -333,10 +333,20 @@ int sb_hier_from_levels(int nlevels, const sb_csr *levels, const int32_t *const 
                 if (!f2c || !f2c[k]) throw invalid_argument("sb_hier_from_levels: missing aggregation");
                 L.agg.assign(f2c[k], f2c[k] + L.A.n);
                 L.n_coarse = levels[k + 1].nrows;
-                for (int32_t c : L.agg)
+                // Aggregation::validate (inc/aggregation.hpp:42-58): a surjection
+                // with 1 or 2 fine nodes per coarse node (the device restriction
+                // stores at most two members per aggregate)
+                std::vector<int32_t> count(static_cast<size_t>(L.n_coarse), 0);
+                for (int32_t c : L.agg) {
                     if (c < 0 || c >= L.n_coarse)
                         throw invalid_argument("Aggregation: coarse index " + std::to_string(c) +
                                                " outside [0, " + std::to_string(L.n_coarse) + ")");
+                    ++count[static_cast<size_t>(c)];
+                }
+                for (int64_t c = 0; c < L.n_coarse; ++c)
+                    if (count[c] < 1 || count[c] > 2)
+                        throw invalid_argument("Aggregation: coarse node " + std::to_string(c) + " has " +
+                                               std::to_string(count[c]) + " fine nodes");
             }
             h->levels.push_back(std::move(L));
         }

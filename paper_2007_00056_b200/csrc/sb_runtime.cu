@@ -1468,9 +1468,17 @@ struct Cyc {
     double omega = 2.0 / 3.0;
 };
 
+// Kernels a whole-solve graph executes: pre + once (prologue body, when the
+// loop is entered) + iterations x per_it + (iterations - skipped) x per_it_cond
+// + post. Counted while the graph is captured (launch_count deltas).
+struct LaunchPlan {
+    int pre = 0, once = 0, per_it = 0, per_it_cond = 0, post = 0;
+};
+
 struct GraphEntry {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t exec = nullptr;
+    LaunchPlan plan;
 };
 
 } // namespace sb
@@ -1495,6 +1503,8 @@ struct sb_ctx_s {
     int64_t bytes = 0;
     int nvec_blocks = 1;
     bool graphs = true;
+    sb::LaunchPlan plan;         // of the graph being built
+    int64_t last_launches = 0;   // kernels the last solve executed
     std::vector<void *> allocs;
     std::vector<void *> host_allocs;  // hybrid mode: pinned mapped host arrays
     bool alloc_host = false;
@@ -1563,8 +1573,14 @@ static Red make_red(sb_ctx c, int op, int nval, const double *w0 = nullptr, cons
     return r;
 }
 
+// Eager mode (sb_device_opts.use_graphs = 0): the solve drivers below emit the
+// same kernels straight onto the stream and the host evaluates each
+// conditional node itself (every condition in this file is !st->done).
+static thread_local bool tl_eager = false;
+
 static CondSet conds(std::initializer_list<cudaGraphConditionalHandle> hs) {
     CondSet cs{{0, 0}, 0};
+    if (tl_eager) return cs;
     for (auto h : hs) cs.h[cs.n++] = static_cast<unsigned long long>(h);
     return cs;
 }
@@ -1897,6 +1913,7 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
 // ---- graph construction helpers -------------------------------------------------
 
 static cudaGraphConditionalHandle new_handle(cudaStream_t s) {
+    if (tl_eager) return cudaGraphConditionalHandle{};
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
     CK(cudaStreamGetCaptureInfo(s, &status, nullptr, &g, nullptr, nullptr));
@@ -1908,6 +1925,20 @@ static cudaGraphConditionalHandle new_handle(cudaStream_t s) {
 static void add_cond(sb_ctx c, cudaStream_t s, int depth, cudaGraphConditionalHandle h,
                      cudaGraphConditionalNodeType type,
                      const std::function<void(cudaStream_t, int)> &body) {
+    if (tl_eager) {  // host-side loop control: wait for the kernel that decided, read done
+        auto done = [&]() {
+            int d = 0;
+            CK(cudaMemcpyAsync(&d, &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            return d != 0;
+        };
+        if (type == cudaGraphCondTypeWhile) {
+            while (!done()) body(s, depth + 1);
+        } else if (!done()) {
+            body(s, depth + 1);
+        }
+        return;
+    }
     cudaStreamCaptureStatus status;
     cudaGraph_t g;
     const cudaGraphNode_t *deps = nullptr;
@@ -1931,6 +1962,7 @@ static void add_cond(sb_ctx c, cudaStream_t s, int depth, cudaGraphConditionalHa
 }
 
 static cudaGraph_t begin_capture(sb_ctx c) {
+    if (tl_eager) return nullptr;
     cudaGraph_t g;
     CK(cudaGraphCreate(&g, 0));
     CK(cudaStreamBeginCaptureToGraph(c->stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
@@ -1938,6 +1970,7 @@ static cudaGraph_t begin_capture(sb_ctx c) {
 }
 
 static cudaGraph_t end_capture(sb_ctx c, cudaGraph_t g) {
+    if (tl_eager) return nullptr;
     cudaGraph_t out;
     CK(cudaStreamEndCapture(c->stream, &out));
     return g;
@@ -1962,15 +1995,23 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
     const int L = static_cast<int>(c->L.size());
     double *x0 = (cp && cp->pre >= 1 && L >= 2 && c->tail_from != 0) ? zero_sweep_dest(c, *cp, 0, z) : nullptr;
     cudaGraph_t g = begin_capture(c);
+    c->launch_count = 0;
+    int mark = 0;
+    auto plan = [&](int &field) {  // graph mode: kernels emitted since the last mark
+        if (!tl_eager) field = c->launch_count - mark;
+        mark = c->launch_count;
+    };
     cudaGraphConditionalHandle h_pro = new_handle(s);
     launch_k(c, k_init, dim3(vb), dim3(kVecThreads), 0, s, n, b, x, r, make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_pro})));
     CK(cudaGetLastError());
+    plan(c->plan.pre);
     add_cond(c, s, 0, h_pro, cudaGraphCondTypeIf, [&](cudaStream_t s1, int d1) {
         precond(s1, r, z, false);
         cudaGraphConditionalHandle h_loop = new_handle(s1);
         launch_k(c, k_copy_dot, dim3(vb), dim3(kVecThreads), 0, s1, n, z, p, nullptr, r,
                                               make_red(c, EP_PCG_RZ0, 1, nullptr, nullptr, conds({h_loop})), X0{});
         CK(cudaGetLastError());
+        plan(c->plan.once);
         add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
             launch_csr<M_SPMV, 1>(c, l0, s2, p, nullptr, Ap, 0.0, &c->st->done, make_red(c, EP_PCG_PAP, 1, p));
             cudaGraphConditionalHandle h_vc = new_handle(s2);
@@ -1978,6 +2019,7 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
                 n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})),
                 X0{static_cast<const double *>(l0.diag), x0, cp ? cp->omega : 0.0});
             CK(cudaGetLastError());
+            plan(c->plan.per_it);
             add_cond(c, s2, d2, h_vc, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
                 const Red rz = make_red(c, EP_PCG_RZ, 1, r);
                 c->final_red = &rz;  // (r, z) rides on the V-cycle's last sweep when it is a Jacobi sweep
@@ -1990,11 +2032,13 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
                 }
                 launch_k(c, k_xpay, dim3(vb), dim3(kVecThreads), 0, s3, n, z, p, c->st);
                 CK(cudaGetLastError());
+                plan(c->plan.per_it_cond);
             });
         });
     });
     // true residual ||b - A x|| (krylov.hpp:116)
     launch_csr<M_RESID, 1>(c, l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
+    plan(c->plan.post);
     return end_capture(c, g);
 }
 
@@ -2017,14 +2061,22 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
         else CK(cudaMemcpyAsync(out, in, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToDevice, ss));
     };
     cudaGraph_t g = begin_capture(c);
+    c->launch_count = 0;
+    int mark = 0;
+    auto plan = [&](int &field) {  // graph mode: kernels emitted since the last mark
+        if (!tl_eager) field = c->launch_count - mark;
+        mark = c->launch_count;
+    };
     cudaGraphConditionalHandle h_pro = new_handle(s);
     launch_k(c, k_init, dim3(vb), dim3(kVecThreads), 0, s, n, b, x, r, make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_pro})));
     CK(cudaGetLastError());
+    plan(c->plan.pre);
     add_cond(c, s, 0, h_pro, cudaGraphCondTypeIf, [&](cudaStream_t s1, int d1) {
         cudaGraphConditionalHandle h_loop = new_handle(s1);
         launch_k(c, k_copy_dot, dim3(vb), dim3(kVecThreads), 0, s1, n, r, rbar, p, r,
                                               make_red(c, EP_BI_RHO0, 1, nullptr, nullptr, conds({h_loop})), x0p);
         CK(cudaGetLastError());
+        plan(c->plan.once);
         add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
             // (the loop is only entered / re-entered with done == 0)
             precond(s2, p, pt);
@@ -2035,6 +2087,7 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
             CK(cudaGetLastError());
             launch_k(c, k_bi_half, dim3(vb), dim3(kVecThreads), 0, s2, n, x, pt, c->st);
             CK(cudaGetLastError());
+            plan(c->plan.per_it);
             add_cond(c, s2, d2, h_v2, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
                 precond(s3, sv, stv);
                 launch_csr<M_SPMV, 2>(c, l0, s3, stv, nullptr, Ast, 0.0, nullptr,
@@ -2044,12 +2097,19 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
                 CK(cudaGetLastError());
                 launch_k(c, k_bi_p, dim3(vb), dim3(kVecThreads), 0, s3, n, r, p, Apt, c->st, x0p);
                 CK(cudaGetLastError());
+                plan(c->plan.per_it_cond);
             });
-            k_set_cond<<<1, 1, 0, s2>>>(c->st, conds({h_loop}));
-            CK(cudaGetLastError());
+            if (!tl_eager) {
+                k_set_cond<<<1, 1, 0, s2>>>(c->st, conds({h_loop}));
+                CK(cudaGetLastError());
+                ++c->launch_count;
+                ++c->plan.per_it;  // k_set_cond runs every iteration
+                mark = c->launch_count;
+            }
         });
     });
     launch_csr<M_RESID, 1>(c, l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
+    plan(c->plan.post);
     return end_capture(c, g);
 }
 
@@ -2060,14 +2120,18 @@ static cudaGraph_t build_amg(sb_ctx c, const Cyc &cp, const double *b, double *x
     const int vb = vec_grid(n);
     cudaStream_t s = c->stream;
     cudaGraph_t g = begin_capture(c);
+    c->launch_count = 0;
     cudaGraphConditionalHandle h_loop = new_handle(s);
     launch_k(c, k_init, dim3(vb), dim3(kVecThreads), 0, s, n, b, x, nullptr,
                                       make_red(c, EP_INIT_NORM, 1, nullptr, nullptr, conds({h_loop})));
     CK(cudaGetLastError());
+    if (!tl_eager) c->plan.pre = c->launch_count;
     add_cond(c, s, 0, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s1, int) {
+        const int m0 = c->launch_count;
         emit_vcycle(c, s1, cp, 0, b, x, false);
         launch_csr<M_RESID, 1>(c, l0, s1, x, b, c->rs, 0.0, nullptr,
                                make_red(c, EP_AMG_RN, 1, nullptr, nullptr, conds({h_loop})));
+        if (!tl_eager) c->plan.per_it = c->launch_count - m0;
     });
     return end_capture(c, g);
 }
@@ -2981,19 +3045,39 @@ static int run_solve(sb_ctx c, SolveKind kind, const sb_cycle *cpa, const double
     hs.hist_t = c->hist_t;
     CK(cudaMemcpyAsync(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
     const char *kname = kind == K_PCG ? "pcg" : kind == K_BICG ? "bicg" : "amg";
-    const std::string key = key_of(kname, cp, db, dx, c->hist_r);
-    auto it = c->cache.find(key);
-    if (it == c->cache.end()) {
-        GraphEntry e;
-        if (kind == K_PCG) e.g = build_pcg(c, cp, db, dx);
-        else if (kind == K_BICG) e.g = build_bicg(c, cp, db, dx);
-        else e.g = build_amg(c, *cp, db, dx);
-        CK(cudaGraphInstantiate(&e.exec, e.g, 0));
-        it = c->cache.emplace(key, e).first;
+    auto build = [&]() {
+        if (kind == K_PCG) return build_pcg(c, cp, db, dx);
+        if (kind == K_BICG) return build_bicg(c, cp, db, dx);
+        return build_amg(c, *cp, db, dx);
+    };
+    if (!c->graphs) {  // eager: the same kernels, host-side loop control
+        CK(cudaEventRecord(c->ev0, c->stream));
+        c->launch_count = 0;
+        tl_eager = true;
+        try {
+            build();
+        } catch (...) {
+            tl_eager = false;
+            throw;
+        }
+        tl_eager = false;
+        c->last_launches = c->launch_count;
+        CK(cudaEventRecord(c->ev1, c->stream));
+    } else {
+        const std::string key = key_of(kname, cp, db, dx, c->hist_r);
+        auto it = c->cache.find(key);
+        if (it == c->cache.end()) {
+            GraphEntry e;
+            c->plan = LaunchPlan{};
+            e.g = build();
+            e.plan = c->plan;
+            CK(cudaGraphInstantiate(&e.exec, e.g, 0));
+            it = c->cache.emplace(key, e).first;
+        }
+        CK(cudaEventRecord(c->ev0, c->stream));
+        CK(cudaGraphLaunch(it->second.exec, c->stream));
+        CK(cudaEventRecord(c->ev1, c->stream));
     }
-    CK(cudaEventRecord(c->ev0, c->stream));
-    CK(cudaGraphLaunch(it->second.exec, c->stream));
-    CK(cudaEventRecord(c->ev1, c->stream));
     CK(cudaMemcpyAsync(&hs, c->st, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));
     if (host)
         CK(cudaMemcpyAsync(x, dx, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, c->stream));
@@ -3001,6 +3085,13 @@ static int run_solve(sb_ctx c, SolveKind kind, const sb_cycle *cpa, const double
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     c->last_solve_ms = ms;
+    if (c->graphs) {  // kernels the graph executed (LaunchPlan)
+        const LaunchPlan &P = c->cache.find(key_of(kname, cp, db, dx, c->hist_r))->second.plan;
+        const bool entered = hs.iter > 0 || kind == K_AMG;
+        const int skipped = kind == K_BICG ? hs.half : (kind == K_PCG && hs.iter > 0 ? 1 : 0);
+        c->last_launches = P.pre + P.post + (entered ? P.once : 0) + int64_t(hs.iter) * P.per_it +
+                           std::max<int64_t>(0, int64_t(hs.iter) - skipped) * P.per_it_cond;
+    }
     const int hist_len = hs.iter + 1;
     if (rep) {
         rep->iterations = hs.iter;
@@ -3268,6 +3359,7 @@ int sb_pbicgstab_dev(sb_ctx c, const sb_cycle *cp, const double *d_b, double *d_
     return guard([&] { run_solve(c, K_BICG, cp, d_b, d_x, tol, max_iters, rep, false, "pbicgstab"); });
 }
 
+int64_t sb_last_solve_launches(sb_ctx c) { return c ? c->last_launches : 0; }
 double sb_last_solve_ms(sb_ctx c) { return c ? c->last_solve_ms : 0.0; }
 
 // Streamed storage of level k: fmt[0] = 2 row patterns / 1 sliced-ELL / 0 CSR, fmt[1] = value
@@ -3348,7 +3440,8 @@ int sb_vcycle_launches(sb_ctx c, const sb_cycle *cp) {
     return rc == SB_OK ? out : -1;
 }
 
-int sb_time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int reps, double *avg_ms, int *launches) {
+static int time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int reps, int64_t flush_bytes,
+                       double *avg_ms, int *launches) {
     return guard([&] {
         const DevLevel &l = level_of(c, level);
         if (reps < 1) throw invalid_argument("sb_time_kernel: reps must be >= 1");
@@ -3391,16 +3484,49 @@ int sb_time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int reps, 
             }
         };
         once();  // warm-up
-        CK(cudaEventRecord(c->ev0, s));
-        for (int i = 0; i < reps; ++i) once();
-        CK(cudaEventRecord(c->ev1, s));
-        CK(cudaEventSynchronize(c->ev1));
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        if (flush_bytes <= 0) {
+            CK(cudaEventRecord(c->ev0, s));
+            for (int i = 0; i < reps; ++i) once();
+            CK(cudaEventRecord(c->ev1, s));
+            CK(cudaEventSynchronize(c->ev1));
+            CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        } else {
+            // cold L2: a write of flush_bytes (> L2) before every launch, each
+            // launch bracketed by its own event pair on the launching stream
+            double *fb = nullptr;
+            CK(cudaMalloc(&fb, static_cast<size_t>(flush_bytes)));
+            struct Free {
+                double *p;
+                ~Free() { cudaFree(p); }
+            } free_fb{fb};
+            const int64_t nf = flush_bytes / 8;
+            for (int i = 0; i < reps; ++i) {
+                k_fill<<<vec_grid(nf), kVecThreads, 0, s>>>(nf, fb, static_cast<double>(i));
+                CK(cudaEventRecord(c->ev0, s));
+                once();
+                CK(cudaEventRecord(c->ev1, s));
+                CK(cudaEventSynchronize(c->ev1));
+                float one = 0.f;
+                CK(cudaEventElapsedTime(&one, c->ev0, c->ev1));
+                ms += one;
+            }
+        }
         if (avg_ms) *avg_ms = ms / reps;
         if (launches) *launches = c->launch_count;
         if (vgraph) cudaGraphExecDestroy(vgraph);
     });
+}
+
+int sb_time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int reps, double *avg_ms, int *launches) {
+    return time_kernel(c, kind, level, cp, reps, 0, avg_ms, launches);
+}
+
+int sb_time_kernel_cold(sb_ctx c, int kind, int level, const sb_cycle *cp, int reps, int64_t flush_bytes,
+                        double *avg_ms, int *launches) {
+    if (flush_bytes <= 0)
+        return guard([] { throw invalid_argument("sb_time_kernel_cold: flush_bytes must be > 0"); });
+    return time_kernel(c, kind, level, cp, reps, flush_bytes, avg_ms, launches);
 }
 
 int sb_spmv(sb_ctx c, int level, const double *x, double *y) {

@@ -313,7 +313,8 @@ class HierarchyStats:
 # --------------------------------------------------------------------------
 class Hierarchy:
     def __init__(self, A: CsrMatrix, cfg: SolverConfig = None, device: int = 0, *, _coarse_solver=None,
-                 coarse_exact: bool = False, galerkin_gpu: bool = False, host_levels_from: int = -1):
+                 coarse_exact: bool = False, galerkin_gpu: bool = False, host_levels_from: int = -1,
+                 graphs: bool = True):
         cfg = cfg or SolverConfig()
         if not A.is_square():
             raise InvalidArgument("Hierarchy: matrix must be square")
@@ -334,6 +335,7 @@ class Hierarchy:
         self._device = device
         self._coarse_exact = bool(coarse_exact)
         self._host_from = int(host_levels_from)  # hybrid mode
+        self._graphs = bool(graphs)  # False: eager launches, host-side loop control (sb_device_opts.use_graphs)
         self._levels = None
         self._A0 = A
         self.config = cfg
@@ -352,7 +354,7 @@ class Hierarchy:
         h = C.c_void_p()
         check(_lib.lib().sb_setup_stencil27(int(nx), int(ny), int(nz), float(diag), float(off), C.byref(opts),
                                             C.byref(h)))
-        self._h, self._ctx, self._device, self._coarse_exact = h, None, device, False
+        self._h, self._ctx, self._device, self._coarse_exact, self._graphs = h, None, device, False, True
         self._host_from, self._levels, self._A0, self.config = int(host_levels_from), None, None, cfg
         return self
 
@@ -407,10 +409,15 @@ class Hierarchy:
     def ctx(self):
         if self._ctx is None:
             c = C.c_void_p()
-            opts = _lib.sb_device_opts(self._device, 1, self._host_from, int(self._coarse_exact))
+            opts = _lib.sb_device_opts(self._device, 1 if self._graphs else 0, self._host_from,
+                                       int(self._coarse_exact))
             check(_lib.lib().sb_create(self._h, C.byref(opts), C.byref(c)))
             self._ctx = c
         return self._ctx
+
+    def last_solve_launches(self) -> int:
+        """Kernels the last solve executed (sb_last_solve_launches)."""
+        return int(_lib.lib().sb_last_solve_launches(self.ctx()))
 
     def device_bytes(self) -> int:
         return int(_lib.lib().sb_device_bytes(self.ctx()))

@@ -12,7 +12,7 @@ from conftest import golden_path
 from helpers import example_6x6, from_npz
 
 CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(golden_path("*.npz"))
-               if not p.endswith("example_6x6.npz"))
+               if not p.endswith("example_6x6.npz") and not os.path.basename(p).startswith("config_"))
 
 
 def test_example_6x6_known_answer(sp, port):
@@ -90,3 +90,38 @@ def test_amg_divergence_reported(sp, port, ref):
     r = ref.hierarchy(A, 1, 40)
     a, b = p.amg_solve(np.array([1.0, -1.0]), 1e-8, 50), r.amg_solve(np.array([1.0, -1.0]), 1e-8, 50)
     assert a.status == 2 and b.status == 2 and "diverged" in b.error
+
+
+def test_reference_generators_match_product(sp, ref):
+    """The reference-built 3D generators (oracle/ref_capi.cpp, used by bench.py's
+    reference arm and the config fixtures) and the product's (sb_gen_*) give the
+    same CSR bit for bit."""
+    import oracle as orc
+
+    def same(rm, A):
+        rp, ci, v = rm.arrays()
+        return (np.array_equal(rp, A.row_ptr()) and np.array_equal(ci, A.col_idx())
+                and np.array_equal(v.view(np.uint64), np.asarray(A.values()).view(np.uint64)))
+
+    assert same(ref.poisson3d(9), sp.poisson3d(9))
+    assert same(ref.aniso3d(8, 1e-3), sp.aniso3d(8, 1e-3))
+    assert same(ref.convdiff3d(7, 8, 9, 1.0, 100.0, 1.0, 1.0), sp.convdiff3d(7, 8, 9, 1.0, 100.0, 1.0, 1.0))
+    assert same(ref.stencil27(6, 6, 6), sp.poisson3d_27(6))
+    assert same(ref.convdiff2d(12, 10, 0.0, 0.0, 0.0), sp.poisson2d(12, 10))
+    rp, ci, v = orc.graph_laplacian3d_arrays(9, seed=7)
+    G = sp.graph_laplacian3d(9, seed=7)
+    assert np.array_equal(rp, G.row_ptr()) and np.array_equal(ci, G.col_idx())
+    assert np.array_equal(v.view(np.uint64), np.asarray(G.values()).view(np.uint64))
+
+
+def test_config_fixtures_consistent():
+    """tests/golden/config_*.npz (the reference at the BASELINE configs) hold the
+    survey-measured iteration counts and converged."""
+    import json
+    expect = {"C1": 60, "C2": 22, "C3": 43, "P27_128": 20}
+    for name, k in expect.items():
+        p = golden_path(f"config_{name}.npz")
+        if not os.path.exists(p):
+            continue
+        m = json.loads(str(np.load(p)["meta"]))
+        assert m["iterations"] == k and m["termination"] == 0, (name, m["iterations"])
