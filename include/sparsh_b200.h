@@ -220,6 +220,14 @@ int sb_level_march(sb_ctx ctx, int level, int *geo, int *stride);
 /* Name of the kernel a Jacobi sweep of `level` launches (k_boxpair, k_march,
  * k_rowpat, k_sellg or k_csr_tile), NUL-terminated into buf[cap]. */
 int sb_level_sweep_kernel(sb_ctx ctx, int level, char *buf, int cap);
+/* Jacobi sweeps one HBM pass performs on level k: 2 when consecutive sweeps
+ * run fused in k_cross_tb2 (temporal blocking on structured 7-point levels),
+ * else 1; -1 on error. geo (8 ints, optional) receives {nx, ny, nz, TX, TY,
+ * ZL, grid, smem bytes} of the fused kernel. */
+int sb_level_fused_sweeps(sb_ctx ctx, int level, int *geo);
+/* Build flags of the library: bit 0 = built with SB_EXPERIMENTAL=1 (the
+ * kernels kept for A/B work: k_march, k_cross_rr, k_cross_tb2). */
+int sb_build_flags(void);
 /* Kernels launched by one V-cycle from level 0 (graph node count). */
 int sb_vcycle_launches(sb_ctx ctx, const sb_cycle *cp);
 

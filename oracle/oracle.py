@@ -104,7 +104,13 @@ class Port:
         L.oc_restrict.argtypes = [C.c_int32, _I, C.c_int32, _D, _D]
         L.oc_galerkin.argtypes = [C.POINTER(OcCsr), _I, C.c_int32, C.POINTER(OcCsr)]
         L.oc_prolong_add.argtypes = [C.c_int32, _I, _D, _D]
+        L.oc_set_dot_mode.argtypes = [C.c_int]
         self.L = L
+
+    def set_dot_mode(self, mode):
+        """0: the reference's sequential dots; 1: reordered (blocked + pairwise) dots
+        (noise-floor measurements only, tools/noise_floor.py)."""
+        self.L.oc_set_dot_mode(int(mode))
 
     def _csr(self, rp, ci, v, n, ncols=None):
         rp = np.ascontiguousarray(rp, dtype=np.int32)

@@ -75,8 +75,27 @@ void oc_spmv(const oc_csr *A, const double *x, double *y) {
     }
 }
 
+/* Dot-product summation order. 0 (default): the reference's sequential sum
+ * (inc/csr.hpp:245-251). 1: a reordered sum -- sequential within blocks of 256
+ * products, then a pairwise tree over the block sums -- used only to measure
+ * how far a legal reordering of the reference's own dots moves a solve (the
+ * rounding-noise floor of the parity contract; tools/noise_floor.py). */
+static int g_dot_mode = 0;
+void oc_set_dot_mode(int mode) { g_dot_mode = mode; }
+
+static double dot_tree(int64_t n, const double *a, const double *b) {
+    if (n <= 256) {
+        double s = 0.0;
+        for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+        return s;
+    }
+    int64_t h = ((n + 511) / 512) * 256; /* split at a block boundary */
+    return dot_tree(h, a, b) + dot_tree(n - h, a + h, b + h);
+}
+
 /* inc/csr.hpp:245-251 */
 double oc_dot(int64_t n, const double *a, const double *b) {
+    if (g_dot_mode == 1) return dot_tree(n, a, b);
     double s = 0.0;
     for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
     return s;

@@ -30,10 +30,23 @@
 #include <thread>
 #include <type_traits>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "sb_internal.h"
 #include "sb_kernels.cuh"
+
+// Kernels that were built, measured slower than the defaults and kept for A/B
+// work only: the plane-marching 27-point sweep (k_march),
+// the pair-based residual + restriction (k_cross_rr) and the two-sweep
+// temporal blocking (k_cross_tb2). They are templates instantiated only when
+// the library is built with SB_EXPERIMENTAL=1 (make EXPERIMENTAL=1); the
+// product build contains none of their code.
+#ifndef SB_EXPERIMENTAL
+#define SB_EXPERIMENTAL 0
+#endif
+constexpr bool kExperimental = SB_EXPERIMENTAL != 0;
 
 namespace sb {
 
@@ -882,6 +895,7 @@ __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
 
 #include "sb_rowpat.cuh"
 #include "sb_march.cuh"
+#include "sb_tblock.cuh"
 
 // ===========================================================================
 // Cluster-resident tail: the deepest levels (each CTA's slice of every tail
@@ -1450,6 +1464,11 @@ struct DevLevel {
     int march_geo = -1, march_S = 0, march_N = 0, march_nqf = 0, march_nxb = 0, march_nyb = 0, march_ntiles = 0;
     int march_grid = 0;
     size_t march_tb = 0;
+    // two fused Jacobi sweeps per pass on structured 7-point levels (k_cross_tb2)
+    int tb = 0, tb_grid = 0;
+    TbGeo tb_geo{};
+    size_t tb_smem = 0;
+    const double *tb_tab = nullptr;
     // row pairs on 27-point box levels with even strides (k_boxpair)
     int box_pair = 0, box_grid = 0;
     const uint32_t *box_rmask = nullptr;
@@ -1504,6 +1523,7 @@ struct sb_ctx_s {
     int nvec_blocks = 1;
     bool graphs = true;
     sb::LaunchPlan plan;         // of the graph being built
+    std::map<std::tuple<const void *, int, int, int, int, int>, CUtensorMap> tmaps;  // TMA descriptors by (ptr, dims, box)
     int64_t last_launches = 0;   // kernels the last solve executed
     std::vector<void *> allocs;
     std::vector<void *> host_allocs;  // hybrid mode: pinned mapped host arrays
@@ -1722,9 +1742,8 @@ static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double
                          out, omega, skip, red);
             return;
         }
-        if (l.pat && l.march_geo >= 0) {
-            return launch_march_g<MODE, NV, 0, 28>(c, l, s, x, f, out, omega, skip, red);
-        }
+        if constexpr (kExperimental)
+            if (l.pat && l.march_geo >= 0) return launch_march_g<MODE, NV, 0, 28>(c, l, s, x, f, out, omega, skip, red);
     }
     if (l.pat) {
         switch (l.pat_w) {
@@ -1762,6 +1781,7 @@ static void launch_pat_rr_w(sb_ctx c, const DevLevel &l, const DevLevel &lc, cud
 static void launch_pat_rr(sb_ctx c, const DevLevel &l, const DevLevel &lc, cudaStream_t s, const double *x,
                           const double *f, double *x0, double omega) {
     auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+#if SB_EXPERIMENTAL
     if (l.box_pair == 2 && l.pat_w == 7 && a16(x) && a16(f) && !c_cross_rr_off) {
         const int grid = static_cast<int>(std::max<int64_t>(
             1, std::min<int64_t>((lc.n + kCrossThreads - 1) / kCrossThreads, static_cast<int64_t>(l.box_grid))));
@@ -1770,6 +1790,9 @@ static void launch_pat_rr(sb_ctx c, const DevLevel &l, const DevLevel &lc, cudaS
                  main_pat<7>(l), x, f, lc.f, static_cast<const double *>(lc.diag), x0, omega);
         return;
     }
+#else
+    (void)a16;
+#endif
     switch (l.pat_w) {
     case 5: return launch_pat_rr_w<5>(c, l, lc, s, x, f, x0, omega);
     case 7: return launch_pat_rr_w<7>(c, l, lc, s, x, f, x0, omega);
@@ -1783,6 +1806,63 @@ static void launch_pat_rr(sb_ctx c, const DevLevel &l, const DevLevel &lc, cudaS
 static void launch_jacobi(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *xin, const double *f,
                           double *xout, double omega) {
     launch_csr<M_JACOBI, 0>(c, l, s, xin, f, xout, omega, nullptr, Red{});
+}
+
+// TMA descriptor of an nx x ny x nz f64 grid at p with an (bx, by, 1) box,
+// out-of-grid elements zero-filled; cached per context.
+static CUtensorMap tmap3d(sb_ctx c, const double *p, int nx, int ny, int nz, int bx, int by) {
+    const auto key = std::make_tuple(static_cast<const void *>(p), nx, ny, nz, bx, by);
+    auto it = c->tmaps.find(key);
+    if (it != c->tmaps.end()) return it->second;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) throw sb::cuda_error("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(nx), static_cast<cuuint64_t>(ny), static_cast<cuuint64_t>(nz)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(nx) * 8, static_cast<cuuint64_t>(nx) * ny * 8};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(p), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw sb::cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    c->tmaps.emplace(key, m);
+    return m;
+}
+
+// two Jacobi sweeps xin -> out in one pass (k_cross_tb2)
+static void launch_tb2(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *xin, const double *f,
+                       double *out, double omega) {
+    if (!kExperimental) throw sb::cuda_error("k_cross_tb2 is not built (SB_EXPERIMENTAL=0)");
+    const TbGeo &g = l.tb_geo;
+    const CUtensorMap mx = tmap3d(c, xin, g.nx, g.ny, g.nz, g.TX + 4, g.TY + 4);
+    const CUtensorMap mf = tmap3d(c, f, g.nx, g.ny, g.nz, g.TX + 4, g.TY + 2);
+    launch_k(c, tb_kernel(g.TX), dim3(l.tb_grid), dim3(kTbThreads), l.tb_smem, s, mx, mf, g, l.tb_tab, out, omega);
+}
+
+// How `count` consecutive Jacobi sweeps of level l are launched: fused pairs
+// (k_cross_tb2) where the level has them, then a single sweep; last_single
+// keeps the final launch a single sweep (it may carry the (r, z) reduction).
+static std::vector<int> sweep_groups(const DevLevel &l, int count, bool last_single) {
+    std::vector<int> g;
+    if (!l.tb) {
+        g.assign(static_cast<size_t>(std::max(count, 0)), 1);
+        return g;
+    }
+    int left = count;
+    while (left >= 2 && !(last_single && left == 2)) {
+        g.push_back(2);
+        left -= 2;
+    }
+    while (left-- > 0) g.push_back(1);
+    return g;
+}
+static int sweep_launches(const DevLevel &l, int count, bool last_single) {
+    return static_cast<int>(sweep_groups(l, count, last_single).size());
 }
 
 static void emit_coarse(sb_ctx c, cudaStream_t s, const double *f, double *x) {
@@ -1817,11 +1897,35 @@ static void emit_tail(sb_ctx c, cudaStream_t s, const Cyc &cp, const double *f, 
 
 // Buffer the zero-guess first pre-sweep of level k writes (X = the level's
 // output buffer; see emit_vcycle's buffer plan).
+// (Each launch of a sweep group swaps the ping-pong pair; sweep_groups.)
+static double *post_first_of(sb_ctx c, const Cyc &cp, int k, double *X) {
+    const DevLevel &l = c->L[static_cast<size_t>(k)];
+    return (cp.post >= 1) ? ((sweep_launches(l, cp.post - 1, k == 0) % 2 == 0) ? X : l.t) : X;
+}
 static double *zero_sweep_dest(sb_ctx c, const Cyc &cp, int k, double *X) {
-    double *T = c->L[static_cast<size_t>(k)].t;
-    double *post_first = (cp.post >= 1) ? (((cp.post - 1) % 2 == 0) ? X : T) : X;
+    const DevLevel &l = c->L[static_cast<size_t>(k)];
+    double *T = l.t;
+    double *post_first = post_first_of(c, cp, k, X);
     double *pre_end = (cp.post >= 1) ? (post_first == X ? T : X) : X;
-    return (cp.pre % 2 == 1) ? pre_end : (pre_end == X ? T : X);
+    return (sweep_launches(l, cp.pre - 1, false) % 2 == 0) ? pre_end : (pre_end == X ? T : X);
+}
+
+// Jacobi sweeps of level l in launch groups (1: one sweep, 2: k_cross_tb2),
+// ping-ponging cur / other; the last single sweep carries `red` when given.
+static void emit_sweeps(sb_ctx c, const DevLevel &l, cudaStream_t s, const std::vector<int> &groups, double *&cur,
+                        double *&other, const double *f, double omega, const Red *red = nullptr,
+                        bool *red_used = nullptr) {
+    for (size_t i = 0; i < groups.size(); ++i) {
+        if (groups[i] == 2) {
+            launch_tb2(c, l, s, cur, f, other, omega);
+        } else if (red && i + 1 == groups.size()) {
+            launch_csr<M_JACOBI, 1>(c, l, s, cur, f, other, omega, nullptr, *red);
+            if (red_used) *red_used = true;
+        } else {
+            launch_jacobi(c, l, s, cur, f, other, omega);
+        }
+        std::swap(cur, other);
+    }
 }
 
 // One V-cycle at level k (cycle.hpp:53-75), result written to X. T is the
@@ -1843,7 +1947,7 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
     }
     const DevLevel &l = c->L[static_cast<size_t>(k)];
     double *T = l.t;
-    double *post_first = (cp.post >= 1) ? (((cp.post - 1) % 2 == 0) ? X : T) : X;
+    double *post_first = post_first_of(c, cp, k, X);
     double *cur = X, *other = T;
     if (zero) {
         double *pre_end = (cp.post >= 1) ? (post_first == X ? T : X) : X;
@@ -1856,16 +1960,10 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
             if (!x0_ready)
                 launch_k(c, k_jacobi_zero, dim3(vec_grid(l.n)), dim3(kVecThreads), 0, s, l.n, f,
                          static_cast<const double *>(l.diag), cur, cp.omega);
-            for (int i = 1; i < cp.pre; ++i) {
-                launch_jacobi(c, l, s, cur, f, other, cp.omega);
-                std::swap(cur, other);
-            }
+            emit_sweeps(c, l, s, sweep_groups(l, cp.pre - 1, false), cur, other, f, cp.omega);
         }
     } else {
-        for (int i = 0; i < cp.pre; ++i) {
-            launch_jacobi(c, l, s, cur, f, other, cp.omega);
-            std::swap(cur, other);
-        }
+        emit_sweeps(c, l, s, sweep_groups(l, cp.pre, false), cur, other, f, cp.omega);
     }
     const DevLevel &lc = c->L[static_cast<size_t>(k) + 1];
     // the child's zero-guess sweep rides on the restriction (not for the
@@ -1887,26 +1985,17 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
                                         Aux{l.diag, l.agg, lc.x});
         cur = post_first;
         other = (cur == X) ? T : X;
-        for (int i = 1; i < cp.post; ++i) {
-            if (k == 0 && i + 1 == cp.post && c->final_red) {  // last kernel of the cycle: + (z, r)
-                launch_csr<M_JACOBI, 1>(c, l, s, cur, f, other, cp.omega, nullptr, *c->final_red);
-                c->final_red_used = true;
-            } else {
-                launch_jacobi(c, l, s, cur, f, other, cp.omega);
-            }
-            std::swap(cur, other);
-        }
+        // last kernel of the cycle at level 0: a single sweep + (z, r)
+        emit_sweeps(c, l, s, sweep_groups(l, cp.post - 1, k == 0), cur, other, f, cp.omega,
+                    k == 0 ? c->final_red : nullptr, &c->final_red_used);
     } else {
-        double *pout = (cp.post % 2 == 0) ? X : T;
+        double *pout = (sweep_launches(l, cp.post, k == 0) % 2 == 0) ? X : T;
         launch_k(c, k_prolong, dim3(vec_grid(l.n)), dim3(kVecThreads), 0, s, l.n,
                  static_cast<const int32_t *>(l.agg), static_cast<const double *>(cur),
                  static_cast<const double *>(lc.x), pout);
         cur = pout;
         other = (pout == X) ? T : X;
-        for (int i = 0; i < cp.post; ++i) {
-            launch_jacobi(c, l, s, cur, f, other, cp.omega);
-            std::swap(cur, other);
-        }
+        emit_sweeps(c, l, s, sweep_groups(l, cp.post, k == 0), cur, other, f, cp.omega);
     }
 }
 
@@ -2099,13 +2188,11 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
                 CK(cudaGetLastError());
                 plan(c->plan.per_it_cond);
             });
-            if (!tl_eager) {
-                k_set_cond<<<1, 1, 0, s2>>>(c->st, conds({h_loop}));
-                CK(cudaGetLastError());
-                ++c->launch_count;
-                ++c->plan.per_it;  // k_set_cond runs every iteration
-                mark = c->launch_count;
-            }
+            k_set_cond<<<1, 1, 0, s2>>>(c->st, conds({h_loop}));  // (eager: no handles, a no-op kernel)
+            CK(cudaGetLastError());
+            ++c->launch_count;
+            if (!tl_eager) ++c->plan.per_it;  // k_set_cond runs every iteration
+            mark = c->launch_count;
         });
     });
     launch_csr<M_RESID, 1>(c, l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
@@ -2181,6 +2268,7 @@ static bool march_geo_ok(const DevLevel &D, int &P, int &N) {
 
 static void build_march(sb_ctx c, DevLevel &D, int np, int w, const double *val, const int32_t *off,
                         const uint8_t *len) {
+    if (!kExperimental) return;
     const char *e = std::getenv("SB_MARCH");  // opt-in: measured slower than k_rowpat
     if (!e || std::atoi(e) == 0) return;
     const char *em = std::getenv("SB_MARCH_MIN");
@@ -2222,6 +2310,106 @@ static void build_march(sb_ctx c, DevLevel &D, int np, int w, const double *val,
 // hash their rows, first occurrences become patterns, and every row is
 // verified against its pattern's full key (a hash collision only disables the
 // format). Returns false (nothing allocated) when the level does not qualify.
+// Two-sweep temporal blocking (k_cross_tb2, sb_tblock.cuh): the level must be
+// an nx x ny x nz grid in (iz*ny + iy)*nx + ix order whose row pattern is a
+// function of the row's boundary class and whose absent slots are exactly the
+// out-of-grid neighbours; checked for every row. SB_TB=0 disables it,
+// SB_TB_MIN (rows, default 0) skips smaller levels.
+static constexpr size_t kTbSmemMax = 112 * 1024;  // two CTAs per SM
+static void build_tb(sb_ctx c, DevLevel &D, const std::vector<uint8_t> &pid, int np, const double *val,
+                     const int32_t *off, const uint8_t *len, const double *dg, const double *ry) {
+    if (!kExperimental) return;
+    const char *e = std::getenv("SB_TB");  // opt-in: measured slower
+    if (!e || std::atoi(e) == 0) return;
+    const char *em = std::getenv("SB_TB_MIN");
+    if (em && D.n < std::atoll(em)) return;
+    const std::vector<int> &mo = D.main_o;
+    const int64_t N = mo[5], P = mo[6], n = D.n;
+    if (N < 2 || N % 2 != 0 || P % N != 0 || n % P != 0) return;
+    const int64_t nx = N, ny = P / N, nz = n / P;
+    if (ny < 2 || nz < 2 || nx > INT32_MAX / 2) return;
+    constexpr int wv = 8, wo = 8;  // SmemTab<7> row strides (doubles / int32)
+    const int64_t want[7] = {-P, -N, -1, 0, 1, N, P};
+    std::vector<int> cls_pat(kTbClasses, -1);
+    auto cl = [](int64_t i, int64_t m) { return i == 0 ? 0 : (i == m - 1 ? 2 : 1); };
+    for (int64_t m = 0; m < n; ++m) {
+        const int64_t ix = m % nx, iy = (m / nx) % ny, iz = m / P;
+        const int cx = cl(ix, nx), cy = cl(iy, ny), cz = cl(iz, nz), k = cx + 3 * cy + 9 * cz;
+        const int q = pid[static_cast<size_t>(m)];
+        if (cls_pat[k] < 0) {
+            // the pattern's slots must be exactly the in-grid neighbours, in CSR order
+            const bool present[7] = {iz > 0, iy > 0, ix > 0, true, ix < nx - 1, iy < ny - 1, iz < nz - 1};
+            int j = 0;
+            for (int s = 0; s < 7; ++s) {
+                if (!present[s]) continue;
+                if (j >= len[q] || off[q * wo + j] != want[s]) return;
+                ++j;
+            }
+            if (j != len[q]) return;
+            cls_pat[k] = q;
+        } else if (cls_pat[k] != q) {
+            return;
+        }
+    }
+    std::vector<double> tab(kTbTab, 0.0);
+    for (int k = 0; k < kTbClasses; ++k) {
+        const int q = cls_pat[k];
+        if (q < 0) continue;
+        int j = 0;
+        for (int s = 0; s < 7; ++s)
+            if (j < len[q] && off[q * wo + j] == want[s]) tab[k * 9 + s] = val[q * wv + j++];
+        tab[k * 9 + 7] = dg[q];
+        tab[k * 9 + 8] = ry[q];
+    }
+    (void)np;
+    // tile: 64 x 16 columns (the whole x-line on narrow levels), <= kTbSmemMax of rings
+    TbGeo g{};
+    g.nx = static_cast<int>(nx);
+    g.ny = static_cast<int>(ny);
+    g.nz = static_cast<int>(nz);
+    g.TX = 32;  // kernel instances: TX = 64, 32, 16, 8 with TY = 2 * kTbThreads / TX
+    while (g.TX > nx && g.TX > 8) g.TX /= 2;
+    if (g.TX > nx) return;
+    g.TY = 2 * kTbThreads / g.TX;
+    g.ntx = static_cast<int>((nx + g.TX - 1) / g.TX);
+    g.nty = static_cast<int>((ny + g.TY - 1) / g.TY);
+    static const bool attr = [] {
+        for (int tx : {64, 32, 16, 8})
+            CK(cudaFuncSetAttribute(tb_kernel(tx), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kTbSmemMax)));
+        return true;
+    }();
+    (void)attr;
+    const size_t smem = tb_smem_bytes(g.TX, g.TY);
+    if (smem > kTbSmemMax) return;
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tb_kernel(g.TX), kTbThreads, smem));
+    if (occ < 1) return;
+    // z-chunks: minimise waves x steps per CTA (each CTA marches ZL + 4 planes)
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    const int64_t tiles = int64_t(g.ntx) * g.nty, res = int64_t(nsm) * occ;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int nch = 1; nch <= g.nz; ++nch) {
+        const int zl = (g.nz + nch - 1) / nch;
+        const int real = (g.nz + zl - 1) / zl;
+        const double cost = static_cast<double>((tiles * real + res - 1) / res) * (zl + 4);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = real;
+        }
+    }
+    g.ZL = (g.nz + best - 1) / best;
+    auto *dt = dalloc<double>(c, kTbTab);
+    CK(cudaMemcpy(dt, tab.data(), sizeof(double) * kTbTab, cudaMemcpyHostToDevice));
+    D.tb_tab = dt;
+    D.tb_geo = g;
+    D.tb_smem = smem;
+    D.tb_grid = static_cast<int>(tiles * ((g.nz + g.ZL - 1) / g.ZL));
+    D.tb = 1;
+}
+
 static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
     const char *pe = std::getenv("SB_RPAT");
     if ((pe && std::atoi(pe) == 0) || A.n == 0) return false;
@@ -2389,6 +2577,7 @@ static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
             D.box_pair = kind;
         }
     }
+    if (D.box_pair == 2 && w == 7) build_tb(c, D, pid, np, val, off, len, dg, ry);
     auto *dp = dalloc<uint8_t>(c, A.n + 16);
     CK(cudaMemcpy(dp, pid.data(), pid.size(), cudaMemcpyHostToDevice));
     auto *dt = dalloc<unsigned char>(c, static_cast<int64_t>(tb));
@@ -2665,10 +2854,12 @@ template <int MODE, int NV> static void set_smem_attr(size_t smem) {
         CK(cudaFuncSetAttribute(k_boxpair<MODE, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_crosspair<MODE, NV, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
         CK(cudaFuncSetAttribute(k_crosspair<MODE, NV, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-        if constexpr (MODE == M_RESID && NV == 0)
-            CK(cudaFuncSetAttribute(k_cross_rr<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-        CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-        CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        if constexpr (kExperimental) {
+            if constexpr (MODE == M_RESID && NV == 0)
+                CK(cudaFuncSetAttribute(k_cross_rr<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+            CK(cudaFuncSetAttribute(k_march<MODE, NV, 0, 28, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+        }
     }
     CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     CK(cudaFuncSetAttribute(k_rowpat<MODE, NV, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
@@ -3228,7 +3419,11 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
             auto occ_m = [&](auto kern) {
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMarchThreads, sm));
             };
+#if SB_EXPERIMENTAL
             occ_m(k_march<M_JACOBI, 0, 0, 28, true>);
+#else
+            (void)occ_m;
+#endif
             const int64_t need = std::max<int64_t>(l.march_ntiles, 1);
             l.march_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
         }
@@ -3386,6 +3581,23 @@ int sb_level_format(sb_ctx c, int k, int *fmt, int64_t *matrix_bytes, int64_t *n
         }
         *nnz = l.nnz;
     });
+}
+
+int sb_build_flags(void) { return kExperimental ? 1 : 0; }
+
+int sb_level_fused_sweeps(sb_ctx c, int k, int *geo) {
+    try {
+        const DevLevel &l = level_of(c, k);
+        if (geo && l.tb) {
+            const TbGeo &g = l.tb_geo;
+            const int v[8] = {g.nx, g.ny, g.nz, g.TX, g.TY, g.ZL, l.tb_grid, static_cast<int>(l.tb_smem)};
+            std::memcpy(geo, v, sizeof v);
+        }
+        return l.tb ? 2 : 1;
+    } catch (const std::exception &e) {
+        set_error(e.what());
+        return -1;
+    }
 }
 
 int sb_level_sweep_kernel(sb_ctx c, int k, char *buf, int cap) {
@@ -3556,10 +3768,7 @@ int sb_smooth(sb_ctx c, int level, const sb_cycle *cp, double *x, const double *
             double *a = c->kv[KX], *b = c->kv[KZ], *df = c->kv[KB];
             h2d(c, a, x, l.n);
             h2d(c, df, f, l.n);
-            for (int i = 0; i < sweeps; ++i) {
-                launch_jacobi(c, l, s, a, df, b, cp->omega);
-                std::swap(a, b);
-            }
+            emit_sweeps(c, l, s, sweep_groups(l, sweeps, false), a, b, df, cp->omega);
             d2h(c, x, a, l.n);
         });
     });

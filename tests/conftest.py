@@ -63,3 +63,16 @@ def ref():
 
 def golden_path(name):
     return os.path.join(ROOT, "tests", "golden", name)
+
+
+def experimental_built():
+    """The library was built with SB_EXPERIMENTAL=1 (k_march, k_cross_rr, k_cross_tb2)."""
+    try:
+        from paper_2007_00056_b200 import _lib
+        return bool(_lib.lib().sb_build_flags() & 1)
+    except Exception:
+        return False
+
+
+needs_experimental = pytest.mark.skipif(not experimental_built(),
+                                        reason="experimental kernels not built (make EXPERIMENTAL=1)")

@@ -11,7 +11,9 @@ the GPU parity tests (tests/test_gpu_configs.py) assert against:
   thread count (inc/krylov.hpp:65-119 / 126-211);
 * the solution x_k at the reference's final iteration: a strided sample
   (every `stride`-th entry), ||x||_2, sum(x) and x . g for the seeded
-  g = default_rng(20070056).standard_normal(n).
+  g = default_rng(20070056).standard_normal(n); the same for the
+  equal-iteration run (tol = 1e-300, max_iters = k_ref: "xe"), which differs
+  from the to-tolerance iterate only for a BiCGStab half-step exit.
 
 The matrices come from oracle/ref_capi.cpp (triplets through the reference's
 CsrMatrix::from_triplets), so the product library is not involved.
@@ -69,13 +71,19 @@ def main(names):
         out = getattr(h, SOLVER[name])(b, tol, 1000)
         x = out.x
         stride = max(1, n // SAMPLES)
+        # the equal-iteration solution (tol = 1e-300, max_iters = k_ref; SURVEY §8c
+        # protocol). For PCG it is the to-tolerance iterate; BiCGStab's half-step
+        # exit (krylov.hpp:167-173) returns x + alpha p~ where the equal-iteration
+        # run completes the step, so it is recorded separately.
+        xe = x if SOLVER[name] == "pcg" else getattr(h, SOLVER[name])(b, 1e-300, out.iterations).x
         meta = {"name": name, "solver": SOLVER[name], "n": n, "nnz": nnz, "levels": levels,
                 "tol": tol, "rhs": "ones", "iterations": out.iterations, "termination": out.termination,
                 "true_residual": out.true_residual, "wall_time": out.wall_time, "threads": threads,
                 "gen_s": t_gen, "setup_s": t_setup, "stride": stride,
                 "x_norm2": float(np.linalg.norm(x)), "x_sum": float(np.sum(x)), "x_dot_g": float(x @ g_vector(n)),
+                "xe_norm2": float(np.linalg.norm(xe)), "xe_sum": float(np.sum(xe)), "xe_dot_g": float(xe @ g_vector(n)),
                 "generator": "oracle/ref_capi.cpp ref_stencil7/ref_convdiff3d/ref_stencil27/convdiff2d"}
-        np.savez_compressed(os.path.join(HERE, f"config_{name}.npz"), x_sample=x[::stride],
+        np.savez_compressed(os.path.join(HERE, f"config_{name}.npz"), x_sample=x[::stride], xe_sample=xe[::stride],
                             residual_history=np.asarray(out.residual_history),
                             time_history=np.asarray(out.time_history), meta=json.dumps(meta))
         print(f"{name}: n={n} levels={len(levels)} {SOLVER[name]} it={out.iterations} term={out.termination} "

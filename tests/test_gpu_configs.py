@@ -16,7 +16,9 @@ Asserted per configuration:
     residual < tol, true relative residual <= 1e-8 (+ rounding slack);
   - equal iteration count (tol = 1e-300, max_iters = k_ref): solution within
     1e-10 relative L2 (on the fixture's strided sample, plus ||x||, sum x and
-    x.g over the full vector), residual histories within 1e-8 relative.
+    x.g over the full vector), residual histories within 1e-8 relative; the
+    to-tolerance solution equals the reference's to-tolerance one (for
+    BiCGStab both end in the half-step exit when it fires).
 """
 import json
 import os
@@ -54,6 +56,7 @@ class Case:
         z = np.load(golden_path(f"config_{name}.npz"))
         self.meta = json.loads(str(z["meta"]))
         self.x_sample = z["x_sample"]
+        self.xe_sample = z["xe_sample"] if "xe_sample" in z.files else z["x_sample"]
         self.hist = z["residual_history"]
         self.name = name
         self.A = GEN[name](sp)
@@ -102,6 +105,8 @@ def test_config_to_tolerance(case):
     assert rep.true_residual / nb < 1.5e-8, rep.true_residual / nb
     if rep.iterations == m["iterations"]:
         assert abs(rep.true_residual - m["true_residual"]) <= 0.05 * m["true_residual"] + 1e-3 * tol
+        # the same exit (incl. BiCGStab's half-step exit, krylov.hpp:167-173): same iterate
+        assert rel(res.x[::m["stride"]], case.x_sample) < 1e-10
 
 
 def test_config_equal_iterations(case):
@@ -111,10 +116,11 @@ def test_config_equal_iterations(case):
     res = case.solve(case.A, case.b, case.M, 1e-300, k)
     assert res.report.iterations == k
     x = res.x
-    assert rel(x[::m["stride"]], case.x_sample) < 1e-10
-    assert abs(np.linalg.norm(x) - m["x_norm2"]) <= 1e-10 * m["x_norm2"]
-    assert abs(x @ _g(x.size) - m["x_dot_g"]) <= 1e-10 * np.linalg.norm(x) * np.sqrt(x.size)
-    assert abs(np.sum(x) - m["x_sum"]) <= 1e-10 * np.sum(np.abs(x))
+    pre = "xe_" if "xe_norm2" in m else "x_"
+    assert rel(x[::m["stride"]], case.xe_sample) < 1e-10
+    assert abs(np.linalg.norm(x) - m[pre + "norm2"]) <= 1e-10 * m[pre + "norm2"]
+    assert abs(x @ _g(x.size) - m[pre + "dot_g"]) <= 1e-10 * np.linalg.norm(x) * np.sqrt(x.size)
+    assert abs(np.sum(x) - m[pre + "sum"]) <= 1e-10 * np.sum(np.abs(x))
     hist = np.asarray(res.report.residual_history)
     assert hist.size == case.hist.size
     assert np.max(np.abs(hist - case.hist) / case.hist) < 1e-8

@@ -11,6 +11,8 @@ import ctypes as C
 import numpy as np
 import pytest
 
+from conftest import needs_experimental
+
 from helpers import stencil27_varied
 
 pytestmark = pytest.mark.gpu
@@ -45,6 +47,7 @@ def _cases(sp):
     ]
 
 
+@needs_experimental
 @pytest.mark.parametrize("idx", range(8))
 def test_march_kernels_bitexact(sp, oracle_best, idx, monkeypatch):
     monkeypatch.setenv("SB_BOXPAIR", "0")
@@ -109,6 +112,7 @@ def _solve(sp, A, march, monkeypatch):
     return geos, v, res
 
 
+@needs_experimental
 @pytest.mark.parametrize("dims", [(48, 16, 40), (45, 13, 37)])  # even / odd line and plane strides
 def test_march_vcycle_pcg_identical(sp, dims, monkeypatch):
     A = _p27(sp, *dims)
@@ -187,6 +191,7 @@ def test_boxpair_vcycle_pcg_identical(sp, which, monkeypatch):
     assert np.linalg.norm(out["1"][2].x - out["0"][2].x) <= 1e-12 * np.linalg.norm(out["0"][2].x)
 
 
+@needs_experimental
 def test_cross_rr_vcycle_identical():
     # k_cross_rr (opt-in, read once per process): residual + restriction from row
     # pairs gives bitwise the same V-cycle as k_pat_resid_restrict
