@@ -138,6 +138,7 @@ struct RankDev {
     Partition P;
     std::vector<DistLevel> D;
     cudaEvent_t ready = nullptr, done = nullptr;
+    cudaStream_t s = nullptr;      // stream the solve is emitted on (the context stream, or a graph body's)
     double **part_ptrs = nullptr;  // in-process: device array of every rank's st->part
     int64_t lo = 0, hi = 0;        // owned rows of level 0
 };
@@ -151,6 +152,7 @@ struct sb_dist_s {
     ncclComm_t comm = nullptr;
     double last_ms = 0.0;
     int last_launches = 0;
+    std::map<std::string, sb::GraphEntry> cache;  // captured whole-solve graphs (NCCL mode)
 };
 
 namespace sb {
@@ -202,10 +204,10 @@ static void upload_dist_level(sb_ctx c, const PartLevel &pl, DevLevel &D, DistLe
 // ---- collectives ---------------------------------------------------------------------
 
 static void barrier_local(sb_dist d) {
-    for (auto &r : d->R) CK(cudaEventRecord(r.done, r.c->stream));
+    for (auto &r : d->R) CK(cudaEventRecord(r.done, r.s));
     for (auto &r : d->R)
         for (auto &q : d->R)
-            if (&q != &r) CK(cudaStreamWaitEvent(r.c->stream, q.done, 0));
+            if (&q != &r) CK(cudaStreamWaitEvent(r.s, q.done, 0));
 }
 
 // Fill the ghost entries of every rank r from own(q) of its peers q, per the
@@ -218,7 +220,7 @@ static void exchange(sb_dist d, int k, int which, const std::function<const doub
         return which == 0 ? L.halo : which == 1 ? L.rx : L.px;
     };
     if (d->local) {
-        for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.c->stream));
+        for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.s));
         for (auto &r : d->R) {
             DevExch &e = plan(r);
             for (size_t j = 0; j < e.recv_peers.size(); ++j) {
@@ -228,8 +230,8 @@ static void exchange(sb_dist d, int k, int which, const std::function<const doub
                 while (jj < eq.send_peers.size() && eq.send_peers[jj] != r.rank) ++jj;
                 if (jj == eq.send_peers.size()) throw runtime_error("exchange: inconsistent plans");
                 const int64_t cnt = e.recv_off[j + 1] - e.recv_off[j];
-                CK(cudaStreamWaitEvent(r.c->stream, q.ready, 0));
-                launch_k(r.c, k_gather_idx, dim3(vec_grid(cnt)), dim3(kVecThreads), 0, r.c->stream, cnt, own(q),
+                CK(cudaStreamWaitEvent(r.s, q.ready, 0));
+                launch_k(r.c, k_gather_idx, dim3(vec_grid(cnt)), dim3(kVecThreads), 0, r.s, cnt, own(q),
                          static_cast<const int32_t *>(eq.send_idx + eq.send_off[jj]), ghost(r) + e.recv_dst[j]);
             }
         }
@@ -239,7 +241,7 @@ static void exchange(sb_dist d, int k, int which, const std::function<const doub
     RankDev &r = d->R[0];
     DevExch &e = plan(r);
     if (e.nsend == 0 && e.nrecv == 0) return;
-    cudaStream_t s = r.c->stream;
+    cudaStream_t s = r.s;
     if (e.nsend)
         launch_k(r.c, k_gather_idx, dim3(vec_grid(e.nsend)), dim3(kVecThreads), 0, s, e.nsend, own(r),
                  static_cast<const int32_t *>(e.send_idx), e.sendbuf);
@@ -256,14 +258,14 @@ static void exchange(sb_dist d, int k, int which, const std::function<const doub
 // every rank ends with the whole vector v(r) whose piece [b[q], b[q+1]) rank q owns
 static void allgatherv(sb_dist d, const std::vector<int64_t> &b, const std::function<double *(RankDev &)> &v) {
     if (d->local) {
-        for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.c->stream));
+        for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.s));
         for (auto &r : d->R)
             for (auto &q : d->R) {
                 if (&q == &r || b[q.rank + 1] == b[q.rank]) continue;
-                CK(cudaStreamWaitEvent(r.c->stream, q.ready, 0));
+                CK(cudaStreamWaitEvent(r.s, q.ready, 0));
                 CK(cudaMemcpyAsync(v(r) + b[q.rank], v(q) + b[q.rank],
                                    sizeof(double) * static_cast<size_t>(b[q.rank + 1] - b[q.rank]),
-                                   cudaMemcpyDeviceToDevice, r.c->stream));
+                                   cudaMemcpyDeviceToDevice, r.s));
             }
         barrier_local(d);
         return;
@@ -274,29 +276,29 @@ static void allgatherv(sb_dist d, const std::vector<int64_t> &b, const std::func
         if (q == r.rank) continue;
         if (b[r.rank + 1] > b[r.rank])
             NC(nccl().Send(v(r) + b[r.rank], static_cast<size_t>(b[r.rank + 1] - b[r.rank]), ncclFloat64, q, d->comm,
-                           r.c->stream));
+                           r.s));
         if (b[q + 1] > b[q])
-            NC(nccl().Recv(v(r) + b[q], static_cast<size_t>(b[q + 1] - b[q]), ncclFloat64, q, d->comm, r.c->stream));
+            NC(nccl().Recv(v(r) + b[q], static_cast<size_t>(b[q + 1] - b[q]), ncclFloat64, q, d->comm, r.s));
     }
     NC(nccl().GroupEnd());
 }
 
 // st->red = sum over ranks of st->part; then the scalar logic `op` on every rank
-static void allreduce_logic(sb_dist d, int op) {
+static void allreduce_logic(sb_dist d, int op, CondSet cs = CondSet{{0, 0}, 0}) {
     if (d->local) {
-        for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.c->stream));
+        for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.s));
         for (auto &r : d->R) {
             for (auto &q : d->R)
-                if (&q != &r) CK(cudaStreamWaitEvent(r.c->stream, q.ready, 0));
-            launch_k(r.c, k_sum_partials, dim3(1), dim3(1), 0, r.c->stream,
+                if (&q != &r) CK(cudaStreamWaitEvent(r.s, q.ready, 0));
+            launch_k(r.c, k_sum_partials, dim3(1), dim3(1), 0, r.s,
                      static_cast<const double *const *>(r.part_ptrs), d->nranks, r.c->st->red);
         }
         barrier_local(d);
     } else {
         RankDev &r = d->R[0];
-        NC(nccl().AllReduce(r.c->st->part, r.c->st->red, 2, ncclFloat64, ncclSum, d->comm, r.c->stream));
+        NC(nccl().AllReduce(r.c->st->part, r.c->st->red, 2, ncclFloat64, ncclSum, d->comm, r.s));
     }
-    for (auto &r : d->R) launch_k(r.c, k_logic, dim3(1), dim3(1), 0, r.c->stream, r.c->st, op);
+    for (auto &r : d->R) launch_k(r.c, k_logic, dim3(1), dim3(1), 0, r.s, r.c->st, op, cs);
 }
 
 static Red red_partial(sb_ctx c, int nval, const double *w0 = nullptr, const double *w1 = nullptr) {
@@ -311,7 +313,7 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
                         const std::vector<double *> &X, bool zero) {
     const size_t N = d->R.size();
     if (k >= d->fr) {
-        for (size_t i = 0; i < N; ++i) emit_vcycle(d->R[i].c, d->R[i].c->stream, cp, k, f[i], X[i], zero);
+        for (size_t i = 0; i < N; ++i) emit_vcycle(d->R[i].c, d->R[i].s, cp, k, f[i], X[i], zero);
         return;
     }
     std::vector<double *> cur(N), oth(N);
@@ -323,7 +325,7 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
                  [&](RankDev &r) { return vv[static_cast<size_t>(&r - d->R.data())]; });
     };
     auto sweep = [&]() {
-        for (size_t i = 0; i < N; ++i) launch_jacobi(d->R[i].c, lev(i), d->R[i].c->stream, cur[i], f[i], oth[i], cp.omega);
+        for (size_t i = 0; i < N; ++i) launch_jacobi(d->R[i].c, lev(i), d->R[i].s, cur[i], f[i], oth[i], cp.omega);
         std::swap(cur, oth);
     };
     for (size_t i = 0; i < N; ++i) {
@@ -334,7 +336,7 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
         if (cp.pre >= 1) {
             for (size_t i = 0; i < N; ++i)
                 launch_k(d->R[i].c, k_jacobi_zero, dim3(vec_grid(dl(i).n_own)), dim3(kVecThreads), 0,
-                         d->R[i].c->stream, dl(i).n_own, f[i], static_cast<const double *>(lev(i).diag), cur[i],
+                         d->R[i].s, dl(i).n_own, f[i], static_cast<const double *>(lev(i).diag), cur[i],
                          cp.omega);
             for (int s = 1; s < cp.pre; ++s) {
                 halo(cur);
@@ -342,7 +344,7 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
             }
         } else {
             for (size_t i = 0; i < N; ++i)
-                CK(cudaMemsetAsync(cur[i], 0, sizeof(double) * static_cast<size_t>(dl(i).n_own), d->R[i].c->stream));
+                CK(cudaMemsetAsync(cur[i], 0, sizeof(double) * static_cast<size_t>(dl(i).n_own), d->R[i].s));
         }
     } else {
         for (int s = 0; s < cp.pre; ++s) {
@@ -350,18 +352,31 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
             sweep();
         }
     }
-    // residual, partner residuals, restriction
+    // residual, partner residuals, restriction. A rank whose aggregates are all
+    // local (no straddling pair: no rx plan; every BASELINE grid at plane-aligned
+    // splits) runs the single-GPU fused residual + restriction kernel
+    // (k_pat_resid_restrict: no r vector) when the coarse level is partitioned too.
     halo(cur);
-    for (size_t i = 0; i < N; ++i)
-        launch_csr<M_RESID, 0>(d->R[i].c, lev(i), d->R[i].c->stream, cur[i], f[i], d->R[i].c->rs, 0.0, nullptr,
+    const bool next_rep = k + 1 >= d->fr;
+    auto fused_rr = [&](size_t i) {
+        const DistLevel &L = dl(i);
+        return !next_rep && lev(i).pat && L.rx.nsend == 0 && L.rx.nrecv == 0;
+    };
+    for (size_t i = 0; i < N; ++i) {
+        if (fused_rr(i)) continue;
+        launch_csr<M_RESID, 0>(d->R[i].c, lev(i), d->R[i].s, cur[i], f[i], d->R[i].c->rs, 0.0, nullptr,
                                Red{});
+    }
     exchange(d, k, 1, [&](RankDev &r) -> const double * { return r.c->rs; },
              [&](RankDev &r) { return r.D[static_cast<size_t>(k)].rg; });
-    const bool next_rep = k + 1 >= d->fr;
     for (size_t i = 0; i < N; ++i) {
         DevLevel &lc = d->R[i].c->L[static_cast<size_t>(k) + 1];
+        if (fused_rr(i)) {
+            launch_pat_rr(d->R[i].c, lev(i), lc, d->R[i].s, cur[i], f[i], nullptr, cp.omega);
+            continue;
+        }
         double *out = next_rep ? lc.f + dl(i).c_lo : lc.f;
-        launch_k(d->R[i].c, k_restrict_dist, dim3(vec_grid(dl(i).nc_own)), dim3(kVecThreads), 0, d->R[i].c->stream,
+        launch_k(d->R[i].c, k_restrict_dist, dim3(vec_grid(dl(i).nc_own)), dim3(kVecThreads), 0, d->R[i].s,
                  dl(i).nc_own, static_cast<const int2 *>(lev(i).mem), static_cast<const double *>(d->R[i].c->rs),
                  static_cast<const double *>(dl(i).rg), dl(i).n_own, out);
     }
@@ -381,7 +396,7 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
     for (size_t i = 0; i < N; ++i) {
         pout[i] = (cp.post % 2 == 0) ? X[i] : lev(i).t;
         const int64_t ncown = next_rep ? (int64_t(1) << 62) : dl(i).nc_own;
-        launch_k(d->R[i].c, k_prolong_dist, dim3(vec_grid(dl(i).n_own)), dim3(kVecThreads), 0, d->R[i].c->stream,
+        launch_k(d->R[i].c, k_prolong_dist, dim3(vec_grid(dl(i).n_own)), dim3(kVecThreads), 0, d->R[i].s,
                  dl(i).n_own, static_cast<const int32_t *>(lev(i).agg), static_cast<const double *>(cur[i]),
                  static_cast<const double *>(xc[i]), static_cast<const double *>(dl(i).xcg), ncown, pout[i]);
         cur[i] = pout[i];
@@ -393,24 +408,39 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
     }
 }
 
-// ---- distributed Krylov drivers (host-driven iteration, device scalar logic) ----------------
-
-static int read_done(sb_dist d) {
-    RankDev &r = d->R[0];
-    int done = 0;
-    CK(cudaMemcpyAsync(&done, &r.c->st->done, sizeof(int), cudaMemcpyDeviceToHost, r.c->stream));
-    CK(cudaStreamSynchronize(r.c->stream));
-    return done;
-}
+// ---- distributed Krylov drivers -------------------------------------------------------------
+// The control flow of build_pcg / build_bicg (conditional nodes driven by the
+// scalar logic, every condition = !st->done), expressed once: with one rank
+// per process (NCCL) the whole solve is captured as ONE CUDA graph (the NCCL
+// calls are captured with it) and launched once; with in-process virtual
+// ranks it runs eagerly with host-side evaluation of each condition (tl_eager).
 
 static void dist_halo_vec(sb_dist d, int kv) {
     exchange(d, 0, 0, [&](RankDev &r) -> const double * { return r.c->kv[kv]; },
              [&](RankDev &r) { return r.c->kv[kv]; });
 }
 
+// conditional region: the body is emitted on rank 0's body stream when capturing
+static void dist_cond(sb_dist d, int depth, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                      const std::function<void(int)> &body) {
+    RankDev &r0 = d->R[0];
+    add_cond(r0.c, r0.s, depth, h, type, [&](cudaStream_t sb, int d2) {
+        const cudaStream_t saved = r0.s;
+        if (!tl_eager) r0.s = sb;
+        body(d2);
+        r0.s = saved;
+    });
+}
+
 // vectors: KX x, KR r, KZ z, KP p, KAP Ap, KB b (own rows; x / p / pt / st with ghost room)
-static void dist_pcg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
+static void dist_pcg(sb_dist d, const Cyc *cp) {
     const size_t N = d->R.size();
+    sb_ctx c0 = d->R[0].c;
+    int mark = c0->launch_count;
+    auto plan = [&](int &field) {  // graph mode: rank 0's kernels emitted since the last mark
+        if (!tl_eager) field = c0->launch_count - mark;
+        mark = c0->launch_count;
+    };
     auto each = [&](const std::function<void(RankDev &, int64_t)> &fn) {
         for (auto &r : d->R) fn(r, r.D[0].n_own);
     };
@@ -425,62 +455,77 @@ static void dist_pcg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
             dist_vcycle(d, *cp, 0, f, X, true);
         } else {
             each([&](RankDev &r, int64_t n) {
-                CK(cudaMemcpyAsync(r.c->kv[out], r.c->kv[in], sizeof(double) * n, cudaMemcpyDeviceToDevice, r.c->stream));
+                CK(cudaMemcpyAsync(r.c->kv[out], r.c->kv[in], sizeof(double) * n, cudaMemcpyDeviceToDevice, r.s));
             });
         }
     };
     each([&](RankDev &r, int64_t n) {
-        launch_k(r.c, k_init, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+        launch_k(r.c, k_init, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n,
                  static_cast<const double *>(r.c->kv[KB]), r.c->kv[KX], r.c->kv[KR], red_partial(r.c, 1));
     });
-    allreduce_logic(d, EP_INIT_NORM);
-    if (!read_done(d)) {
+    cudaGraphConditionalHandle h_pro = new_handle(d->R[0].s);
+    allreduce_logic(d, EP_INIT_NORM, conds({h_pro}));
+    plan(c0->plan.pre);
+    dist_cond(d, 0, h_pro, cudaGraphCondTypeIf, [&](int d1) {
         precond(KR, KZ);
         each([&](RankDev &r, int64_t n) {
-            launch_k(r.c, k_copy_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+            launch_k(r.c, k_copy_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n,
                      static_cast<const double *>(r.c->kv[KZ]), r.c->kv[KP], static_cast<double *>(nullptr),
                      static_cast<const double *>(r.c->kv[KR]), red_partial(r.c, 1), X0{});
         });
-        allreduce_logic(d, EP_PCG_RZ0);
-        for (int j = 0; j < max_iters; ++j) {
+        cudaGraphConditionalHandle h_loop = new_handle(d->R[0].s);
+        allreduce_logic(d, EP_PCG_RZ0, conds({h_loop}));
+        plan(c0->plan.once);
+        dist_cond(d, d1, h_loop, cudaGraphCondTypeWhile, [&](int d2) {
             dist_halo_vec(d, KP);
             each([&](RankDev &r, int64_t) {
-                launch_csr<M_SPMV, 1>(r.c, r.c->L[0], r.c->stream, r.c->kv[KP], nullptr, r.c->kv[KAP], 0.0, nullptr,
+                launch_csr<M_SPMV, 1>(r.c, r.c->L[0], r.s, r.c->kv[KP], nullptr, r.c->kv[KAP], 0.0, nullptr,
                                       red_partial(r.c, 1, r.c->kv[KP]));
             });
             allreduce_logic(d, EP_PCG_PAP);
             each([&](RankDev &r, int64_t n) {
-                launch_k(r.c, k_pcg_update, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n, r.c->kv[KX],
+                launch_k(r.c, k_pcg_update, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n, r.c->kv[KX],
                          r.c->kv[KR], static_cast<const double *>(r.c->kv[KP]),
                          static_cast<const double *>(r.c->kv[KAP]), red_partial(r.c, 1), X0{});
             });
-            allreduce_logic(d, EP_PCG_RN);
-            if (read_done(d)) break;
-            precond(KR, KZ);
-            each([&](RankDev &r, int64_t n) {
-                launch_k(r.c, k_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
-                         static_cast<const double *>(r.c->kv[KR]), static_cast<const double *>(r.c->kv[KZ]),
-                         static_cast<const int *>(nullptr), red_partial(r.c, 1));
+            cudaGraphConditionalHandle h_vc = new_handle(d->R[0].s);
+            allreduce_logic(d, EP_PCG_RN, conds({h_vc, h_loop}));
+            plan(c0->plan.per_it);
+            dist_cond(d, d2, h_vc, cudaGraphCondTypeIf, [&](int) {
+                precond(KR, KZ);
+                each([&](RankDev &r, int64_t n) {
+                    launch_k(r.c, k_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n,
+                             static_cast<const double *>(r.c->kv[KR]), static_cast<const double *>(r.c->kv[KZ]),
+                             static_cast<const int *>(nullptr), red_partial(r.c, 1));
+                });
+                allreduce_logic(d, EP_PCG_RZ);
+                each([&](RankDev &r, int64_t n) {
+                    launch_k(r.c, k_xpay, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n,
+                             static_cast<const double *>(r.c->kv[KZ]), r.c->kv[KP],
+                             static_cast<const DevState *>(r.c->st));
+                });
+                plan(c0->plan.per_it_cond);
             });
-            allreduce_logic(d, EP_PCG_RZ);
-            each([&](RankDev &r, int64_t n) {
-                launch_k(r.c, k_xpay, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
-                         static_cast<const double *>(r.c->kv[KZ]), r.c->kv[KP],
-                         static_cast<const DevState *>(r.c->st));
-            });
-        }
-    }
+        });
+    });
     // true residual
     dist_halo_vec(d, KX);
     each([&](RankDev &r, int64_t) {
-        launch_csr<M_RESID, 1>(r.c, r.c->L[0], r.c->stream, r.c->kv[KX], r.c->kv[KB], r.c->rs, 0.0, nullptr,
+        launch_csr<M_RESID, 1>(r.c, r.c->L[0], r.s, r.c->kv[KX], r.c->kv[KB], r.c->rs, 0.0, nullptr,
                                red_partial(r.c, 1));
     });
     allreduce_logic(d, EP_STORE);
+    plan(c0->plan.post);
 }
 
-static void dist_bicg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
+static void dist_bicg(sb_dist d, const Cyc *cp) {
     const size_t N = d->R.size();
+    sb_ctx c0 = d->R[0].c;
+    int mark = c0->launch_count;
+    auto plan = [&](int &field) {  // graph mode: rank 0's kernels emitted since the last mark
+        if (!tl_eager) field = c0->launch_count - mark;
+        mark = c0->launch_count;
+    };
     auto each = [&](const std::function<void(RankDev &, int64_t)> &fn) {
         for (auto &r : d->R) fn(r, r.D[0].n_own);
     };
@@ -495,72 +540,85 @@ static void dist_bicg(sb_dist d, const Cyc *cp, double tol, int max_iters) {
             dist_vcycle(d, *cp, 0, f, X, true);
         } else {
             each([&](RankDev &r, int64_t n) {
-                CK(cudaMemcpyAsync(r.c->kv[out], r.c->kv[in], sizeof(double) * n, cudaMemcpyDeviceToDevice, r.c->stream));
+                CK(cudaMemcpyAsync(r.c->kv[out], r.c->kv[in], sizeof(double) * n, cudaMemcpyDeviceToDevice, r.s));
             });
         }
     };
-    auto half = [&]() {
-        each([&](RankDev &r, int64_t n) {
-            launch_k(r.c, k_bi_half, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n, r.c->kv[KX],
-                     static_cast<const double *>(r.c->kv[KPT]), static_cast<const DevState *>(r.c->st));
-        });
-    };
     each([&](RankDev &r, int64_t n) {
-        launch_k(r.c, k_init, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+        launch_k(r.c, k_init, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n,
                  static_cast<const double *>(r.c->kv[KB]), r.c->kv[KX], r.c->kv[KR], red_partial(r.c, 1));
     });
-    allreduce_logic(d, EP_INIT_NORM);
-    if (!read_done(d)) {
+    cudaGraphConditionalHandle h_pro = new_handle(d->R[0].s);
+    allreduce_logic(d, EP_INIT_NORM, conds({h_pro}));
+    plan(c0->plan.pre);
+    dist_cond(d, 0, h_pro, cudaGraphCondTypeIf, [&](int d1) {
         each([&](RankDev &r, int64_t n) {
-            launch_k(r.c, k_copy_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+            launch_k(r.c, k_copy_dot, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n,
                      static_cast<const double *>(r.c->kv[KR]), r.c->kv[KRBAR], r.c->kv[KP],
                      static_cast<const double *>(r.c->kv[KR]), red_partial(r.c, 1), X0{});
         });
-        allreduce_logic(d, EP_BI_RHO0);
-        for (int j = 0; j < max_iters && !read_done(d); ++j) {
+        cudaGraphConditionalHandle h_loop = new_handle(d->R[0].s);
+        allreduce_logic(d, EP_BI_RHO0, conds({h_loop}));
+        plan(c0->plan.once);
+        dist_cond(d, d1, h_loop, cudaGraphCondTypeWhile, [&](int d2) {
             precond(KP, KPT);
             dist_halo_vec(d, KPT);
             each([&](RankDev &r, int64_t) {
-                launch_csr<M_SPMV, 1>(r.c, r.c->L[0], r.c->stream, r.c->kv[KPT], nullptr, r.c->kv[KAPT], 0.0, nullptr,
+                launch_csr<M_SPMV, 1>(r.c, r.c->L[0], r.s, r.c->kv[KPT], nullptr, r.c->kv[KAPT], 0.0, nullptr,
                                       red_partial(r.c, 1, r.c->kv[KRBAR]));
             });
             allreduce_logic(d, EP_BI_DENOM);
             each([&](RankDev &r, int64_t n) {
-                launch_k(r.c, k_bi_s, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
+                launch_k(r.c, k_bi_s, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n,
                          static_cast<const double *>(r.c->kv[KR]), static_cast<const double *>(r.c->kv[KAPT]),
                          r.c->kv[KS], red_partial(r.c, 1), X0{});
             });
-            allreduce_logic(d, EP_BI_SN);
-            half();
-            if (read_done(d)) break;
-            precond(KS, KST);
-            dist_halo_vec(d, KST);
-            each([&](RankDev &r, int64_t) {
-                launch_csr<M_SPMV, 2>(r.c, r.c->L[0], r.c->stream, r.c->kv[KST], nullptr, r.c->kv[KAST], 0.0, nullptr,
-                                      red_partial(r.c, 2, nullptr, r.c->kv[KS]));
-            });
-            allreduce_logic(d, EP_BI_AS);
+            cudaGraphConditionalHandle h_v2 = new_handle(d->R[0].s);
+            allreduce_logic(d, EP_BI_SN, conds({h_v2}));
             each([&](RankDev &r, int64_t n) {
-                launch_k(r.c, k_bi_update, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n, r.c->kv[KX],
-                         r.c->kv[KR], static_cast<const double *>(r.c->kv[KPT]),
-                         static_cast<const double *>(r.c->kv[KST]), static_cast<const double *>(r.c->kv[KS]),
-                         static_cast<const double *>(r.c->kv[KAST]), static_cast<const double *>(r.c->kv[KRBAR]),
-                         red_partial(r.c, 2));
+                launch_k(r.c, k_bi_half, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n, r.c->kv[KX],
+                         static_cast<const double *>(r.c->kv[KPT]), static_cast<const DevState *>(r.c->st));
             });
-            allreduce_logic(d, EP_BI_RN_RHO);
-            each([&](RankDev &r, int64_t n) {
-                launch_k(r.c, k_bi_p, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.c->stream, n,
-                         static_cast<const double *>(r.c->kv[KR]), r.c->kv[KP],
-                         static_cast<const double *>(r.c->kv[KAPT]), static_cast<const DevState *>(r.c->st), X0{});
+            plan(c0->plan.per_it);
+            dist_cond(d, d2, h_v2, cudaGraphCondTypeIf, [&](int) {
+                precond(KS, KST);
+                dist_halo_vec(d, KST);
+                each([&](RankDev &r, int64_t) {
+                    launch_csr<M_SPMV, 2>(r.c, r.c->L[0], r.s, r.c->kv[KST], nullptr, r.c->kv[KAST], 0.0, nullptr,
+                                          red_partial(r.c, 2, nullptr, r.c->kv[KS]));
+                });
+                allreduce_logic(d, EP_BI_AS);
+                each([&](RankDev &r, int64_t n) {
+                    launch_k(r.c, k_bi_update, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n, r.c->kv[KX],
+                             r.c->kv[KR], static_cast<const double *>(r.c->kv[KPT]),
+                             static_cast<const double *>(r.c->kv[KST]), static_cast<const double *>(r.c->kv[KS]),
+                             static_cast<const double *>(r.c->kv[KAST]), static_cast<const double *>(r.c->kv[KRBAR]),
+                             red_partial(r.c, 2));
+                });
+                allreduce_logic(d, EP_BI_RN_RHO);
+                each([&](RankDev &r, int64_t n) {
+                    launch_k(r.c, k_bi_p, dim3(vec_grid(n)), dim3(kVecThreads), 0, r.s, n,
+                             static_cast<const double *>(r.c->kv[KR]), r.c->kv[KP],
+                             static_cast<const double *>(r.c->kv[KAPT]), static_cast<const DevState *>(r.c->st), X0{});
+                });
+                plan(c0->plan.per_it_cond);
             });
-        }
-    }
+            // the loop condition after the iteration (!done), as build_bicg's k_set_cond
+            RankDev &r0 = d->R[0];
+            k_set_cond<<<1, 1, 0, r0.s>>>(r0.c->st, conds({h_loop}));
+            CK(cudaGetLastError());
+            ++r0.c->launch_count;
+            if (!tl_eager) ++c0->plan.per_it;
+            mark = c0->launch_count;
+        });
+    });
     dist_halo_vec(d, KX);
     each([&](RankDev &r, int64_t) {
-        launch_csr<M_RESID, 1>(r.c, r.c->L[0], r.c->stream, r.c->kv[KX], r.c->kv[KB], r.c->rs, 0.0, nullptr,
+        launch_csr<M_RESID, 1>(r.c, r.c->L[0], r.s, r.c->kv[KX], r.c->kv[KB], r.c->rs, 0.0, nullptr,
                                red_partial(r.c, 1));
     });
     allreduce_logic(d, EP_STORE);
+    plan(c0->plan.post);
 }
 
 // ---- construction ------------------------------------------------------------------------------
@@ -584,12 +642,15 @@ static void build_rank(sb_dist d, RankDev &R, const Hier &h, int rank, int64_t g
     R.lo = R.P.L[0].lo;
     R.hi = R.P.L[0].hi;
     ctx_finish(c, h, o, nvec, d->fr, d->fr > 0 ? R.D[0].wb : 0);
+    R.s = c->stream;
     CK(cudaEventCreateWithFlags(&R.ready, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&R.done, cudaEventDisableTiming));
 }
 
 static int run_dist(sb_dist d, SolveKind kind, const sb_cycle *cpa, const double *b, double *x, double tol,
                     int max_iters, sb_report *rep, bool device_ptrs) {
+    // (graph mode: b and x are staged through the rank's own vectors, so the
+    // captured graph does not depend on them)
     const auto t0 = std::chrono::steady_clock::now();
     const char *who = kind == K_PCG ? "pcg" : "pbicgstab";
     if (!(tol > 0.0)) throw invalid_argument(std::string(who) + ": tol must be > 0");
@@ -616,10 +677,40 @@ static int run_dist(sb_dist d, SolveKind kind, const sb_cycle *cpa, const double
                            device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, r.c->stream));
     }
     RankDev &r0 = d->R[0];
-    for (auto &r : d->R) r.c->launch_count = 0;
+    for (auto &r : d->R) {
+        r.c->launch_count = 0;
+        r.s = r.c->stream;
+    }
     for (auto &r : d->R) CK(cudaEventRecord(r.c->ev0, r.c->stream));
-    if (kind == K_PCG) dist_pcg(d, cp, tol, max_iters);
-    else dist_bicg(d, cp, tol, max_iters);
+    // one rank per process: the whole solve as one graph (NCCL calls captured);
+    // in-process ranks or use_graphs = 0: eager, host-evaluated conditions
+    const bool graph = !d->local && r0.c->graphs;
+    if (graph) {
+        const std::string key = key_of(kind == K_PCG ? "dist-pcg" : "dist-bicg", cp, nullptr, nullptr, r0.c->hist_r);
+        auto it = d->cache.find(key);
+        if (it == d->cache.end()) {
+            GraphEntry e;
+            r0.c->plan = LaunchPlan{};
+            e.g = begin_capture(r0.c);
+            if (kind == K_PCG) dist_pcg(d, cp);
+            else dist_bicg(d, cp);
+            end_capture(r0.c, e.g);
+            CK(cudaGraphInstantiate(&e.exec, e.g, 0));
+            e.plan = r0.c->plan;
+            it = d->cache.emplace(key, e).first;
+        }
+        CK(cudaGraphLaunch(it->second.exec, r0.c->stream));
+    } else {
+        tl_eager = true;
+        try {
+            if (kind == K_PCG) dist_pcg(d, cp);
+            else dist_bicg(d, cp);
+        } catch (...) {
+            tl_eager = false;
+            throw;
+        }
+        tl_eager = false;
+    }
     for (auto &r : d->R) CK(cudaEventRecord(r.c->ev1, r.c->stream));
     DevState hs;
     for (auto &r : d->R) {
@@ -637,6 +728,13 @@ static int run_dist(sb_dist d, SolveKind kind, const sb_cycle *cpa, const double
     }
     d->last_ms = ms_max;
     d->last_launches = r0.c->launch_count;
+    if (graph) {  // kernels the graph executed on this rank (LaunchPlan, as run_solve)
+        const LaunchPlan &P = d->cache.begin()->second.plan;
+        const bool entered = hs.iter > 0;
+        const int skipped = kind == K_BICG ? hs.half : (hs.iter > 0 ? 1 : 0);
+        d->last_launches = static_cast<int>(P.pre + P.post + (entered ? P.once : 0) + int64_t(hs.iter) * P.per_it +
+                                            std::max<int64_t>(0, int64_t(hs.iter) - skipped) * P.per_it_cond);
+    }
     if (rep) {
         rep->iterations = hs.iter;
         rep->termination = hs.term;
@@ -713,6 +811,10 @@ int sb_dist_create_local(sb_hier hh, int nranks, int64_t gather_rows, const sb_d
 
 void sb_dist_destroy(sb_dist d) {
     if (!d) return;
+    for (auto &kv : d->cache) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.g) cudaGraphDestroy(kv.second.g);
+    }
     if (d->comm) nccl().CommDestroy(d->comm);
     for (auto &r : d->R) {
         if (r.ready) cudaEventDestroy(r.ready);
@@ -754,7 +856,7 @@ int sb_dist_vcycle(sb_dist d, const sb_cycle *cpa, const double *f, double *x) {
             CK(cudaSetDevice(r.c->device));
             const double *src = d->local ? f + r.lo : f;
             CK(cudaMemcpyAsync(r.c->kv[KB], src, sizeof(double) * static_cast<size_t>(r.hi - r.lo),
-                               cudaMemcpyHostToDevice, r.c->stream));
+                               cudaMemcpyHostToDevice, r.s));
             fv[i] = r.c->kv[KB];
             xv[i] = r.c->kv[KZ];
         }
@@ -763,9 +865,9 @@ int sb_dist_vcycle(sb_dist d, const sb_cycle *cpa, const double *f, double *x) {
             RankDev &r = d->R[i];
             double *dst = d->local ? x + r.lo : x;
             CK(cudaMemcpyAsync(dst, r.c->kv[KZ], sizeof(double) * static_cast<size_t>(r.hi - r.lo),
-                               cudaMemcpyDeviceToHost, r.c->stream));
+                               cudaMemcpyDeviceToHost, r.s));
         }
-        for (auto &r : d->R) CK(cudaStreamSynchronize(r.c->stream));
+        for (auto &r : d->R) CK(cudaStreamSynchronize(r.s));
     });
 }
 

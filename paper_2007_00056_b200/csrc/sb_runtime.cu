@@ -313,9 +313,11 @@ __device__ void epilogue(const Red &r, double a, double b) {
 }
 
 // Multi-rank: the scalar logic on the allreduced totals (st->red).
-__global__ void k_logic(DevState *st, int op) {
+__global__ void k_logic(DevState *st, int op, CondSet cs) {
     pdl_wait();
     epilogue_logic(st, op, st->red[0], st->red[1]);
+    for (int i = 0; i < cs.n; ++i)
+        cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(cs.h[i]), st->done ? 0u : 1u);
 }
 
 // Grid-wide deterministic reduction + epilogue. Every thread of every block

@@ -85,10 +85,12 @@ class DistSolver:
     this rank's rows [lo, hi)."""
 
     def __init__(self, h: Hierarchy, nranks: int, gather_rows: int = 65536, *, local: bool = True,
-                 rank: int = 0, nccl_id: bytes = None, device: int = 0):
+                 rank: int = 0, nccl_id: bytes = None, device: int = 0, graphs: bool = True):
+        """graphs (NCCL mode): the whole solve captured as one CUDA graph with the
+        NCCL calls inside (False: eager launches, host-evaluated conditions)."""
         L = _lib.lib()
         d = C.c_void_p()
-        opts = _lib.sb_device_opts(device, 1, -1, 0)
+        opts = _lib.sb_device_opts(device, 1 if graphs else 0, -1, 0)
         if local:
             check(L.sb_dist_create_local(h._h, int(nranks), int(gather_rows), C.byref(opts), C.byref(d)))
         else:

@@ -71,3 +71,31 @@ def test_dist_identity_cg(sp):
     rd = ds.pcg(b, None, 1e-300, 7)
     rs = sp.cg(A, b, 1e-300, 7)
     assert rd.report.iterations == 7 and rel(rd.x, rs.x) < 1e-12
+
+
+@pytest.mark.parametrize("solver", ["pcg", "pbicgstab"])
+def test_dist_nccl_one_rank_graph(sp, solver):
+    """One NCCL rank: the whole distributed solve is ONE captured CUDA graph
+    (NCCL calls inside conditional nodes). It must equal the eager (host-driven)
+    run of the same path bit for bit, and the single-GPU solve to rounding with
+    the same iteration count; the graph's kernel count equals the eager one."""
+    from paper_2007_00056_b200.dist import DistSolver, nccl_unique_id
+    A = sp.poisson3d(40) if solver == "pcg" else sp.convdiff3d(24, 24, 24, 1.0, 100.0, 1.0, 1.0)
+    h = sp.Hierarchy(A, sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40))
+    b = sp.rhs_random(A.nrows(), 3)
+    tol = 1e-8 * np.linalg.norm(b)
+    out = {}
+    for graphs in (True, False):
+        ds = DistSolver(h, 1, 4096, local=False, rank=0, nccl_id=nccl_unique_id(), graphs=graphs)
+        r = getattr(ds, solver)(b, _cp(sp), tol, 200)
+        r2 = getattr(ds, solver)(b, _cp(sp), tol, 200)  # graph replay
+        assert np.array_equal(r.x, r2.x)
+        out[graphs] = (r, ds.last_launches())
+        del ds
+    (rg, lg), (re, le) = out[True], out[False]
+    assert rg.report.converged() and rg.report.iterations == re.report.iterations
+    assert np.array_equal(rg.x.view(np.uint64), re.x.view(np.uint64))
+    assert lg == le > 0
+    single = getattr(sp, solver)(A, b, sp.make_amg_preconditioner(h, _cp(sp)), tol, 200)
+    assert abs(single.report.iterations - rg.report.iterations) <= 1
+    assert rel(rg.x, single.x) < 1e-9
