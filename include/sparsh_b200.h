@@ -228,6 +228,11 @@ int sb_level_fused_sweeps(sb_ctx ctx, int level, int *geo);
 /* Build flags of the library: bit 0 = built with SB_EXPERIMENTAL=1 (the
  * kernels kept for A/B work: k_march, k_cross_rr, k_cross_tb2). */
 int sb_build_flags(void);
+/* Placement of level k's matrix storage (hybrid mode, sb_device_opts.host_levels_from):
+ * *on_host = 1 when it lives in pinned host memory, *matrix_bytes = its streamed
+ * bytes (as sb_level_format). Compare with the reference's analytical model
+ * (inc/memory_model.hpp: csr_bytes, plan_mi / plan_ci). */
+int sb_level_residency(sb_ctx ctx, int level, int *on_host, int64_t *matrix_bytes);
 /* Kernels launched by one V-cycle from level 0 (graph node count). */
 int sb_vcycle_launches(sb_ctx ctx, const sb_cycle *cp);
 

@@ -276,6 +276,10 @@ class Ref:
         L.ref_krylov.argtypes = [C.c_int, P, P, _D, _D, C.c_double, C.c_int, C.POINTER(Report)]
         L.ref_amg_solve.argtypes = [P, _D, _D, C.c_double, C.c_int, C.POINTER(Report)]
         L.ref_read_mm.argtypes = [C.c_char_p, C.POINTER(P)]
+        L.ref_memory_plan.argtypes = [P, C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                      C.POINTER(C.c_longlong)]
+        L.ref_csr_bytes.restype = C.c_longlong
+        L.ref_csr_bytes.argtypes = [P]
         L.ref_write_mm.argtypes = [P, C.c_char_p]
         self.L = L
 
@@ -457,6 +461,17 @@ class RefHier:
 
     def set_cycle(self, pre=6, post=6, omega=2.0 / 3.0, family=0):
         self.R.L.ref_hier_set_cycle(self.h, family, omega, pre, post)
+
+    def memory_plan(self, scheme="MI"):
+        """inc/memory_model.hpp plan_mi / plan_ci: (peak, resident after setup, per-cycle transfer) bytes."""
+        pk, rs, pc = C.c_longlong(), C.c_longlong(), C.c_longlong()
+        self.R.check(self.R.L.ref_memory_plan(self.h, 0 if scheme == "CI" else 1, C.byref(pk), C.byref(rs),
+                                              C.byref(pc)))
+        return pk.value, rs.value, pc.value
+
+    def csr_bytes(self, k):
+        """inc/memory_model.hpp csr_bytes of level k's matrix (8 B values, 4 B indices)."""
+        return int(self.R.L.ref_csr_bytes(self.R.L.ref_hier_level_matrix(self.h, k)))
 
     def vcycle(self, f, x, k=0):
         f, x = _d(f), _d(x).copy()

@@ -293,6 +293,19 @@ void ref_coarse_counts(void *h, long *symbolic, long *numeric, long *solves) {
     *solves = F ? F->solve_count() : -1;
 }
 
+// ---- analytical memory model (inc/memory_model.hpp) ---------------------------
+// scheme 0: CI (level streaming), 1: MI (resident hierarchy); BytesModel{8, 4}
+int ref_memory_plan(void *h, int scheme, long long *peak, long long *resident, long long *per_cycle) {
+    return guard([&] {
+        auto *rh = static_cast<RefHier *>(h);
+        const MemoryPlan p = scheme == 0 ? plan_ci(*rh->h, rh->cp) : plan_mi(*rh->h, rh->cp);
+        *peak = p.peak_device_bytes;
+        *resident = p.resident_setup_bytes;
+        *per_cycle = p.per_cycle_transfer_bytes;
+    });
+}
+long long ref_csr_bytes(void *m) { return csr_bytes(*static_cast<CsrMatrix *>(m), BytesModel{}); }
+
 // ---- solve phase ----------------------------------------------------------
 void ref_hier_set_cycle(void *h, int family, double omega, int pre, int post) {
     static_cast<RefHier *>(h)->cp = make_cp(family, omega, pre, post);

@@ -81,7 +81,7 @@ EXPORTS = [
     "sb_smooth", "sb_residual", "sb_restrict", "sb_prolong", "sb_coarse_solve",
     "sb_gen_convdiff2d", "sb_gen_stencil7", "sb_gen_convdiff3d", "sb_gen_stencil27",
     "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_last_solve_launches", "sb_time_kernel", "sb_time_kernel_cold", "sb_vcycle_launches", "sb_tail_trace",
-    "sb_tail_info", "sb_level_format", "sb_level_march", "sb_level_sweep_kernel", "sb_level_fused_sweeps", "sb_build_flags", "sb_partition", "sb_partition_free", "sb_partition_info",
+    "sb_tail_info", "sb_level_format", "sb_level_march", "sb_level_sweep_kernel", "sb_level_fused_sweeps", "sb_build_flags", "sb_level_residency", "sb_partition", "sb_partition_free", "sb_partition_info",
     "sb_partition_level", "sb_partition_exchange", "sb_nccl_unique_id", "sb_dist_create",
     "sb_dist_create_local", "sb_dist_destroy", "sb_dist_rows", "sb_dist_pcg", "sb_dist_pbicgstab",
     "sb_dist_vcycle", "sb_dist_last_solve_ms", "sb_dist_last_launches", "sb_galerkin_gpu", "sb_host_bytes", "sb_setup_stencil27",
@@ -142,6 +142,7 @@ _SIGS = {
     "sb_level_sweep_kernel": (C.c_int, [_P, C.c_int, C.c_char_p, C.c_int]),
     "sb_level_fused_sweeps": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int)]),
     "sb_build_flags": (C.c_int, []),
+    "sb_level_residency": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int64)]),
     "sb_partition": (C.c_int, [_P, C.c_int, C.c_int, C.c_int64, C.POINTER(_P)]),
     "sb_partition_free": (None, [_P]),
     "sb_nccl_unique_id": (C.c_int, [C.c_char_p]),

@@ -3587,6 +3587,20 @@ int sb_level_format(sb_ctx c, int k, int *fmt, int64_t *matrix_bytes, int64_t *n
 
 int sb_build_flags(void) { return kExperimental ? 1 : 0; }
 
+int sb_level_residency(sb_ctx c, int k, int *on_host, int64_t *matrix_bytes) {
+    return guard([&] {
+        const DevLevel &l = level_of(c, k);
+        if (on_host) *on_host = k >= c->host_from ? 1 : 0;
+        if (matrix_bytes) {
+            int fmt[4];
+            int64_t nnz = 0;
+            const int rc = sb_level_format(c, k, fmt, matrix_bytes, &nnz);
+            if (rc != SB_OK) throw runtime_error(sb_last_error());
+        }
+        (void)l;
+    });
+}
+
 int sb_level_fused_sweeps(sb_ctx c, int k, int *geo) {
     try {
         const DevLevel &l = level_of(c, k);

@@ -53,3 +53,70 @@ def test_hybrid_everything_on_host(sp, monkeypatch):
     assert r_h.report.converged() and r_h.report.iterations == r_d.report.iterations
     assert rel(r_h.x, r_d.x) < 1e-14
     assert hh.device_bytes() < hd.device_bytes() / 2
+
+
+HYB = {
+    "poisson3d_32": (lambda sp: sp.poisson3d(32), "pcg"),
+    "graph_laplacian_20": (lambda sp: sp.graph_laplacian3d(20, seed=3), "pcg"),
+    "convdiff3d_20": (lambda sp: sp.convdiff3d(20, 18, 17, 1.0, 100.0, 1.0, 1.0), "pbicgstab"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(HYB))
+def test_hybrid_vs_reference(sp, oracle_best, name):
+    """Hybrid placement against the REFERENCE (not the device path): one V-cycle
+    within 1e-12, solves with iterations +-1 and, at equal iteration counts,
+    solutions within 1e-10, for several host_levels_from."""
+    mk, solver = HYB[name]
+    A = mk(sp)
+    cfg = _cfg(sp)
+    cp = sp.CycleParams.from_config(cfg)
+    o = oracle_best.hierarchy(A, 500, 40)
+    f = sp.rhs_random(A.nrows(), 11)
+    v_ref = o.vcycle(f, np.zeros(A.nrows()))
+    b = sp.rhs_ones(A.nrows())
+    tol = 1e-8 * np.linalg.norm(b)
+    ref = getattr(o, solver)(b, tol, 300)
+    k = ref.iterations
+    ref_k = getattr(o, solver)(b, 1e-300, k)
+    L = sp.Hierarchy(A, cfg).nlevels()
+    for hf in sorted({1, L // 2, L - 1}):
+        hh = sp.Hierarchy(A, cfg, host_levels_from=hf)
+        assert rel(sp.vcycle(hh, 0, f, np.zeros(A.nrows()), cp), v_ref) < 1e-12, hf
+        M = sp.make_amg_preconditioner(hh, cp)
+        r = getattr(sp, solver)(A, b, M, tol, 300)
+        assert r.report.converged() and abs(r.report.iterations - k) <= 1, hf
+        rk = getattr(sp, solver)(A, b, M, 1e-300, k)
+        assert rel(rk.x, ref_k.x) < 1e-10, hf
+
+
+def test_hybrid_residency_vs_memory_model(sp, ref):
+    """Residency of the MI-style placement (every level but the coarsest on the
+    device, inc/memory_model.hpp plan_mi) against the reference's byte model:
+    the coarsest level's storage is on the host and every other level's on the
+    device (sb_level_residency); each level streams no more bytes than the
+    model's csr_bytes (the lossless formats only shrink CSR); the device holds
+    less than plan_mi's resident bytes plus the Krylov work vectors."""
+    import ctypes as C
+    from paper_2007_00056_b200 import _lib
+    A = sp.graph_laplacian3d(24, seed=5)  # general values: SELL-G / CSR levels, not row patterns
+    cfg = _cfg(sp)
+    L = sp.Hierarchy(A, cfg).nlevels()
+    hh = sp.Hierarchy(A, cfg, host_levels_from=L - 1)
+    rh = ref.hierarchy(A, 500, 40)
+    assert rh.nlevels() == L
+    _, mi_resident, mi_cycle = rh.memory_plan("MI")
+    on_host, mb = C.c_int(), C.c_int64()
+    dev_mat = 0
+    for k in range(L):
+        _lib.check(_lib.lib().sb_level_residency(hh.ctx(), k, C.byref(on_host), C.byref(mb)))
+        assert on_host.value == (1 if k == L - 1 else 0), k
+        assert mb.value <= rh.csr_bytes(k), (k, mb.value, rh.csr_bytes(k))
+        dev_mat += 0 if on_host.value else mb.value
+    n0 = A.nrows()
+    assert dev_mat < mi_resident
+    assert hh.device_bytes() <= mi_resident + 12 * 8 * n0  # + the Krylov vectors the V-cycle model omits
+    assert hh.host_bytes() > 0
+    # MI moves only the coarse rhs down and the coarse solution up per cycle
+    nc = rh.level(L - 1)[0].size - 1
+    assert mi_cycle == 2 * 8 * nc

@@ -126,3 +126,21 @@ def test_setup_stencil27_matches_generated(sp):
         assert a.A == b.A
         if a.agg is not None:
             assert np.array_equal(a.agg.fine_to_coarse, b.agg.fine_to_coarse)
+
+
+@pytest.mark.parametrize("n", [16, 33, 48])
+def test_setup_stencil27_equals_gen_plus_setup(sp, n):
+    """sb_setup_stencil27 (operator generated straight into the setup, int64
+    offsets: the C5 path) builds the same hierarchy as sb_gen_stencil27 +
+    sb_setup, bit for bit (level CSRs and aggregates)."""
+    cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40)
+    a = sp.Hierarchy.from_stencil27(n, n, n, 26.0, -1.0, cfg)
+    b = sp.Hierarchy(sp.poisson3d_27(n), cfg)
+    la, lb = a.levels(), b.levels()
+    assert len(la) == len(lb)
+    for k, (x, y) in enumerate(zip(la, lb)):
+        assert np.array_equal(np.asarray(x.A.row_ptr(), dtype=np.int64), np.asarray(y.A.row_ptr(), dtype=np.int64)), k
+        assert np.array_equal(x.A.col_idx(), y.A.col_idx()), k
+        assert np.array_equal(np.asarray(x.A.values()).view(np.uint64), np.asarray(y.A.values()).view(np.uint64)), k
+        if y.agg is not None:
+            assert np.array_equal(x.agg.fine_to_coarse, y.agg.fine_to_coarse), k
