@@ -898,6 +898,7 @@ __global__ void __launch_bounds__(kTileRows, SB_SG_MINB)
 #include "sb_rowpat.cuh"
 #include "sb_march.cuh"
 #include "sb_tblock.cuh"
+#include "sb_box2.cuh"
 
 // ===========================================================================
 // Cluster-resident tail: the deepest levels (each CTA's slice of every tail
@@ -1466,8 +1467,10 @@ struct DevLevel {
     int march_geo = -1, march_S = 0, march_N = 0, march_nqf = 0, march_nxb = 0, march_nyb = 0, march_ntiles = 0;
     int march_grid = 0;
     size_t march_tb = 0;
-    // two fused Jacobi sweeps per pass on structured 7-point levels (k_cross_tb2)
-    int tb = 0, tb_grid = 0;
+    // two fused Jacobi sweeps per launch on mid-size structured 7-point levels
+    // (k_cross_box2; tb = 2) or per HBM pass (experimental k_cross_tb2; tb = 1)
+    int tb = 0, tb_grid = 0, box_tx = 0;
+    BoxGeo box_geo{};
     TbGeo tb_geo{};
     size_t tb_smem = 0;
     const double *tb_tab = nullptr;
@@ -1812,8 +1815,8 @@ static void launch_jacobi(sb_ctx c, const DevLevel &l, cudaStream_t s, const dou
 
 // TMA descriptor of an nx x ny x nz f64 grid at p with an (bx, by, 1) box,
 // out-of-grid elements zero-filled; cached per context.
-static CUtensorMap tmap3d(sb_ctx c, const double *p, int nx, int ny, int nz, int bx, int by) {
-    const auto key = std::make_tuple(static_cast<const void *>(p), nx, ny, nz, bx, by);
+static CUtensorMap tmap3d(sb_ctx c, const double *p, int nx, int ny, int nz, int bx, int by, int bz = 1) {
+    const auto key = std::make_tuple(static_cast<const void *>(p), nx, ny, nz, bx, by * 4096 + bz);
     auto it = c->tmaps.find(key);
     if (it != c->tmaps.end()) return it->second;
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
@@ -1826,7 +1829,7 @@ static CUtensorMap tmap3d(sb_ctx c, const double *p, int nx, int ny, int nz, int
     CUtensorMap m;
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(nx), static_cast<cuuint64_t>(ny), static_cast<cuuint64_t>(nz)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(nx) * 8, static_cast<cuuint64_t>(nx) * ny * 8};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), 1};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), static_cast<cuuint32_t>(bz)};
     const cuuint32_t es[3] = {1, 1, 1};
     const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(p), dims, strides, box, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1836,9 +1839,21 @@ static CUtensorMap tmap3d(sb_ctx c, const double *p, int nx, int ny, int nz, int
     return m;
 }
 
+// two Jacobi sweeps xin -> out in one launch (k_cross_box2)
+static void launch_box2(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *xin, const double *f,
+                        double *out, double omega) {
+    const BoxGeo &g = l.box_geo;
+    const int TX = l.box_tx, TY = TX >= 16 ? 8 : 16, TZ = 8;
+    const CUtensorMap mx = tmap3d(c, xin, g.nx, g.ny, g.nz, TX + 4, TY + 4, TZ + 4);
+    const CUtensorMap mf = tmap3d(c, f, g.nx, g.ny, g.nz, TX + 4, TY + 2, TZ + 2);
+    launch_k(c, box2_kernel(TX), dim3(l.tb_grid), dim3(kTbThreads), box2_smem(TX), s, mx, mf, g, l.tb_tab, out,
+             omega);
+}
+
 // two Jacobi sweeps xin -> out in one pass (k_cross_tb2)
 static void launch_tb2(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *xin, const double *f,
                        double *out, double omega) {
+    if (l.tb == 2) return launch_box2(c, l, s, xin, f, out, omega);
     if (!kExperimental) throw sb::cuda_error("k_cross_tb2 is not built (SB_EXPERIMENTAL=0)");
     const TbGeo &g = l.tb_geo;
     const CUtensorMap mx = tmap3d(c, xin, g.nx, g.ny, g.nz, g.TX + 4, g.TY + 4);
@@ -2318,18 +2333,22 @@ static void build_march(sb_ctx c, DevLevel &D, int np, int w, const double *val,
 // out-of-grid neighbours; checked for every row. SB_TB=0 disables it,
 // SB_TB_MIN (rows, default 0) skips smaller levels.
 static constexpr size_t kTbSmemMax = 112 * 1024;  // two CTAs per SM
-static void build_tb(sb_ctx c, DevLevel &D, const std::vector<uint8_t> &pid, int np, const double *val,
-                     const int32_t *off, const uint8_t *len, const double *dg, const double *ry) {
-    if (!kExperimental) return;
-    const char *e = std::getenv("SB_TB");  // opt-in: measured slower (DESIGN.md §3.3)
-    if (!e || std::atoi(e) == 0) return;
-    const char *em = std::getenv("SB_TB_MIN");
-    if (em && D.n < std::atoll(em)) return;
+// A structured 7-point level for the fused two-sweep kernels: an nx x ny x nz
+// grid in (iz*ny + iy)*nx + ix order whose row pattern is a function of the
+// row's boundary class and whose absent slots are exactly the out-of-grid
+// neighbours (checked for every row). tab: per class the 7 values in CSR order
+// (+0.0 where absent), a_ii, RN(1/a_ii).
+static bool cross_classes(const DevLevel &D, const std::vector<uint8_t> &pid, const double *val, const int32_t *off,
+                          const uint8_t *len, const double *dg, const double *ry, int64_t &nx, int64_t &ny,
+                          int64_t &nz, std::vector<double> &tab) {
     const std::vector<int> &mo = D.main_o;
+    if (D.main_len != 7 || mo.size() < 7) return false;
     const int64_t N = mo[5], P = mo[6], n = D.n;
-    if (N < 2 || N % 2 != 0 || P % N != 0 || n % P != 0) return;
-    const int64_t nx = N, ny = P / N, nz = n / P;
-    if (ny < 2 || nz < 2 || nx > INT32_MAX / 2) return;
+    if (N < 2 || N % 2 != 0 || P % N != 0 || n % P != 0) return false;
+    nx = N;
+    ny = P / N;
+    nz = n / P;
+    if (ny < 2 || nz < 2 || nx > INT32_MAX / 2) return false;
     constexpr int wv = 8, wo = 8;  // SmemTab<7> row strides (doubles / int32)
     const int64_t want[7] = {-P, -N, -1, 0, 1, N, P};
     std::vector<int> cls_pat(kTbClasses, -1);
@@ -2342,27 +2361,77 @@ static void build_tb(sb_ctx c, DevLevel &D, const std::vector<uint8_t> &pid, int
             // the pattern's slots must be exactly the in-grid neighbours, in CSR order
             const bool present[7] = {iz > 0, iy > 0, ix > 0, true, ix < nx - 1, iy < ny - 1, iz < nz - 1};
             int j = 0;
-            for (int s = 0; s < 7; ++s) {
-                if (!present[s]) continue;
-                if (j >= len[q] || off[q * wo + j] != want[s]) return;
+            for (int sl = 0; sl < 7; ++sl) {
+                if (!present[sl]) continue;
+                if (j >= len[q] || off[q * wo + j] != want[sl]) return false;
                 ++j;
             }
-            if (j != len[q]) return;
+            if (j != len[q]) return false;
             cls_pat[k] = q;
         } else if (cls_pat[k] != q) {
-            return;
+            return false;
         }
     }
-    std::vector<double> tab(kTbTab, 0.0);
+    tab.assign(kTbTab, 0.0);
     for (int k = 0; k < kTbClasses; ++k) {
         const int q = cls_pat[k];
         if (q < 0) continue;
         int j = 0;
-        for (int s = 0; s < 7; ++s)
-            if (j < len[q] && off[q * wo + j] == want[s]) tab[k * 9 + s] = val[q * wv + j++];
+        for (int sl = 0; sl < 7; ++sl)
+            if (j < len[q] && off[q * wo + j] == want[sl]) tab[k * 9 + sl] = val[q * wv + j++];
         tab[k * 9 + 7] = dg[q];
         tab[k * 9 + 8] = ry[q];
     }
+    return true;
+}
+
+// k_cross_box2 on the latency-bound mid levels: SB_BOX2=0 disables it;
+// rows in [SB_BOX2_MIN, SB_BOX2_MAX] (defaults below, measured) take it.
+static void build_box2(sb_ctx c, DevLevel &D, const std::vector<uint8_t> &pid, const double *val,
+                       const int32_t *off, const uint8_t *len, const double *dg, const double *ry) {
+    const char *e = std::getenv("SB_BOX2");
+    if (e && std::atoi(e) == 0) return;
+    const char *emin = std::getenv("SB_BOX2_MIN"), *emax = std::getenv("SB_BOX2_MAX");
+    const int64_t nmin = emin ? std::atoll(emin) : 0, nmax = emax ? std::atoll(emax) : (int64_t(1) << 20);
+    if (D.n < nmin || D.n > nmax) return;
+    int64_t nx = 0, ny = 0, nz = 0;
+    std::vector<double> tab;
+    if (!cross_classes(D, pid, val, off, len, dg, ry, nx, ny, nz, tab)) return;
+    const int TX = nx >= 16 ? 16 : 8, TY = TX >= 16 ? 8 : 16, TZ = 8;
+    if (nx < 8 || nx * 8 % 16 != 0) return;
+    static const bool attr = [] {
+        for (int tx : {16, 8})
+            CK(cudaFuncSetAttribute(box2_kernel(tx), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(box2_smem(tx))));
+        return true;
+    }();
+    (void)attr;
+    BoxGeo g{};
+    g.nx = static_cast<int>(nx);
+    g.ny = static_cast<int>(ny);
+    g.nz = static_cast<int>(nz);
+    g.nbx = static_cast<int>((nx + TX - 1) / TX);
+    g.nby = static_cast<int>((ny + TY - 1) / TY);
+    g.nbz = static_cast<int>((nz + TZ - 1) / TZ);
+    auto *dt = dalloc<double>(c, kTbTab);
+    CK(cudaMemcpy(dt, tab.data(), sizeof(double) * kTbTab, cudaMemcpyHostToDevice));
+    D.tb_tab = dt;
+    D.box_geo = g;
+    D.box_tx = TX;
+    D.tb_grid = g.nbx * g.nby * g.nbz;
+    D.tb = 2;
+}
+
+static void build_tb(sb_ctx c, DevLevel &D, const std::vector<uint8_t> &pid, int np, const double *val,
+                     const int32_t *off, const uint8_t *len, const double *dg, const double *ry) {
+    if (!kExperimental) return;
+    const char *e = std::getenv("SB_TB");  // opt-in: measured slower (DESIGN.md §3.4)
+    if (!e || std::atoi(e) == 0) return;
+    const char *em = std::getenv("SB_TB_MIN");
+    if (em && D.n < std::atoll(em)) return;
+    int64_t nx = 0, ny = 0, nz = 0;
+    std::vector<double> tab;
+    if (!cross_classes(D, pid, val, off, len, dg, ry, nx, ny, nz, tab)) return;
     (void)np;
     // tile: 64 x 16 columns (the whole x-line on narrow levels), <= kTbSmemMax of rings
     TbGeo g{};
@@ -2579,7 +2648,10 @@ static bool build_rpat(sb_ctx c, const HostCsr &A, DevLevel &D) {
             D.box_pair = kind;
         }
     }
-    if (D.box_pair == 2 && w == 7) build_tb(c, D, pid, np, val, off, len, dg, ry);
+    if (D.box_pair == 2 && w == 7) {
+        build_tb(c, D, pid, np, val, off, len, dg, ry);
+        if (!D.tb) build_box2(c, D, pid, val, off, len, dg, ry);
+    }
     auto *dp = dalloc<uint8_t>(c, A.n + 16);
     CK(cudaMemcpy(dp, pid.data(), pid.size(), cudaMemcpyHostToDevice));
     auto *dt = dalloc<unsigned char>(c, static_cast<int64_t>(tb));
@@ -3604,9 +3676,14 @@ int sb_level_residency(sb_ctx c, int k, int *on_host, int64_t *matrix_bytes) {
 int sb_level_fused_sweeps(sb_ctx c, int k, int *geo) {
     try {
         const DevLevel &l = level_of(c, k);
-        if (geo && l.tb) {
+        if (geo && l.tb == 1) {
             const TbGeo &g = l.tb_geo;
             const int v[8] = {g.nx, g.ny, g.nz, g.TX, g.TY, g.ZL, l.tb_grid, static_cast<int>(l.tb_smem)};
+            std::memcpy(geo, v, sizeof v);
+        } else if (geo && l.tb == 2) {
+            const BoxGeo &g = l.box_geo;
+            const int v[8] = {g.nx, g.ny, g.nz, l.box_tx, l.box_tx >= 16 ? 8 : 16, 8, l.tb_grid,
+                              static_cast<int>(box2_smem(l.box_tx))};
             std::memcpy(geo, v, sizeof v);
         }
         return l.tb ? 2 : 1;

@@ -212,3 +212,22 @@ def test_cross_rr_vcycle_identical():
         assert out.returncode == 0, out.stderr[-2000:]
         vs.append(out.stdout)
     assert vs[0] and vs[0] == vs[1]
+
+
+def test_cross5_default_selection(sp, monkeypatch):
+    """Default 5-point selection (SB_CROSS5 unset): the pair kernel on 2D levels
+    of >= 2^19 rows only (k_crosspair at L0 of a 1024x512 grid, k_rowpat at L1);
+    the V-cycle is bitwise the one with the pair kernel off everywhere."""
+    A = sp.poisson2d(1024, 512)
+    cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40)
+    cp = sp.CycleParams.from_config(cfg)
+    f = sp.rhs_random(A.nrows(), 4)
+    monkeypatch.delenv("SB_CROSS5", raising=False)
+    h = sp.Hierarchy(A, cfg)
+    assert _sweep_kernel(sp, h, 0) == "k_crosspair" and _sweep_kernel(sp, h, 1) == "k_rowpat"
+    v = sp.vcycle(h, 0, f, np.zeros(A.nrows()), cp)
+    monkeypatch.setenv("SB_CROSS5", "0")
+    h0 = sp.Hierarchy(A, cfg)
+    assert _sweep_kernel(sp, h0, 0) == "k_rowpat"
+    v0 = sp.vcycle(h0, 0, f, np.zeros(A.nrows()), cp)
+    assert np.array_equal(v.view(np.uint64), v0.view(np.uint64))
