@@ -1,6 +1,11 @@
 // Two Jacobi sweeps in one launch on the mid-size structured 7-point levels
 // (k_cross_box2), included by sb_runtime.cu after sb_tblock.cuh (whose level
-// analysis it shares: build_tb's class table, TMA tensor maps).
+// analysis it shares: the class table, TMA tensor maps). EXPERIMENTAL: bitwise
+// equal to two sweeps, but measured slower than two k_crosspair / k_rowpat
+// launches at every level (C2 L9: 131 vs 106 us from the level down; the
+// in-CTA chain load -> sweep -> barrier -> sweep costs ~6 us per launch
+// against ~2.1 us per plain kernel), with the boxes loaded by TMA or by
+// plain per-thread loads alike.
 //
 // The mid levels of the 3-D hierarchies (~32K .. 1M rows) are latency-bound:
 // a kernel of the graph costs ~2-3.5 us whatever its size (launch, the
@@ -15,6 +20,10 @@
 // (-P, -N, -1, 0, 1, N, P); an absent slot is an out-of-grid neighbour whose x
 // is the TMA's +0.0 and whose table value is +0.0, so it adds +0 * +0 = +0.0
 // to a running sum that is never -0.0; x' of an out-of-grid position is +0.0.
+
+#ifndef SB_BOX2_TMA
+#define SB_BOX2_TMA 0  // 1: the boxes arrive by TMA (measured slower: one serial ~1.5 us load per CTA)
+#endif
 
 struct BoxGeo {
     int nx, ny, nz;
@@ -65,7 +74,8 @@ __device__ __forceinline__ void box_rows(const double *tab, const int (&c)[K], c
 template <int TX, int TY, int TZ>
 __global__ void __launch_bounds__(kTbThreads, 3)
     k_cross_box2(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mf, const BoxGeo g,
-                 const double *__restrict__ ctab, double *__restrict__ out, double omega) {
+                 const double *__restrict__ ctab, double *__restrict__ out, double omega, const double *xglob,
+                 const double *fglob) {
     using B = Box2<TX, TY, TZ>;
     constexpr int WX = B::WX, SXP = B::WX * B::HX, SFP = B::WX * B::HF;  // line / plane strides
     constexpr int N1 = (TX + 2) * (TY + 2) * (TZ + 2), N2 = TX * TY * TZ;
@@ -88,12 +98,46 @@ __global__ void __launch_bounds__(kTbThreads, 3)
     }
     __syncthreads();
     pdl_wait();  // x and f come from the predecessor
+#if SB_BOX2_TMA
     if (threadIdx.x == 0) {
         mbar_expect_tx(bar, static_cast<uint32_t>((B::NX + B::NF) * 8));
         tma_load_3d(xs, &mx, x0 - 2, y0 - 2, z0 - 2, bar);
         tma_load_3d(fs, &mf, x0 - 2, y0 - 1, z0 - 1, bar);
     }
     mbar_wait(bar, 0u);
+#else
+    // every thread loads its share of both boxes (all loads in flight at once:
+    // one L2 round trip), out-of-grid elements +0.0
+    {
+        const double *xg = xglob;
+        const double *fg = fglob;
+        constexpr int LX = (B::NX + kTbThreads - 1) / kTbThreads, LF = (B::NF + kTbThreads - 1) / kTbThreads;
+        double vx[LX], vf[LF];
+#pragma unroll
+        for (int k = 0; k < LX; ++k) {
+            const int q = threadIdx.x + k * kTbThreads;
+            const int u = q % B::WX, v = (q / B::WX) % B::HX, w = q / (B::WX * B::HX);
+            const int gx = x0 - 2 + u, gy = y0 - 2 + v, gz = z0 - 2 + w;
+            const bool ok = q < B::NX && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz;
+            vx[k] = ok ? __ldcg(xg + (static_cast<int64_t>(gz) * g.ny + gy) * g.nx + gx) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < LF; ++k) {
+            const int q = threadIdx.x + k * kTbThreads;
+            const int u = q % B::WX, v = (q / B::WX) % B::HF, w = q / (B::WX * B::HF);
+            const int gx = x0 - 2 + u, gy = y0 - 1 + v, gz = z0 - 1 + w;
+            const bool ok = q < B::NF && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny && gz >= 0 && gz < g.nz;
+            vf[k] = ok ? __ldcg(fg + (static_cast<int64_t>(gz) * g.ny + gy) * g.nx + gx) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < LX; ++k)
+            if (threadIdx.x + k * kTbThreads < B::NX) xs[threadIdx.x + k * kTbThreads] = vx[k];
+#pragma unroll
+        for (int k = 0; k < LF; ++k)
+            if (threadIdx.x + k * kTbThreads < B::NF) fs[threadIdx.x + k * kTbThreads] = vf[k];
+    }
+    __syncthreads();
+#endif
     // sweep 1 on the box + 1-wide halo: F-position (u, v, w) <-> grid (x0-1+u,
     // y0-1+v, z0-1+w); x box index (w+1) SXP + (v+1) WX + u+1; f / x' index
     // w SFP + v WX + u+1
@@ -149,7 +193,15 @@ __global__ void __launch_bounds__(kTbThreads, 3)
     }
 }
 
-using Box2Kernel = void (*)(CUtensorMap, CUtensorMap, BoxGeo, const double *, double *, double);
+using Box2Kernel = void (*)(CUtensorMap, CUtensorMap, BoxGeo, const double *, double *, double, const double *,
+                           const double *);
 // instances: TX = 16 (box 16 x 8 x 8) or 8 (box 8 x 16 x 8), 1024 rows per CTA
-static Box2Kernel box2_kernel(int TX) { return TX >= 16 ? k_cross_box2<16, 8, 8> : k_cross_box2<8, 16, 8>; }
+static Box2Kernel box2_kernel(int TX) {
+#if SB_EXPERIMENTAL
+    return TX >= 16 ? k_cross_box2<16, 8, 8> : k_cross_box2<8, 16, 8>;
+#else
+    (void)TX;
+    return nullptr;
+#endif
+}
 static size_t box2_smem(int TX) { return TX >= 16 ? Box2<16, 8, 8>::smem() : Box2<8, 16, 8>::smem(); }

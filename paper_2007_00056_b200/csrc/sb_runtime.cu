@@ -1847,7 +1847,7 @@ static void launch_box2(sb_ctx c, const DevLevel &l, cudaStream_t s, const doubl
     const CUtensorMap mx = tmap3d(c, xin, g.nx, g.ny, g.nz, TX + 4, TY + 4, TZ + 4);
     const CUtensorMap mf = tmap3d(c, f, g.nx, g.ny, g.nz, TX + 4, TY + 2, TZ + 2);
     launch_k(c, box2_kernel(TX), dim3(l.tb_grid), dim3(kTbThreads), box2_smem(TX), s, mx, mf, g, l.tb_tab, out,
-             omega);
+             omega, xin, f);
 }
 
 // two Jacobi sweeps xin -> out in one pass (k_cross_tb2)
@@ -2385,12 +2385,13 @@ static bool cross_classes(const DevLevel &D, const std::vector<uint8_t> &pid, co
     return true;
 }
 
-// k_cross_box2 on the latency-bound mid levels: SB_BOX2=0 disables it;
-// rows in [SB_BOX2_MIN, SB_BOX2_MAX] (defaults below, measured) take it.
+// k_cross_box2 on the latency-bound mid levels (EXPERIMENTAL=1 and SB_BOX2=1;
+// rows in [SB_BOX2_MIN, SB_BOX2_MAX] take it).
 static void build_box2(sb_ctx c, DevLevel &D, const std::vector<uint8_t> &pid, const double *val,
                        const int32_t *off, const uint8_t *len, const double *dg, const double *ry) {
-    const char *e = std::getenv("SB_BOX2");
-    if (e && std::atoi(e) == 0) return;
+    if (!kExperimental) return;
+    const char *e = std::getenv("SB_BOX2");  // opt-in: measured slower than two kernels
+    if (!e || std::atoi(e) == 0) return;
     const char *emin = std::getenv("SB_BOX2_MIN"), *emax = std::getenv("SB_BOX2_MAX");
     const int64_t nmin = emin ? std::atoll(emin) : 0, nmax = emax ? std::atoll(emax) : (int64_t(1) << 20);
     if (D.n < nmin || D.n > nmax) return;

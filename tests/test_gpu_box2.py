@@ -1,5 +1,5 @@
-"""Two Jacobi sweeps per launch (k_cross_box2, csrc/sb_box2.cuh) on mid-size
-structured 7-point levels: bitwise equal to the reference's sweeps
+"""Two Jacobi sweeps per launch (k_cross_box2, csrc/sb_box2.cuh; built with
+make EXPERIMENTAL=1, enabled with SB_BOX2=1) on mid-size structured 7-point levels: bitwise equal to the reference's sweeps
 (inc/smoother.hpp:95-123) for any sweep count, including non-finite inputs
 and levels whose tiles / z-chunks do not divide the grid; V-cycles and whole
 solves bitwise equal to the unfused path (SB_BOX2=0)."""
@@ -10,11 +10,14 @@ import pytest
 
 from helpers import rel
 
-pytestmark = pytest.mark.gpu
+from conftest import needs_experimental
+
+pytestmark = [pytest.mark.gpu, needs_experimental]
 
 
 @pytest.fixture(autouse=True)
 def _box_all(monkeypatch):
+    monkeypatch.setenv("SB_BOX2", "1")  # opt-in (measured slower)
     monkeypatch.setenv("SB_BOX2_MIN", "0")  # every structured level of these small grids takes it
 
 GRIDS = {
