@@ -284,6 +284,22 @@ int sb_dist_create(sb_hier h, int rank, int nranks, const unsigned char *nccl_id
                    const sb_device_opts *opts, sb_dist *out);
 int sb_dist_create_local(sb_hier h, int nranks, int64_t gather_rows, const sb_device_opts *opts,
                          sb_dist *out);
+/* Peer-memory (P2P) transport instead of NCCL: halo / straddle / gather
+ * exchanges are gathers straight out of the peers' own rows, dot products sum
+ * every rank's partials in rank order; ordering through per-rank epoch
+ * counters in peer-visible memory (publish after the producing kernels, one
+ * spinning thread waits for the peers). One rank per process:
+ * sb_dist_create_p2p, then sb_dist_p2p_export (CUDA IPC handles of the
+ * buffers peers read; call with buf = NULL for the length), exchange the blobs
+ * out of band, sb_dist_p2p_connect with every rank's blob in rank order
+ * (len_each bytes apart). sb_dist_create_local_p2p: nranks in-process ranks on
+ * one device over the same protocol (tests). */
+int sb_dist_create_p2p(sb_hier h, int rank, int nranks, int64_t gather_rows, const sb_device_opts *opts,
+                       sb_dist *out);
+int sb_dist_p2p_export(sb_dist d, unsigned char *buf, int64_t cap, int64_t *len);
+int sb_dist_p2p_connect(sb_dist d, const unsigned char *blobs, int64_t len_each);
+int sb_dist_create_local_p2p(sb_hier h, int nranks, int64_t gather_rows, const sb_device_opts *opts,
+                             sb_dist *out);
 void sb_dist_destroy(sb_dist d);
 int sb_dist_rows(sb_dist d, int local_rank, int64_t *lo, int64_t *hi, int *first_replicated);
 int sb_dist_pcg(sb_dist d, const sb_cycle *cp, const double *b, double *x, double tol, int max_iters,

@@ -83,7 +83,8 @@ EXPORTS = [
     "sb_free_csr", "sb_gen_rhs_random", "sb_last_solve_ms", "sb_last_solve_launches", "sb_time_kernel", "sb_time_kernel_cold", "sb_vcycle_launches", "sb_tail_trace",
     "sb_tail_info", "sb_level_format", "sb_level_march", "sb_level_sweep_kernel", "sb_level_fused_sweeps", "sb_build_flags", "sb_level_residency", "sb_partition", "sb_partition_free", "sb_partition_info",
     "sb_partition_level", "sb_partition_exchange", "sb_nccl_unique_id", "sb_dist_create",
-    "sb_dist_create_local", "sb_dist_destroy", "sb_dist_rows", "sb_dist_pcg", "sb_dist_pbicgstab",
+    "sb_dist_create_local", "sb_dist_create_local_p2p", "sb_dist_create_p2p", "sb_dist_p2p_export",
+    "sb_dist_p2p_connect", "sb_dist_destroy", "sb_dist_rows", "sb_dist_pcg", "sb_dist_pbicgstab",
     "sb_dist_vcycle", "sb_dist_last_solve_ms", "sb_dist_last_launches", "sb_galerkin_gpu", "sb_host_bytes", "sb_setup_stencil27",
     "sb_read_matrix_market", "sb_write_matrix_market",
 ]
@@ -148,6 +149,10 @@ _SIGS = {
     "sb_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "sb_dist_create": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p, C.c_int64, C.POINTER(sb_device_opts), C.POINTER(_P)]),
     "sb_dist_create_local": (C.c_int, [_P, C.c_int, C.c_int64, C.POINTER(sb_device_opts), C.POINTER(_P)]),
+    "sb_dist_create_local_p2p": (C.c_int, [_P, C.c_int, C.c_int64, C.POINTER(sb_device_opts), C.POINTER(_P)]),
+    "sb_dist_create_p2p": (C.c_int, [_P, C.c_int, C.c_int, C.c_int64, C.POINTER(sb_device_opts), C.POINTER(_P)]),
+    "sb_dist_p2p_export": (C.c_int, [_P, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]),
+    "sb_dist_p2p_connect": (C.c_int, [_P, C.c_char_p, C.c_int64]),
     "sb_dist_destroy": (None, [_P]),
     "sb_dist_rows": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
     "sb_dist_pcg": (C.c_int, [_P, C.POINTER(sb_cycle), _P, _P, C.c_double, C.c_int, C.POINTER(sb_report), C.c_int]),

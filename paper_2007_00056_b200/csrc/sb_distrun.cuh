@@ -10,9 +10,16 @@
 // are rank-local deterministic reductions + an allreduce, after which a
 // one-thread kernel runs the reference's scalar logic on every rank.
 //
-// Two transports:
+// Three transports:
 //  * NCCL (one rank per process / GPU; libnccl.so.2 loaded with dlopen):
 //    grouped send/recv for exchanges, ncclAllReduce for dots;
+//  * peer memory (P2P, one rank per process / GPU, or in-process ranks): every
+//    rank exports the buffers its peers read (CUDA IPC handles; on one node
+//    they map over NVLink / NVSwitch) and a monotonic epoch counter. An
+//    exchange is: publish (epoch += 1 after the producing kernels), wait until
+//    the peers' epochs reach ours (one spinning thread), then the receiver
+//    gathers its ghost values straight out of the peers' own rows. Dot products
+//    sum every rank's partials in rank order (deterministic, no NCCL);
 //  * in-process "virtual ranks" (all ranks in this process, one device):
 //    receivers pull peer values with a gather kernel; ordering through CUDA
 //    events. Used to test the partitioned GPU path on a single GPU.
@@ -101,6 +108,58 @@ __global__ void k_prolong_dist(int64_t n, const int32_t *__restrict__ parent, co
     }
 }
 
+// ---- peer-memory (P2P) transport kernels ----
+// publish: every kernel this rank issued before is complete; make its writes
+// visible system-wide, then advance the epoch (single writer)
+__global__ void k_p2p_publish(unsigned long long *epoch) {
+    pdl_wait();
+    __threadfence_system();
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(epoch) + 1ull;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(epoch), "l"(e) : "memory");
+}
+// wait until each listed peer's epoch reached ours (acquire)
+__global__ void k_p2p_wait(const unsigned long long *epoch, const unsigned long long *const *peer_epoch, int npeers) {
+    pdl_wait();
+    const unsigned long long want = *reinterpret_cast<const volatile unsigned long long *>(epoch);
+    for (int i = threadIdx.x; i < npeers; i += blockDim.x) {
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(peer_epoch[i]) : "memory");
+        } while (v < want);
+    }
+    __syncthreads();
+}
+// ghost(dst[i]) = peer_own[src[i]]: the receiver pulls its ghost values out of
+// a peer's own rows (peer memory: L2-bypassing loads)
+__global__ void k_p2p_gather(int64_t n, const double *peer_own, const int32_t *__restrict__ src,
+                             double *__restrict__ dst) {
+    pdl_wait();
+    GRID_LOOP(i, n) dst[i] = __ldcv(peer_own + src[i]);
+}
+__global__ void k_p2p_copy(int64_t n, const double *src, double *__restrict__ dst) {
+    pdl_wait();
+    GRID_LOOP(i, n) dst[i] = __ldcv(src + i);
+}
+// every rank's partials (slot `slot`) summed in rank order -> st->red
+__global__ void k_p2p_put(const double *part, double *slotbase, const int *slot) {
+    pdl_wait();
+    double *dst = slotbase + 2 * (*slot & 1);
+    dst[0] = part[0];
+    dst[1] = part[1];
+}
+__global__ void k_p2p_sum(const double *const *slots, int nranks, int *slot, double *out) {
+    pdl_wait();
+    const int sl = *slot & 1;
+    double a = 0.0, b = 0.0;
+    for (int r = 0; r < nranks; ++r) {
+        a += __ldcv(slots[r] + 2 * sl);
+        b += __ldcv(slots[r] + 2 * sl + 1);
+    }
+    out[0] = a;
+    out[1] = b;
+    *slot = sl + 1;
+}
+
 // in-process allreduce: every rank sums the ranks' partials in rank order
 __global__ void k_sum_partials(const double *const *parts, int nranks, double *out) {
     pdl_wait();
@@ -140,6 +199,21 @@ struct RankDev {
     cudaEvent_t ready = nullptr, done = nullptr;
     cudaStream_t s = nullptr;      // stream the solve is emitted on (the context stream, or a graph body's)
     double **part_ptrs = nullptr;  // in-process: device array of every rank's st->part
+    // P2P transport
+    unsigned long long *epoch = nullptr;  // exported
+    double *pslots = nullptr;             // exported: 2 slots x 2 partials
+    int *pslot = nullptr;                 // which slot the next allreduce uses
+    const unsigned long long **peer_epochs = nullptr;  // device: every rank's epoch pointer (rank order)
+    const double **peer_slots = nullptr;               // device: every rank's pslots (rank order)
+    std::vector<const unsigned long long *> h_peer_epochs;
+    std::vector<std::vector<const double *>> peer_own;  // [buffer id][rank]: that rank's own-row-0 pointer
+    std::map<const double *, int> buf_id;               // own-row-0 pointer -> exported buffer id
+    std::vector<std::pair<void *, int64_t>> exported;   // (allocation base, own-row-0 offset in bytes) per id
+    std::vector<const double *> exported_own;           // own-row-0 pointer per id
+    std::vector<void *> opened;                          // IPC mappings to close
+    // per distributed level and plan (halo, rx, px): the peers' send indices
+    // for this rank, aligned with recv_off
+    std::vector<std::array<int32_t *, 3>> src_idx;
     int64_t lo = 0, hi = 0;        // owned rows of level 0
 };
 
@@ -152,7 +226,11 @@ struct sb_dist_s {
     ncclComm_t comm = nullptr;
     double last_ms = 0.0;
     int last_launches = 0;
-    std::map<std::string, sb::GraphEntry> cache;  // captured whole-solve graphs (NCCL mode)
+    std::map<std::string, sb::GraphEntry> cache;  // captured whole-solve graphs (NCCL / P2P mode)
+    bool p2p = false;       // peer-memory transport
+    bool connected = false; // P2P: peers' buffers mapped
+    bool graph_failed = false;  // capture failed once: eager from then on (graph_error says why)
+    std::string graph_error;
 };
 
 namespace sb {
@@ -210,6 +288,16 @@ static void barrier_local(sb_dist d) {
             if (&q != &r) CK(cudaStreamWaitEvent(r.s, q.done, 0));
 }
 
+// P2P: publish this rank's epoch, then wait until every rank reached it (the
+// producers' writes are visible; no rank can overwrite a buffer a peer still
+// reads, because every rank publishes only after its previous gathers)
+static void p2p_sync(sb_dist d) {
+    for (auto &r : d->R) launch_k(r.c, k_p2p_publish, dim3(1), dim3(1), 0, r.s, r.epoch);
+    for (auto &r : d->R)
+        launch_k(r.c, k_p2p_wait, dim3(1), dim3(32), 0, r.s, static_cast<const unsigned long long *>(r.epoch),
+                 static_cast<const unsigned long long *const *>(r.peer_epochs), d->nranks);
+}
+
 // Fill the ghost entries of every rank r from own(q) of its peers q, per the
 // level-k plan `which`: chunk j of r lands at dst(r) + recv_dst[j] (halo: dst
 // is the own-rows pointer of the x vector; rx / px: the packed ghost buffers).
@@ -219,6 +307,23 @@ static void exchange(sb_dist d, int k, int which, const std::function<const doub
         DistLevel &L = r.D[static_cast<size_t>(k)];
         return which == 0 ? L.halo : which == 1 ? L.rx : L.px;
     };
+    if (d->p2p) {
+        p2p_sync(d);
+        for (auto &r : d->R) {
+            DevExch &e = plan(r);
+            if (e.recv_peers.empty()) continue;
+            const int id = r.buf_id.at(own(r));
+            const int32_t *src = r.src_idx[static_cast<size_t>(k)][static_cast<size_t>(which)];
+            for (size_t j = 0; j < e.recv_peers.size(); ++j) {
+                const int64_t cnt = e.recv_off[j + 1] - e.recv_off[j];
+                if (!cnt) continue;
+                launch_k(r.c, k_p2p_gather, dim3(vec_grid(cnt)), dim3(kVecThreads), 0, r.s, cnt,
+                         r.peer_own[static_cast<size_t>(id)][static_cast<size_t>(e.recv_peers[j])],
+                         src + e.recv_off[j], ghost(r) + e.recv_dst[j]);
+            }
+        }
+        return;
+    }
     if (d->local) {
         for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.s));
         for (auto &r : d->R) {
@@ -257,6 +362,19 @@ static void exchange(sb_dist d, int k, int which, const std::function<const doub
 
 // every rank ends with the whole vector v(r) whose piece [b[q], b[q+1]) rank q owns
 static void allgatherv(sb_dist d, const std::vector<int64_t> &b, const std::function<double *(RankDev &)> &v) {
+    if (d->p2p) {
+        p2p_sync(d);
+        for (auto &r : d->R) {
+            const int id = r.buf_id.at(v(r));
+            for (int q = 0; q < d->nranks; ++q) {
+                const int64_t cnt = b[q + 1] - b[q];
+                if (q == r.rank || cnt == 0) continue;
+                launch_k(r.c, k_p2p_copy, dim3(vec_grid(cnt)), dim3(kVecThreads), 0, r.s, cnt,
+                         r.peer_own[static_cast<size_t>(id)][static_cast<size_t>(q)] + b[q], v(r) + b[q]);
+            }
+        }
+        return;
+    }
     if (d->local) {
         for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.s));
         for (auto &r : d->R)
@@ -285,7 +403,15 @@ static void allgatherv(sb_dist d, const std::vector<int64_t> &b, const std::func
 
 // st->red = sum over ranks of st->part; then the scalar logic `op` on every rank
 static void allreduce_logic(sb_dist d, int op, CondSet cs = CondSet{{0, 0}, 0}) {
-    if (d->local) {
+    if (d->p2p) {
+        for (auto &r : d->R)
+            launch_k(r.c, k_p2p_put, dim3(1), dim3(1), 0, r.s, static_cast<const double *>(r.c->st->part), r.pslots,
+                     static_cast<const int *>(r.pslot));
+        p2p_sync(d);
+        for (auto &r : d->R)
+            launch_k(r.c, k_p2p_sum, dim3(1), dim3(1), 0, r.s, static_cast<const double *const *>(r.peer_slots),
+                     d->nranks, r.pslot, r.c->st->red);
+    } else if (d->local) {
         for (auto &r : d->R) CK(cudaEventRecord(r.ready, r.s));
         for (auto &r : d->R) {
             for (auto &q : d->R)
@@ -647,6 +773,89 @@ static void build_rank(sb_dist d, RankDev &R, const Hier &h, int rank, int64_t g
     CK(cudaEventCreateWithFlags(&R.done, cudaEventDisableTiming));
 }
 
+// ---- peer-memory transport: buffers, plans, connection -----------------------------
+
+static void *alloc_base(const void *p) {
+    static PFN_cuMemGetAddressRange_v3020 range = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) throw cuda_error("cuMemGetAddressRange unavailable");
+        return reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    }();
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+        throw cuda_error("cuMemGetAddressRange failed");
+    return reinterpret_cast<void *>(base);
+}
+
+// The buffers peers read, in the same order on every rank (ids): the x / t
+// vectors of every distributed level, the residual, the first replicated
+// level's rhs, the Krylov vectors; then the partial-sum slots. Plus the epoch.
+static void p2p_register(sb_dist d, RankDev &R) {
+    sb_ctx c = R.c;
+    R.epoch = dalloc<unsigned long long>(c, 1, false);
+    R.pslots = dalloc<double>(c, 4, false);
+    R.pslot = dalloc<int>(c, 1, false);
+    auto reg = [&](const double *own) {
+        if (!own) throw runtime_error("p2p_register: null buffer");
+        if (R.buf_id.count(own)) throw runtime_error("p2p_register: buffer registered twice");
+        R.buf_id[own] = static_cast<int>(R.exported.size());
+        void *base = alloc_base(own);
+        R.exported.push_back({base, reinterpret_cast<const char *>(own) - static_cast<const char *>(base)});
+        R.exported_own.push_back(own);
+    };
+    const int L = static_cast<int>(c->L.size());
+    for (int k = 0; k < d->fr; ++k) {
+        reg(c->L[static_cast<size_t>(k)].x);
+        reg(c->L[static_cast<size_t>(k)].t);
+    }
+    reg(c->rs);
+    if (d->fr > 0 && d->fr < L) reg(c->L[static_cast<size_t>(d->fr)].f);
+    for (double *v : c->kv) reg(v);
+    reg(R.pslots);
+}
+
+// src_idx[k][which]: for each recv chunk of this rank's plan, the SENDING
+// peer's own-row indices (its send list towards this rank), concatenated in
+// recv order. parts(q) = rank q's host partition.
+static void p2p_plans(RankDev &R, const std::function<const Partition &(int)> &parts) {
+    R.src_idx.assign(R.D.size(), {nullptr, nullptr, nullptr});
+    for (size_t k = 0; k < R.D.size(); ++k) {
+        if (!R.D[k].dist) continue;
+        for (int which = 0; which < 3; ++which) {
+            const DistLevel &L = R.D[k];
+            const DevExch &e = which == 0 ? L.halo : which == 1 ? L.rx : L.px;
+            std::vector<int32_t> idx;
+            for (size_t j = 0; j < e.recv_peers.size(); ++j) {
+                const PartLevel &pl = parts(e.recv_peers[j]).L[k];
+                const Exchange &x = which == 0 ? pl.halo : which == 1 ? pl.rx : pl.px;
+                size_t jj = 0;
+                while (jj < x.send_peers.size() && x.send_peers[jj] != R.rank) ++jj;
+                if (jj == x.send_peers.size()) throw runtime_error("p2p: inconsistent exchange plans");
+                const int64_t cnt = x.send_off[jj + 1] - x.send_off[jj];
+                if (cnt != e.recv_off[j + 1] - e.recv_off[j]) throw runtime_error("p2p: plan size mismatch");
+                idx.insert(idx.end(), x.send_idx.begin() + x.send_off[jj], x.send_idx.begin() + x.send_off[jj + 1]);
+            }
+            auto *dv = dalloc<int32_t>(R.c, std::max<int64_t>(static_cast<int64_t>(idx.size()), 1), false);
+            if (!idx.empty())
+                CK(cudaMemcpy(dv, idx.data(), sizeof(int32_t) * idx.size(), cudaMemcpyHostToDevice));
+            R.src_idx[k][static_cast<size_t>(which)] = dv;
+        }
+    }
+}
+
+// device tables of every rank's epoch and partial slots, in rank order
+static void p2p_tables(RankDev &R, const std::vector<const unsigned long long *> &epochs,
+                       const std::vector<const double *> &slots) {
+    R.h_peer_epochs = epochs;
+    R.peer_epochs = dalloc<const unsigned long long *>(R.c, static_cast<int64_t>(epochs.size()), false);
+    CK(cudaMemcpy(R.peer_epochs, epochs.data(), sizeof(void *) * epochs.size(), cudaMemcpyHostToDevice));
+    R.peer_slots = dalloc<const double *>(R.c, static_cast<int64_t>(slots.size()), false);
+    CK(cudaMemcpy(R.peer_slots, slots.data(), sizeof(void *) * slots.size(), cudaMemcpyHostToDevice));
+}
+
 static int run_dist(sb_dist d, SolveKind kind, const sb_cycle *cpa, const double *b, double *x, double tol,
                     int max_iters, sb_report *rep, bool device_ptrs) {
     // (graph mode: b and x are staged through the rank's own vectors, so the
@@ -654,6 +863,7 @@ static int run_dist(sb_dist d, SolveKind kind, const sb_cycle *cpa, const double
     const auto t0 = std::chrono::steady_clock::now();
     const char *who = kind == K_PCG ? "pcg" : "pbicgstab";
     if (!(tol > 0.0)) throw invalid_argument(std::string(who) + ": tol must be > 0");
+    if (d->p2p && !d->connected) throw invalid_argument(std::string(who) + ": P2P ranks not connected");
     Cyc cyc;
     const Cyc *cp = nullptr;
     if (cpa) {
@@ -684,7 +894,7 @@ static int run_dist(sb_dist d, SolveKind kind, const sb_cycle *cpa, const double
     for (auto &r : d->R) CK(cudaEventRecord(r.c->ev0, r.c->stream));
     // one rank per process: the whole solve as one graph (NCCL calls captured);
     // in-process ranks or use_graphs = 0: eager, host-evaluated conditions
-    const bool graph = !d->local && r0.c->graphs;
+    bool graph = d->R.size() == 1 && !d->local && r0.c->graphs && !d->graph_failed;
     if (graph) {
         const std::string key = key_of(kind == K_PCG ? "dist-pcg" : "dist-bicg", cp, nullptr, nullptr, r0.c->hist_r);
         auto it = d->cache.find(key);
@@ -692,15 +902,31 @@ static int run_dist(sb_dist d, SolveKind kind, const sb_cycle *cpa, const double
             GraphEntry e;
             r0.c->plan = LaunchPlan{};
             e.g = begin_capture(r0.c);
-            if (kind == K_PCG) dist_pcg(d, cp);
-            else dist_bicg(d, cp);
-            end_capture(r0.c, e.g);
-            CK(cudaGraphInstantiate(&e.exec, e.g, 0));
-            e.plan = r0.c->plan;
-            it = d->cache.emplace(key, e).first;
+            try {
+                if (kind == K_PCG) dist_pcg(d, cp);
+                else dist_bicg(d, cp);
+                end_capture(r0.c, e.g);
+                CK(cudaGraphInstantiate(&e.exec, e.g, 0));
+                e.plan = r0.c->plan;
+                it = d->cache.emplace(key, e).first;
+            } catch (const std::exception &ex) {
+                // a transport that cannot be captured (e.g. a library inserting
+                // host nodes into conditional bodies): run eagerly from now on
+                cudaGraph_t dummy = nullptr;
+                cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+                cudaStreamIsCapturing(r0.c->stream, &st);
+                if (st != cudaStreamCaptureStatusNone) cudaStreamEndCapture(r0.c->stream, &dummy);
+                if (dummy) cudaGraphDestroy(dummy);
+                if (e.g) cudaGraphDestroy(e.g);
+                cudaGetLastError();
+                d->graph_failed = true;
+                d->graph_error = ex.what();
+                graph = false;
+            }
         }
-        CK(cudaGraphLaunch(it->second.exec, r0.c->stream));
-    } else {
+        if (graph) CK(cudaGraphLaunch(it->second.exec, r0.c->stream));
+    }
+    if (!graph) {
         tl_eager = true;
         try {
             if (kind == K_PCG) dist_pcg(d, cp);
@@ -809,8 +1035,149 @@ int sb_dist_create_local(sb_hier hh, int nranks, int64_t gather_rows, const sb_d
     return rc;
 }
 
+// In-process ranks over the peer-memory transport (the peers' buffers are
+// plain device pointers here): the P2P protocol and kernels on one GPU.
+int sb_dist_create_local_p2p(sb_hier hh, int nranks, int64_t gather_rows, const sb_device_opts *opts,
+                             sb_dist *out) {
+    sb_dist d = nullptr;
+    const int rc = guard([&] {
+        Hier *h = hier_of(hh);
+        if (!h || !out || nranks < 1) throw invalid_argument("sb_dist_create_local_p2p: bad argument");
+        sb_device_opts o{0, 1, -1, 0};
+        if (opts) o = *opts;
+        d = new sb_dist_s;
+        d->nranks = nranks;
+        d->local = true;
+        d->p2p = true;
+        d->R.resize(static_cast<size_t>(nranks));
+        for (int r = 0; r < nranks; ++r) build_rank(d, d->R[static_cast<size_t>(r)], *h, r, gather_rows, o);
+        for (auto &r : d->R) p2p_register(d, r);
+        std::vector<const unsigned long long *> ep;
+        std::vector<const double *> sl;
+        for (auto &q : d->R) {
+            ep.push_back(q.epoch);
+            sl.push_back(q.pslots);
+        }
+        for (auto &r : d->R) {
+            p2p_plans(r, [&](int q) -> const Partition & { return d->R[static_cast<size_t>(q)].P; });
+            p2p_tables(r, ep, sl);
+            r.peer_own.assign(r.exported_own.size(), std::vector<const double *>(static_cast<size_t>(nranks)));
+            for (size_t id = 0; id < r.exported_own.size(); ++id)
+                for (int q = 0; q < nranks; ++q)
+                    r.peer_own[id][static_cast<size_t>(q)] = d->R[static_cast<size_t>(q)].exported_own[id];
+        }
+        d->connected = true;
+        *out = d;
+    });
+    if (rc != SB_OK && d) sb_dist_destroy(d);
+    return rc;
+}
+
+// One rank per process over peer memory: create, export the IPC handles of the
+// buffers peers read (sb_dist_p2p_export), exchange the blobs out of band (every
+// rank needs every rank's), then sb_dist_p2p_connect with all of them in rank order.
+int sb_dist_create_p2p(sb_hier hh, int rank, int nranks, int64_t gather_rows, const sb_device_opts *opts,
+                       sb_dist *out) {
+    sb_dist d = nullptr;
+    const int rc = guard([&] {
+        Hier *h = hier_of(hh);
+        if (!h || !out || nranks < 1 || rank < 0 || rank >= nranks)
+            throw invalid_argument("sb_dist_create_p2p: bad argument");
+        sb_device_opts o{0, 1, -1, 0};
+        if (opts) o = *opts;
+        d = new sb_dist_s;
+        d->nranks = nranks;
+        d->local = false;
+        d->p2p = true;
+        d->R.resize(1);
+        RankDev &R = d->R[0];
+        build_rank(d, R, *h, rank, gather_rows, o);
+        p2p_register(d, R);
+        std::map<int, Partition> peers;  // the partitions of the ranks this rank receives from
+        p2p_plans(R, [&](int q) -> const Partition & {
+            if (q == rank) return R.P;
+            auto it = peers.find(q);
+            if (it == peers.end()) it = peers.emplace(q, build_partition(*h, q, nranks, gather_rows)).first;
+            return it->second;
+        });
+        *out = d;
+    });
+    if (rc != SB_OK && d) sb_dist_destroy(d);
+    return rc;
+}
+
+// blob: int32 count, then per exported buffer (ids in order, then the epoch):
+// int64 own-row-0 offset + cudaIpcMemHandle_t
+int sb_dist_p2p_export(sb_dist d, unsigned char *buf, int64_t cap, int64_t *len) {
+    return guard([&] {
+        if (!d || !d->p2p || d->local || !len) throw invalid_argument("sb_dist_p2p_export: not a P2P rank");
+        RankDev &R = d->R[0];
+        CK(cudaSetDevice(R.c->device));
+        const int n = static_cast<int>(R.exported.size()) + 1;
+        const int64_t need = 4 + static_cast<int64_t>(n) * (8 + static_cast<int64_t>(sizeof(cudaIpcMemHandle_t)));
+        *len = need;
+        if (!buf) return;
+        if (cap < need) throw invalid_argument("sb_dist_p2p_export: buffer too small");
+        std::memcpy(buf, &n, 4);
+        unsigned char *p = buf + 4;
+        for (int i = 0; i < n; ++i) {
+            void *base = i + 1 < n ? R.exported[static_cast<size_t>(i)].first : static_cast<void *>(R.epoch);
+            const int64_t off = i + 1 < n ? R.exported[static_cast<size_t>(i)].second : 0;
+            cudaIpcMemHandle_t hnd;
+            CK(cudaIpcGetMemHandle(&hnd, base));
+            std::memcpy(p, &off, 8);
+            std::memcpy(p + 8, &hnd, sizeof(hnd));
+            p += 8 + sizeof(hnd);
+        }
+    });
+}
+
+int sb_dist_p2p_connect(sb_dist d, const unsigned char *blobs, int64_t len_each) {
+    return guard([&] {
+        if (!d || !d->p2p || d->local || !blobs) throw invalid_argument("sb_dist_p2p_connect: not a P2P rank");
+        RankDev &R = d->R[0];
+        CK(cudaSetDevice(R.c->device));
+        const size_t nid = R.exported.size();
+        R.peer_own.assign(nid, std::vector<const double *>(static_cast<size_t>(d->nranks)));
+        std::vector<const unsigned long long *> ep(static_cast<size_t>(d->nranks));
+        std::vector<const double *> sl(static_cast<size_t>(d->nranks));
+        const int slot_id = R.buf_id.at(R.pslots);
+        for (int q = 0; q < d->nranks; ++q) {
+            if (q == R.rank) {
+                for (size_t id = 0; id < nid; ++id) R.peer_own[id][static_cast<size_t>(q)] = R.exported_own[id];
+                ep[static_cast<size_t>(q)] = R.epoch;
+                sl[static_cast<size_t>(q)] = R.pslots;
+                continue;
+            }
+            const unsigned char *p = blobs + static_cast<int64_t>(q) * len_each;
+            int n = 0;
+            std::memcpy(&n, p, 4);
+            if (n != static_cast<int>(nid) + 1) throw invalid_argument("sb_dist_p2p_connect: blob of another layout");
+            p += 4;
+            for (int i = 0; i < n; ++i) {
+                int64_t off = 0;
+                cudaIpcMemHandle_t hnd;
+                std::memcpy(&off, p, 8);
+                std::memcpy(&hnd, p + 8, sizeof(hnd));
+                p += 8 + sizeof(hnd);
+                void *mp = nullptr;
+                CK(cudaIpcOpenMemHandle(&mp, hnd, cudaIpcMemLazyEnablePeerAccess));
+                R.opened.push_back(mp);
+                const char *own = static_cast<const char *>(mp) + off;
+                if (i + 1 < n) R.peer_own[static_cast<size_t>(i)][static_cast<size_t>(q)] = reinterpret_cast<const double *>(own);
+                else ep[static_cast<size_t>(q)] = reinterpret_cast<const unsigned long long *>(own);
+            }
+            sl[static_cast<size_t>(q)] = R.peer_own[static_cast<size_t>(slot_id)][static_cast<size_t>(q)];
+        }
+        p2p_tables(R, ep, sl);
+        d->connected = true;
+    });
+}
+
 void sb_dist_destroy(sb_dist d) {
     if (!d) return;
+    for (auto &r : d->R)
+        for (void *p : r.opened) cudaIpcCloseMemHandle(p);
     for (auto &kv : d->cache) {
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
         if (kv.second.g) cudaGraphDestroy(kv.second.g);

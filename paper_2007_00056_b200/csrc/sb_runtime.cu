@@ -15,6 +15,7 @@
 //   amg_solve       cycle.hpp:91-130     -> build_amg_graph
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>

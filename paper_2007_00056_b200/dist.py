@@ -85,14 +85,22 @@ class DistSolver:
     this rank's rows [lo, hi)."""
 
     def __init__(self, h: Hierarchy, nranks: int, gather_rows: int = 65536, *, local: bool = True,
-                 rank: int = 0, nccl_id: bytes = None, device: int = 0, graphs: bool = True):
-        """graphs (NCCL mode): the whole solve captured as one CUDA graph with the
-        NCCL calls inside (False: eager launches, host-evaluated conditions)."""
+                 rank: int = 0, nccl_id: bytes = None, device: int = 0, graphs: bool = True,
+                 transport: str = "nccl"):
+        """graphs (one rank per process): the whole solve captured as one CUDA graph
+        with the exchanges inside (False: eager launches, host-evaluated conditions).
+        transport: "nccl", or "p2p" (peer memory: gathers out of the peers' buffers,
+        epoch flags; one rank per process needs p2p_export / p2p_connect)."""
         L = _lib.lib()
         d = C.c_void_p()
         opts = _lib.sb_device_opts(device, 1 if graphs else 0, -1, 0)
-        if local:
+        self.transport = transport
+        if local and transport == "p2p":
+            check(L.sb_dist_create_local_p2p(h._h, int(nranks), int(gather_rows), C.byref(opts), C.byref(d)))
+        elif local:
             check(L.sb_dist_create_local(h._h, int(nranks), int(gather_rows), C.byref(opts), C.byref(d)))
+        elif transport == "p2p":
+            check(L.sb_dist_create_p2p(h._h, int(rank), int(nranks), int(gather_rows), C.byref(opts), C.byref(d)))
         else:
             check(L.sb_dist_create(h._h, int(rank), int(nranks), nccl_id, int(gather_rows), C.byref(opts),
                                    C.byref(d)))
@@ -140,6 +148,22 @@ class DistSolver:
 
     def pbicgstab(self, b, p: CycleParams, tol, max_iters, x_out=None) -> SolveResult:
         return self._solve(_lib.lib().sb_dist_pbicgstab, b, p, tol, max_iters, x_out)
+
+    def p2p_export(self) -> bytes:
+        """This rank's IPC handle blob (every rank needs every rank's, in rank order)."""
+        L = _lib.lib()
+        n = C.c_int64()
+        check(L.sb_dist_p2p_export(self._d, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(L.sb_dist_p2p_export(self._d, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def p2p_connect(self, blobs) -> None:
+        """blobs: every rank's p2p_export() in rank order (equal lengths)."""
+        each = len(blobs[0])
+        if any(len(b) != each for b in blobs):
+            raise ValueError("p2p_connect: blobs of different lengths")
+        check(_lib.lib().sb_dist_p2p_connect(self._d, b"".join(blobs), each))
 
     def last_solve_ms(self) -> float:
         return float(_lib.lib().sb_dist_last_solve_ms(self._d))

@@ -99,3 +99,94 @@ def test_dist_nccl_one_rank_graph(sp, solver):
     single = getattr(sp, solver)(A, b, sp.make_amg_preconditioner(h, _cp(sp)), tol, 200)
     assert abs(single.report.iterations - rg.report.iterations) <= 1
     assert rel(rg.x, single.x) < 1e-9
+
+
+# ---- peer-memory (P2P) transport -----------------------------------------------
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+@pytest.mark.parametrize("mk,gather", [(lambda sp: sp.poisson3d(32), 4096), (lambda sp: sp.poisson2d(96, 70), 1000),
+                                       (lambda sp: sp.convdiff3d(20, 18, 17, 1.0, 100.0, 1.0, 1.0), 2000)])
+def test_dist_p2p_vcycle_bitexact(sp, nranks, mk, gather):
+    """In-process ranks over the peer-memory transport (gathers out of the peers'
+    buffers, epoch flags): the partitioned V-cycle is the single-GPU one bit for bit."""
+    from paper_2007_00056_b200.dist import DistSolver
+    A = mk(sp)
+    h = sp.Hierarchy(A, sp.SolverConfig(max_levels=40))
+    ds = DistSolver(h, nranks, gather, transport="p2p")
+    f = sp.rhs_random(A.nrows(), 42)
+    assert np.array_equal(ds.vcycle(f, _cp(sp)), sp.vcycle(h, 0, f, np.zeros(A.nrows()), _cp(sp)))
+    assert np.array_equal(ds.vcycle(f, _cp(sp)), ds.vcycle(f, _cp(sp)))  # repeatable (epochs keep counting)
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+@pytest.mark.parametrize("solver", ["pcg", "pbicgstab"])
+def test_dist_p2p_solve_matches_nccl_free_local(sp, nranks, solver):
+    """P2P and the event-ordered in-process transport sum the partials in the same
+    rank order: the solves agree bit for bit; both match the single-GPU solve."""
+    from paper_2007_00056_b200.dist import DistSolver
+    A = sp.poisson3d(32) if solver == "pcg" else sp.convdiff3d(20, 18, 17, 1.0, 100.0, 1.0, 1.0)
+    h = sp.Hierarchy(A, sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40))
+    b = sp.rhs_random(A.nrows(), 9)
+    tol = 1e-8 * np.linalg.norm(b)
+    rp = getattr(DistSolver(h, nranks, 2048, transport="p2p"), solver)(b, _cp(sp), tol, 200)
+    rl = getattr(DistSolver(h, nranks, 2048), solver)(b, _cp(sp), tol, 200)
+    assert rp.report.converged() and rp.report.iterations == rl.report.iterations
+    assert np.array_equal(rp.x.view(np.uint64), rl.x.view(np.uint64))
+    single = getattr(sp, solver)(A, b, sp.make_amg_preconditioner(h, _cp(sp)), tol, 200)
+    assert abs(single.report.iterations - rp.report.iterations) <= 1
+    assert rel(rp.x, single.x) < 1e-9
+
+
+_P2P_WORKER = r"""
+import os, sys, time, json, numpy as np
+sys.path.insert(0, os.environ["SB_ROOT"])
+from paper_2007_00056_b200 import sparsh as sp
+from paper_2007_00056_b200.dist import DistSolver
+rank, nranks, tmp, graphs = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], sys.argv[4] == "1"
+A = sp.poisson3d(28)
+h = sp.Hierarchy(A, sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40))
+ds = DistSolver(h, nranks, 2048, local=False, rank=rank, transport="p2p", graphs=graphs)
+open(os.path.join(tmp, f"blob{rank}.tmp"), "wb").write(ds.p2p_export())
+os.replace(os.path.join(tmp, f"blob{rank}.tmp"), os.path.join(tmp, f"blob{rank}"))
+while not all(os.path.exists(os.path.join(tmp, f"blob{q}")) for q in range(nranks)):
+    time.sleep(0.05)
+ds.p2p_connect([open(os.path.join(tmp, f"blob{q}"), "rb").read() for q in range(nranks)])
+b = sp.rhs_ones(A.nrows())[ds.lo:ds.hi]
+cp = sp.CycleParams(6, 6, sp.SmootherKind.weighted_jacobi())
+tol = 1e-8 * np.sqrt(A.nrows())
+r1 = ds.pcg(b, cp, tol, 100)
+r2 = ds.pcg(b, cp, tol, 100)  # graph replay / second eager run
+assert np.array_equal(r1.x, r2.x)
+np.save(os.path.join(tmp, f"x{rank}.npy"), r1.x)
+json.dump({"it": r1.report.iterations, "lo": ds.lo, "hi": ds.hi}, open(os.path.join(tmp, f"r{rank}.json"), "w"))
+"""
+
+
+@pytest.mark.parametrize("graphs", ["1", "0"])
+def test_dist_p2p_two_processes_ipc(sp, tmp_path, graphs):
+    """Two PROCESSES (one rank each) on the same GPU over CUDA IPC: each exports
+    its buffers, connects to the other's, and solves (as one captured graph, or
+    eagerly); the joined solution equals the in-process P2P solve bit for bit."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    from paper_2007_00056_b200.dist import DistSolver
+    script = tmp_path / "w.py"
+    script.write_text(_P2P_WORKER)
+    env = dict(os.environ, SB_ROOT=ROOT)
+    procs = [subprocess.Popen([sys.executable, str(script), str(r), "2", str(tmp_path), graphs], env=env,
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=600) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-3000:]
+    A = sp.poisson3d(28)
+    h = sp.Hierarchy(A, sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40))
+    ref = DistSolver(h, 2, 2048, transport="p2p").pcg(sp.rhs_ones(A.nrows()), _cp(sp), 1e-8 * np.sqrt(A.nrows()), 100)
+    x = np.zeros(A.nrows())
+    for r in range(2):
+        m = json.load(open(tmp_path / f"r{r}.json"))
+        assert m["it"] == ref.report.iterations
+        x[m["lo"]:m["hi"]] = np.load(tmp_path / f"x{r}.npy")
+    assert np.array_equal(x.view(np.uint64), ref.x.view(np.uint64))
