@@ -1220,6 +1220,22 @@ __global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const doub
         xout[i] = __dadd_rn(xin[i], __dadd_rn(0.0, xc[agg[i]]));
 }
 
+// the same, two rows per thread with 16-byte loads / stores (n even, 16-byte
+// aligned vectors): the prolongation of the levels whose sweeps run as row
+// pairs (k_crosspair), kept out of the first post-sweep there (emit_vcycle)
+__global__ void k_prolong2(int64_t npairs, const int2 *__restrict__ agg, const double2 *xin,
+                           const double *__restrict__ xc, double2 *xout) {
+    pdl_wait();
+    pdl_trigger_single(npairs);
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < npairs;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int2 a = agg[q];
+        const double2 v = xin[q];
+        const double c0 = xc[a.x], c1 = a.y == a.x ? c0 : xc[a.y];
+        xout[q] = make_double2(__dadd_rn(v.x, __dadd_rn(0.0, c0)), __dadd_rn(v.y, __dadd_rn(0.0, c1)));
+    }
+}
+
 // Coarsest-level solve z = A_c^{-1} f with the precomputed inverse (one warp
 // per row, fixed shuffle tree).
 __global__ void k_coarse_gemv(int n, const double *__restrict__ inv, const double *__restrict__ f,
@@ -1997,7 +2013,16 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
                  static_cast<const double *>(lc.diag), x0, cp.omega);
     }
     emit_vcycle(c, s, cp, k + 1, lc.f, lc.x, true, child_x0);
-    if (cp.post >= 1 && cur != post_first) {
+    // On row-pair (7/5-point cross) levels the prolongation runs as its own
+    // vector pass and every post-sweep as k_crosspair: measured faster at 256^3
+    // than k_rowpat's fused prolongation + sweep; elsewhere the
+    // prolongation rides on the first post-sweep's gathers.
+    static const bool split_env = [] {
+        const char *e = std::getenv("SB_PROLONG_SPLIT");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const bool split = split_env && l.pat && l.box_pair == 2;
+    if (cp.post >= 1 && cur != post_first && !split) {
         // x' = cur + P x_c folded into the first post-sweep's gathers
         launch_csr<M_JACOBI_PROLONG, 0>(c, l, s, cur, f, post_first, cp.omega, nullptr, Red{},
                                         Aux{l.diag, l.agg, lc.x});
@@ -2008,12 +2033,20 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
                     k == 0 ? c->final_red : nullptr, &c->final_red_used);
     } else {
         double *pout = (sweep_launches(l, cp.post, k == 0) % 2 == 0) ? X : T;
-        launch_k(c, k_prolong, dim3(vec_grid(l.n)), dim3(kVecThreads), 0, s, l.n,
-                 static_cast<const int32_t *>(l.agg), static_cast<const double *>(cur),
-                 static_cast<const double *>(lc.x), pout);
+        auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        if (l.n % 2 == 0 && a16(cur) && a16(pout) && a16(l.agg))
+            launch_k(c, k_prolong2, dim3(vec_grid(l.n / 2)), dim3(kVecThreads), 0, s, l.n / 2,
+                     reinterpret_cast<const int2 *>(l.agg), reinterpret_cast<const double2 *>(cur),
+                     static_cast<const double *>(lc.x), reinterpret_cast<double2 *>(pout));
+        else
+            launch_k(c, k_prolong, dim3(vec_grid(l.n)), dim3(kVecThreads), 0, s, l.n,
+                     static_cast<const int32_t *>(l.agg), static_cast<const double *>(cur),
+                     static_cast<const double *>(lc.x), pout);
         cur = pout;
         other = (pout == X) ? T : X;
-        emit_sweeps(c, l, s, sweep_groups(l, cp.post, k == 0), cur, other, f, cp.omega);
+        // last kernel of the cycle at level 0: a single sweep + (z, r)
+        emit_sweeps(c, l, s, sweep_groups(l, cp.post, k == 0), cur, other, f, cp.omega,
+                    k == 0 ? c->final_red : nullptr, &c->final_red_used);
     }
 }
 

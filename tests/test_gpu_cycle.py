@@ -119,3 +119,29 @@ def test_vcycle_27point_varied_bitexact(sp, port, tail_rows, monkeypatch):
         f = sp.rhs_random(A.nrows(), 5)
         assert np.array_equal(sp.vcycle(h, 0, f, np.zeros(A.nrows()), _cp(sp)), o.vcycle(f, np.zeros(A.nrows())))
         assert np.array_equal(sp.make_amg_preconditioner(h, _cp(sp)).apply(f), o.vcycle(f, np.zeros(A.nrows())))
+
+
+@pytest.mark.parametrize("which", ["p3", "p2", "cd"])
+def test_prolong_split_bitwise(sp, which):
+    """On row-pair levels the prolongation runs as its own vector pass
+    (k_prolong2) followed by k_crosspair sweeps; the V-cycle and the solve are
+    bit for bit the fused prolongation + first post-sweep (SB_PROLONG_SPLIT=0)."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from paper_2007_00056_b200 import sparsh as sp; "
+            "A = %s; cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40); "
+            "h = sp.Hierarchy(A, cfg); cp = sp.CycleParams.from_config(cfg); b = sp.rhs_random(A.nrows(), 5); "
+            "v = sp.vcycle(h, 0, b, np.zeros(A.nrows()), cp); "
+            "r = sp.pcg(A, b, sp.make_amg_preconditioner(h, cp), 1e-8 * np.linalg.norm(b), 200); "
+            "sys.stdout.write(v.tobytes().hex() + ' ' + r.x.tobytes().hex())")
+    src = {"p3": "sp.poisson3d(32)", "p2": "sp.poisson2d(128, 96)",
+           "cd": "sp.convdiff3d(20, 18, 16, 1.0, 100.0, 1.0, 1.0)"}[which]
+    outs = []
+    for on in ("1", "0"):
+        import os
+        out = subprocess.run([sys.executable, "-c", code % (ROOT, src)], env=dict(os.environ, SB_PROLONG_SPLIT=on),
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        outs.append(out.stdout)
+    assert outs[0] and outs[0] == outs[1]
