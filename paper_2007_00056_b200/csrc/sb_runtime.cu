@@ -1352,12 +1352,42 @@ __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restri
     const DevState *st = red.st;
     if (!st->done) {
         const double alpha = st->alpha, nalpha = -st->alpha;
-        GRID_LOOP(i, n) {
-            x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
-            const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
-            r[i] = ri;
-            a[0] += ri * ri;
-            z0.put(i, ri);
+        auto a16 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+        if (a16(x) && a16(r) && a16(p) && a16(Ap) && (!z0.x0 || (a16(z0.x0) && a16(z0.diag)))) {
+            // two rows per step with 16-byte accesses (the same per-row arithmetic)
+            const int64_t h = n / 2;
+            GRID_LOOP(q, h) {
+                const double2 xv = reinterpret_cast<const double2 *>(x)[q], pv = reinterpret_cast<const double2 *>(p)[q];
+                const double2 rv = reinterpret_cast<const double2 *>(r)[q], av = reinterpret_cast<const double2 *>(Ap)[q];
+                reinterpret_cast<double2 *>(x)[q] =
+                    make_double2(__dadd_rn(xv.x, __dmul_rn(alpha, pv.x)), __dadd_rn(xv.y, __dmul_rn(alpha, pv.y)));
+                const double r0 = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x)), r1 = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
+                reinterpret_cast<double2 *>(r)[q] = make_double2(r0, r1);
+                a[0] += r0 * r0;
+                a[0] += r1 * r1;
+                if (z0.x0) {
+                    const double2 dv = reinterpret_cast<const double2 *>(z0.diag)[q];
+                    reinterpret_cast<double2 *>(z0.x0)[q] =
+                        make_double2(__dadd_rn(0.0, __ddiv_rn(__dmul_rn(z0.omega, r0), dv.x)),
+                                     __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z0.omega, r1), dv.y)));
+                }
+            }
+            if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+                const int64_t i = n - 1;
+                x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+                const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
+                r[i] = ri;
+                a[0] += ri * ri;
+                z0.put(i, ri);
+            }
+        } else {
+            GRID_LOOP(i, n) {
+                x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+                const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
+                r[i] = ri;
+                a[0] += ri * ri;
+                z0.put(i, ri);
+            }
         }
     }
     finish_reduction<1>(red, a);
