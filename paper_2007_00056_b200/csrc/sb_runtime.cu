@@ -1316,33 +1316,81 @@ __global__ void k_init(int64_t n, const double *__restrict__ b, double *__restri
     finish_reduction<1>(red, a);
 }
 
+// Row loops of the Krylov vector kernels: two rows per step with 16-byte
+// accesses when every vector is 16-byte aligned (warp-uniform test), else one.
+// The per-row arithmetic is identical; only a thread's accumulation order of
+// its reduction partial changes with the width (deterministic per launch).
+template <int V> struct DV {
+    double v[V];
+};
+template <int V> __device__ __forceinline__ DV<V> ldv(const double *p, int64_t i) {
+    DV<V> o;
+    if constexpr (V == 2) {
+        const double2 t = *reinterpret_cast<const double2 *>(p + i);
+        o.v[0] = t.x;
+        o.v[1] = t.y;
+    } else {
+        o.v[0] = p[i];
+    }
+    return o;
+}
+template <int V> __device__ __forceinline__ void stv(double *p, int64_t i, const DV<V> &x) {
+    if constexpr (V == 2) *reinterpret_cast<double2 *>(p + i) = make_double2(x.v[0], x.v[1]);
+    else p[i] = x.v[0];
+}
+__device__ __forceinline__ bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+template <typename... P> __device__ __forceinline__ bool all16(const P *...p) { return (al16(p) && ...); }
+template <typename Body> __device__ __forceinline__ void grid_rows(int64_t n, bool vec, Body &&body) {
+    if (vec) {
+        const int64_t h = n / 2;
+        GRID_LOOP(q, h) body(std::integral_constant<int, 2>{}, 2 * q);
+        if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) body(std::integral_constant<int, 1>{}, n - 1);
+    } else {
+        GRID_LOOP(i, n) body(std::integral_constant<int, 1>{}, i);
+    }
+}
+__device__ __forceinline__ bool x0_ok(const X0 &z0) { return !z0.x0 || (al16(z0.x0) && al16(z0.diag)); }
+template <int V> __device__ __forceinline__ void x0_put(const X0 &z0, int64_t i, const DV<V> &v) {
+    if (!z0.x0) return;
+    const DV<V> d = ldv<V>(z0.diag, i);
+    DV<V> o;
+#pragma unroll
+    for (int k = 0; k < V; ++k) o.v[k] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z0.omega, v.v[k]), d.v[k]));
+    stv<V>(z0.x0, i, o);
+}
+
 // dst = src; sum src*w  (PCG: p = z, rz = (r, z); BiCGStab: rbar = p = r, rho = (r, rbar))
 __global__ void k_copy_dot(int64_t n, const double *__restrict__ src, double *__restrict__ dst,
                            double *__restrict__ dst2, const double *__restrict__ w, Red red, X0 z0) {
     pdl_wait();  // launched with PDL on the partitioned path
     pdl_trigger_single(n);
     double a[1] = {0.0};
-    GRID_LOOP(i, n) {
-        const double s = src[i];
-        dst[i] = s;
-        if (dst2) dst2[i] = s;
-        a[0] += s * w[i];
-        z0.put(i, s);
-    }
+    grid_rows(n, all16(src, dst, w) && (!dst2 || al16(dst2)) && x0_ok(z0), [&](auto vc, int64_t i) {
+        constexpr int V = decltype(vc)::value;
+        const DV<V> sv = ldv<V>(src, i), wv = ldv<V>(w, i);
+        stv<V>(dst, i, sv);
+        if (dst2) stv<V>(dst2, i, sv);
+#pragma unroll
+        for (int k = 0; k < V; ++k) a[0] += sv.v[k] * wv.v[k];
+        x0_put<V>(z0, i, sv);
+    });
     finish_reduction<1>(red, a);
 }
-
 __global__ void k_dot(int64_t n, const double *__restrict__ u, const double *__restrict__ v,
                       const int *skip, Red red) {
     pdl_wait();  // launched with PDL on the partitioned path
     pdl_trigger_single(n);
     double a[1] = {0.0};
     if (!(skip && *skip)) {
-        GRID_LOOP(i, n) a[0] += u[i] * v[i];
+        grid_rows(n, all16(u, v), [&](auto vc, int64_t i) {
+            constexpr int V = decltype(vc)::value;
+            const DV<V> uv = ldv<V>(u, i), vv = ldv<V>(v, i);
+#pragma unroll
+            for (int k = 0; k < V; ++k) a[0] += uv.v[k] * vv.v[k];
+        });
     }
     finish_reduction<1>(red, a);
 }
-
 // PCG update (krylov.hpp:96-98): x += alpha p; r += (-alpha) Ap; ||r||^2 (+ x0 of z = M r)
 __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
                              const double *__restrict__ p, const double *__restrict__ Ap, Red red, X0 z0) {
@@ -1352,56 +1400,38 @@ __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restri
     const DevState *st = red.st;
     if (!st->done) {
         const double alpha = st->alpha, nalpha = -st->alpha;
-        auto a16 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-        if (a16(x) && a16(r) && a16(p) && a16(Ap) && (!z0.x0 || (a16(z0.x0) && a16(z0.diag)))) {
-            // two rows per step with 16-byte accesses (the same per-row arithmetic)
-            const int64_t h = n / 2;
-            GRID_LOOP(q, h) {
-                const double2 xv = reinterpret_cast<const double2 *>(x)[q], pv = reinterpret_cast<const double2 *>(p)[q];
-                const double2 rv = reinterpret_cast<const double2 *>(r)[q], av = reinterpret_cast<const double2 *>(Ap)[q];
-                reinterpret_cast<double2 *>(x)[q] =
-                    make_double2(__dadd_rn(xv.x, __dmul_rn(alpha, pv.x)), __dadd_rn(xv.y, __dmul_rn(alpha, pv.y)));
-                const double r0 = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x)), r1 = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
-                reinterpret_cast<double2 *>(r)[q] = make_double2(r0, r1);
-                a[0] += r0 * r0;
-                a[0] += r1 * r1;
-                if (z0.x0) {
-                    const double2 dv = reinterpret_cast<const double2 *>(z0.diag)[q];
-                    reinterpret_cast<double2 *>(z0.x0)[q] =
-                        make_double2(__dadd_rn(0.0, __ddiv_rn(__dmul_rn(z0.omega, r0), dv.x)),
-                                     __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z0.omega, r1), dv.y)));
-                }
+        grid_rows(n, all16(x, r, p, Ap) && x0_ok(z0), [&](auto vc, int64_t i) {
+            constexpr int V = decltype(vc)::value;
+            DV<V> xv = ldv<V>(x, i), rv = ldv<V>(r, i);
+            const DV<V> pv = ldv<V>(p, i), av = ldv<V>(Ap, i);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                xv.v[k] = __dadd_rn(xv.v[k], __dmul_rn(alpha, pv.v[k]));
+                rv.v[k] = __dadd_rn(rv.v[k], __dmul_rn(nalpha, av.v[k]));
+                a[0] += rv.v[k] * rv.v[k];
             }
-            if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-                const int64_t i = n - 1;
-                x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
-                const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
-                r[i] = ri;
-                a[0] += ri * ri;
-                z0.put(i, ri);
-            }
-        } else {
-            GRID_LOOP(i, n) {
-                x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
-                const double ri = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
-                r[i] = ri;
-                a[0] += ri * ri;
-                z0.put(i, ri);
-            }
-        }
+            stv<V>(x, i, xv);
+            stv<V>(r, i, rv);
+            x0_put<V>(z0, i, rv);
+        });
     }
     finish_reduction<1>(red, a);
 }
-
 // p = z + beta p (krylov.hpp:113)
 __global__ void k_xpay(int64_t n, const double *__restrict__ z, double *__restrict__ p,
                        const DevState *__restrict__ st) {
     pdl_wait();  // launched with PDL on the partitioned path
     pdl_trigger_single(n);
     const double beta = st->beta;
-    GRID_LOOP(i, n) p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+    grid_rows(n, all16(z, p), [&](auto vc, int64_t i) {
+        constexpr int V = decltype(vc)::value;
+        const DV<V> zv = ldv<V>(z, i);
+        DV<V> pv = ldv<V>(p, i);
+#pragma unroll
+        for (int k = 0; k < V; ++k) pv.v[k] = __dadd_rn(zv.v[k], __dmul_rn(beta, pv.v[k]));
+        stv<V>(p, i, pv);
+    });
 }
-
 // BiCGStab s = r + (-alpha) Ap~; ||s||^2 (krylov.hpp:164-166)
 __global__ void k_bi_s(int64_t n, const double *__restrict__ r, const double *__restrict__ Apt,
                        double *__restrict__ s, Red red, X0 z0) {
@@ -1411,16 +1441,21 @@ __global__ void k_bi_s(int64_t n, const double *__restrict__ r, const double *__
     const DevState *st = red.st;
     if (!st->done) {
         const double nalpha = -st->alpha;
-        GRID_LOOP(i, n) {
-            const double si = __dadd_rn(r[i], __dmul_rn(nalpha, Apt[i]));
-            s[i] = si;
-            a[0] += si * si;
-            z0.put(i, si);
-        }
+        grid_rows(n, all16(r, Apt, s) && x0_ok(z0), [&](auto vc, int64_t i) {
+            constexpr int V = decltype(vc)::value;
+            const DV<V> rv = ldv<V>(r, i), av = ldv<V>(Apt, i);
+            DV<V> sv;
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                sv.v[k] = __dadd_rn(rv.v[k], __dmul_rn(nalpha, av.v[k]));
+                a[0] += sv.v[k] * sv.v[k];
+            }
+            stv<V>(s, i, sv);
+            x0_put<V>(z0, i, sv);
+        });
     }
     finish_reduction<1>(red, a);
 }
-
 // Half-step exit: x += alpha p~ (krylov.hpp:168), only when EP_BI_SN fired.
 __global__ void k_bi_half(int64_t n, double *__restrict__ x, const double *__restrict__ pt,
                           const DevState *__restrict__ st) {
@@ -1428,9 +1463,15 @@ __global__ void k_bi_half(int64_t n, double *__restrict__ x, const double *__res
     pdl_trigger_single(n);
     if (!st->half) return;
     const double alpha = st->alpha;
-    GRID_LOOP(i, n) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pt[i]));
+    grid_rows(n, all16(x, pt), [&](auto vc, int64_t i) {
+        constexpr int V = decltype(vc)::value;
+        DV<V> xv = ldv<V>(x, i);
+        const DV<V> pv = ldv<V>(pt, i);
+#pragma unroll
+        for (int k = 0; k < V; ++k) xv.v[k] = __dadd_rn(xv.v[k], __dmul_rn(alpha, pv.v[k]));
+        stv<V>(x, i, xv);
+    });
 }
-
 // x += alpha p~; x += omega s~; r = s + (-omega) As~; ||r||^2, (r, rbar0)  (krylov.hpp:182-186, 201)
 __global__ void k_bi_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
                             const double *__restrict__ pt, const double *__restrict__ st_,
@@ -1442,18 +1483,25 @@ __global__ void k_bi_update(int64_t n, double *__restrict__ x, double *__restric
     const DevState *st = red.st;
     if (!st->done) {
         const double alpha = st->alpha, omega = st->omega, nomega = -st->omega;
-        GRID_LOOP(i, n) {
-            double xi = __dadd_rn(x[i], __dmul_rn(alpha, pt[i]));
-            x[i] = __dadd_rn(xi, __dmul_rn(omega, st_[i]));
-            const double ri = __dadd_rn(s[i], __dmul_rn(nomega, Ast[i]));
-            r[i] = ri;
-            a[0] += ri * ri;
-            a[1] += ri * rbar[i];
-        }
+        grid_rows(n, all16(x, r, pt, st_, s, Ast, rbar), [&](auto vc, int64_t i) {
+            constexpr int V = decltype(vc)::value;
+            DV<V> xv = ldv<V>(x, i), rv;
+            const DV<V> pv = ldv<V>(pt, i), tv = ldv<V>(st_, i), sv = ldv<V>(s, i), av = ldv<V>(Ast, i),
+                        bv = ldv<V>(rbar, i);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                const double xi = __dadd_rn(xv.v[k], __dmul_rn(alpha, pv.v[k]));
+                xv.v[k] = __dadd_rn(xi, __dmul_rn(omega, tv.v[k]));
+                rv.v[k] = __dadd_rn(sv.v[k], __dmul_rn(nomega, av.v[k]));
+                a[0] += rv.v[k] * rv.v[k];
+                a[1] += rv.v[k] * bv.v[k];
+            }
+            stv<V>(x, i, xv);
+            stv<V>(r, i, rv);
+        });
     }
     finish_reduction<2>(red, a);
 }
-
 // p = r + beta (p - omega Ap~)  (krylov.hpp:204-205)
 __global__ void k_bi_p(int64_t n, const double *__restrict__ r, double *__restrict__ p,
                        const double *__restrict__ Apt, const DevState *__restrict__ st, X0 z0) {
@@ -1461,13 +1509,18 @@ __global__ void k_bi_p(int64_t n, const double *__restrict__ r, double *__restri
     pdl_trigger_single(n);
     if (st->done) return;
     const double beta = st->beta, omega = st->omega;
-    GRID_LOOP(i, n) {
-        const double pi = __dadd_rn(r[i], __dmul_rn(beta, __dsub_rn(p[i], __dmul_rn(omega, Apt[i]))));
-        p[i] = pi;
-        z0.put(i, pi);
-    }
+    grid_rows(n, all16(r, p, Apt) && x0_ok(z0), [&](auto vc, int64_t i) {
+        constexpr int V = decltype(vc)::value;
+        const DV<V> rv = ldv<V>(r, i), av = ldv<V>(Apt, i);
+        DV<V> pv = ldv<V>(p, i);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            pv.v[k] = __dadd_rn(rv.v[k], __dmul_rn(beta, __dsub_rn(pv.v[k], __dmul_rn(omega, av.v[k]))));
+        }
+        stv<V>(p, i, pv);
+        x0_put<V>(z0, i, pv);
+    });
 }
-
 __global__ void k_fill(int64_t n, double *x, double v) {
     pdl_wait();  // launched with PDL on the partitioned path
     GRID_LOOP(i, n) x[i] = v;
