@@ -186,6 +186,7 @@ struct DistLevel {
     bool dist = false, next_rep = false;
     int64_t n_own = 0, n_ext = 0, nc_own = 0, c_lo = 0;
     int64_t wb = 0, wa = 0;  // x-like vectors: wb rows below own row 0, wa above (n_ext = n_own + wa)
+    int64_t q_ilo = 0, q_ihi = 0;  // interior row pairs: no column outside the own rows (swept while the halo flies)
     double *rg = nullptr, *xcg = nullptr;  // residual-partner / coarse-parent ghosts
     DevExch halo, rx, px;
     std::vector<int64_t> gather_lo;  // first replicated level: owned pieces per rank
@@ -198,6 +199,8 @@ struct RankDev {
     std::vector<DistLevel> D;
     cudaEvent_t ready = nullptr, done = nullptr;
     cudaStream_t s = nullptr;      // stream the solve is emitted on (the context stream, or a graph body's)
+    cudaStream_t s2 = nullptr;     // side stream: the halo exchange overlapping the interior sweep
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double **part_ptrs = nullptr;  // in-process: device array of every rank's st->part
     // P2P transport
     unsigned long long *epoch = nullptr;  // exported
@@ -273,6 +276,30 @@ static void upload_dist_level(sb_ctx c, const PartLevel &pl, DevLevel &D, DistLe
     D.f = dalloc<double>(c, DL.n_own);
     DL.rg = dalloc<double>(c, std::max<int64_t>(static_cast<int64_t>(pl.rghost_glob.size()), 1));
     DL.xcg = dalloc<double>(c, std::max<int64_t>(static_cast<int64_t>(pl.xcghost_glob.size()), 1));
+    {  // interior rows: a contiguous block whose columns are all own rows and
+       // that no peer reads (P2P gathers read the sender's vector while the
+       // interior of the next sweep is written; row pairs)
+        const HostCsr &A = pl.A;
+        const int64_t n = A.n;
+        std::vector<char> sent(static_cast<size_t>(n), 0);
+        for (int32_t i : pl.halo.send_idx)
+            if (i >= 0 && i < n) sent[static_cast<size_t>(i)] = 1;
+        auto ghosty = [&](int64_t i) {
+            if (sent[static_cast<size_t>(i)]) return true;
+            for (int64_t e = A.rp[i]; e < A.rp[i + 1]; ++e)
+                if (A.ci[e] < 0 || A.ci[e] >= n) return true;
+            return false;
+        };
+        int64_t lo = 0, hi = n;
+        while (lo < n && ghosty(lo)) ++lo;
+        while (hi > lo && ghosty(hi - 1)) --hi;
+        bool ok = hi - lo >= 1024;
+        for (int64_t i = lo; ok && i < hi; ++i) ok = !ghosty(i);
+        lo = (lo + 1) / 2;  // pairs fully inside [lo, hi)
+        hi = hi / 2;
+        DL.q_ilo = ok ? lo : 0;
+        DL.q_ihi = ok ? hi : 0;
+    }
     DL.halo = upload_exch(c, pl.halo);
     DL.rx = upload_exch(c, pl.rx);
     DL.px = upload_exch(c, pl.px);
@@ -291,24 +318,30 @@ static void barrier_local(sb_dist d) {
 // P2P: publish this rank's epoch, then wait until every rank reached it (the
 // producers' writes are visible; no rank can overwrite a buffer a peer still
 // reads, because every rank publishes only after its previous gathers)
-static void p2p_sync(sb_dist d) {
+static void p2p_publish(sb_dist d) {
     for (auto &r : d->R) launch_k(r.c, k_p2p_publish, dim3(1), dim3(1), 0, r.s, r.epoch);
+}
+static void p2p_wait(sb_dist d) {
     for (auto &r : d->R)
         launch_k(r.c, k_p2p_wait, dim3(1), dim3(32), 0, r.s, static_cast<const unsigned long long *>(r.epoch),
                  static_cast<const unsigned long long *const *>(r.peer_epochs), d->nranks);
+}
+static void p2p_sync(sb_dist d) {
+    p2p_publish(d);
+    p2p_wait(d);
 }
 
 // Fill the ghost entries of every rank r from own(q) of its peers q, per the
 // level-k plan `which`: chunk j of r lands at dst(r) + recv_dst[j] (halo: dst
 // is the own-rows pointer of the x vector; rx / px: the packed ghost buffers).
 static void exchange(sb_dist d, int k, int which, const std::function<const double *(RankDev &)> &own,
-                     const std::function<double *(RankDev &)> &ghost) {
+                     const std::function<double *(RankDev &)> &ghost, bool skip_sync = false) {
     auto plan = [&](RankDev &r) -> DevExch & {
         DistLevel &L = r.D[static_cast<size_t>(k)];
         return which == 0 ? L.halo : which == 1 ? L.rx : L.px;
     };
     if (d->p2p) {
-        p2p_sync(d);
+        if (!skip_sync) p2p_sync(d);
         for (auto &r : d->R) {
             DevExch &e = plan(r);
             if (e.recv_peers.empty()) continue;
@@ -454,6 +487,73 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
         for (size_t i = 0; i < N; ++i) launch_jacobi(d->R[i].c, lev(i), d->R[i].s, cur[i], f[i], oth[i], cp.omega);
         std::swap(cur, oth);
     };
+    // halo exchange + sweep. A rank whose level has an interior block of row
+    // pairs (no ghost column) sweeps it on its stream while the exchange runs
+    // on the side stream, then sweeps the edge rows once the ghosts are in.
+    static const bool overlap_env = [] {
+        const char *e = std::getenv("SB_DIST_OVERLAP");
+        return !(e && std::atoi(e) == 0);
+    }();
+    auto can_overlap = [&](size_t i) {
+        return overlap_env && dl(i).q_ihi > dl(i).q_ilo && cross_range_ok(lev(i), cur[i], f[i], oth[i]);
+    };
+    auto halo_sweep = [&]() {
+        bool any = false;
+        for (size_t i = 0; i < N; ++i) any = any || can_overlap(i);
+        if (!any) {
+            halo(cur);
+            sweep();
+            return;
+        }
+        if (d->p2p) {
+            // peer memory: publish, sweep the interior (the peers catch up
+            // meanwhile), then wait, gather the ghosts, sweep the edge rows
+            p2p_publish(d);
+            for (size_t i = 0; i < N; ++i)
+                if (can_overlap(i))
+                    launch_jacobi_range(d->R[i].c, lev(i), d->R[i].s, cur[i], f[i], oth[i], cp.omega, dl(i).q_ilo,
+                                        dl(i).q_ihi);
+            p2p_wait(d);
+            std::vector<double *> vv = cur;
+            exchange(d, k, 0, [&](RankDev &r) -> const double * { return vv[static_cast<size_t>(&r - d->R.data())]; },
+                     [&](RankDev &r) { return vv[static_cast<size_t>(&r - d->R.data())]; }, true);
+        } else if (tl_eager) {
+            // (eager launches only) the exchange on the side stream while the
+            // interior is swept on the rank's stream
+            std::vector<cudaStream_t> main(N);
+            for (size_t i = 0; i < N; ++i) {
+                RankDev &r = d->R[i];
+                main[i] = r.s;
+                CK(cudaEventRecord(r.ev_fork, r.s));
+                CK(cudaStreamWaitEvent(r.s2, r.ev_fork, 0));
+                if (can_overlap(i))
+                    launch_jacobi_range(r.c, lev(i), r.s, cur[i], f[i], oth[i], cp.omega, dl(i).q_ilo, dl(i).q_ihi);
+                r.s = r.s2;
+            }
+            halo(cur);  // on the side streams
+            for (size_t i = 0; i < N; ++i) {
+                RankDev &r = d->R[i];
+                CK(cudaEventRecord(r.ev_join, r.s2));
+                r.s = main[i];
+                CK(cudaStreamWaitEvent(r.s, r.ev_join, 0));
+            }
+        } else {
+            halo(cur);
+            sweep();
+            return;
+        }
+        for (size_t i = 0; i < N; ++i) {
+            RankDev &r = d->R[i];
+            if (can_overlap(i)) {
+                const int64_t np = lev(i).n / 2;
+                launch_jacobi_range(r.c, lev(i), r.s, cur[i], f[i], oth[i], cp.omega, 0, dl(i).q_ilo);
+                launch_jacobi_range(r.c, lev(i), r.s, cur[i], f[i], oth[i], cp.omega, dl(i).q_ihi, np);
+            } else {
+                launch_jacobi(r.c, lev(i), r.s, cur[i], f[i], oth[i], cp.omega);
+            }
+        }
+        std::swap(cur, oth);
+    };
     for (size_t i = 0; i < N; ++i) {
         cur[i] = X[i];
         oth[i] = lev(i).t;
@@ -464,19 +564,13 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
                 launch_k(d->R[i].c, k_jacobi_zero, dim3(vec_grid(dl(i).n_own)), dim3(kVecThreads), 0,
                          d->R[i].s, dl(i).n_own, f[i], static_cast<const double *>(lev(i).diag), cur[i],
                          cp.omega);
-            for (int s = 1; s < cp.pre; ++s) {
-                halo(cur);
-                sweep();
-            }
+            for (int s = 1; s < cp.pre; ++s) halo_sweep();
         } else {
             for (size_t i = 0; i < N; ++i)
                 CK(cudaMemsetAsync(cur[i], 0, sizeof(double) * static_cast<size_t>(dl(i).n_own), d->R[i].s));
         }
     } else {
-        for (int s = 0; s < cp.pre; ++s) {
-            halo(cur);
-            sweep();
-        }
+        for (int s = 0; s < cp.pre; ++s) halo_sweep();
     }
     // residual, partner residuals, restriction. A rank whose aggregates are all
     // local (no straddling pair: no rx plan; every BASELINE grid at plane-aligned
@@ -528,10 +622,7 @@ static void dist_vcycle(sb_dist d, const Cyc &cp, int k, const std::vector<const
         cur[i] = pout[i];
         oth[i] = (pout[i] == X[i]) ? lev(i).t : X[i];
     }
-    for (int s = 0; s < cp.post; ++s) {
-        halo(cur);
-        sweep();
-    }
+    for (int s = 0; s < cp.post; ++s) halo_sweep();
 }
 
 // ---- distributed Krylov drivers -------------------------------------------------------------
@@ -769,6 +860,9 @@ static void build_rank(sb_dist d, RankDev &R, const Hier &h, int rank, int64_t g
     R.hi = R.P.L[0].hi;
     ctx_finish(c, h, o, nvec, d->fr, d->fr > 0 ? R.D[0].wb : 0);
     R.s = c->stream;
+    CK(cudaStreamCreateWithFlags(&R.s2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&R.ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&R.ev_join, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&R.ready, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&R.done, cudaEventDisableTiming));
 }
@@ -1185,6 +1279,9 @@ void sb_dist_destroy(sb_dist d) {
     if (d->comm) nccl().CommDestroy(d->comm);
     for (auto &r : d->R) {
         if (r.ready) cudaEventDestroy(r.ready);
+        if (r.ev_fork) cudaEventDestroy(r.ev_fork);
+        if (r.ev_join) cudaEventDestroy(r.ev_join);
+        if (r.s2) cudaStreamDestroy(r.s2);
         if (r.done) cudaEventDestroy(r.done);
         if (r.c) sb_destroy(r.c);
     }

@@ -504,12 +504,16 @@ __global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
 #define SB_CROSS_MINB 6  // measured (C2 / 256^3 L0 sweeps): 256 x 6 best of 256 x 4,5,6, 128 x 8,10,12, 512 x 2
 #endif
 constexpr int kCrossThreads = SB_CROSS_THREADS;
-template <int MODE, int NV, int W>
+template <int MODE, int NV, int W, bool RG = false>
 __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
     k_crosspair(int n, const uint8_t *__restrict__ pid, int np, const unsigned char *__restrict__ table,
                 const uint32_t *__restrict__ rmask, const __grid_constant__ MainPat<W> mp,
                 const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
-                const int *skip, Red red) {
+                const int *skip, Red red, int q_lo_, int q_hi_) {
+    // RG: only the pairs [q_lo_, q_hi_) (the partitioned path sweeps its
+    // interior while the halo is in flight, then the rest); else every pair.
+    // (Separate instantiation: the range bounds as runtime values cost the
+    // whole-level sweep ~20% at 256^3, measured.)
     static_assert(W == 7 || W == 5, "cross geometries");
     constexpr int C = W / 2;  // centre slot (offset 0)
     extern __shared__ __align__(16) unsigned char smem[];
@@ -518,6 +522,7 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
 #pragma unroll
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
     const int npairs = n >> 1;
+    const int q_lo = RG ? q_lo_ : 0, q_hi = RG ? q_hi_ : npairs;
     const int stride = gridDim.x * kCrossThreads;
     const int lo = -mp.o[0] + 2, hi = n - (mp.o[W - 1] + 3);
     auto emit = [&](int row, double o, double fi, double xi) {
@@ -535,16 +540,16 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
     auto pair_of = [&](int qq) {
         return static_cast<uint32_t>(*reinterpret_cast<const uint16_t *>(pid + 2 * min(qq, npairs - 1)));
     };
-    uint32_t ppn = npairs > 0 ? pair_of(blockIdx.x * kCrossThreads + threadIdx.x) : 0u;
+    uint32_t ppn = q_hi > q_lo ? pair_of(q_lo + blockIdx.x * kCrossThreads + threadIdx.x) : 0u;
     pdl_wait();
     if (!(skip && *skip)) {
-        for (int q = blockIdx.x * kCrossThreads + threadIdx.x, base = blockIdx.x * kCrossThreads; base < npairs;
-             q += stride, base += stride) {
-            if (base + stride >= npairs) pdl_trigger();
-            const bool in = q < npairs;
+        for (int q = q_lo + blockIdx.x * kCrossThreads + threadIdx.x, base = q_lo + blockIdx.x * kCrossThreads;
+             base < q_hi; q += stride, base += stride) {
+            if (base + stride >= q_hi) pdl_trigger();
+            const bool in = q < q_hi;
             const unsigned inm = __ballot_sync(0xffffffffu, in);
             const uint32_t ppc = ppn;
-            if (base + stride < npairs) ppn = pair_of(q + stride);
+            if (base + stride < q_hi) ppn = pair_of(q + stride);
             if (!inm) continue;
             const int src = __ffs(inm) - 1;
             const int r0w = __shfl_sync(0xffffffffu, 2 * q, src);

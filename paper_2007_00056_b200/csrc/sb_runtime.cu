@@ -1840,11 +1840,11 @@ static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double
             else if (l.pat_w == 7)
                 launch_k(c, k_crosspair<MODE, NV, 7>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
                          static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<7>(l), x, f,
-                         out, omega, skip, red);
+                         out, omega, skip, red, 0, static_cast<int>(l.n / 2));
             else
                 launch_k(c, k_crosspair<MODE, NV, 5>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
                          static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<5>(l), x, f,
-                         out, omega, skip, red);
+                         out, omega, skip, red, 0, static_cast<int>(l.n / 2));
             return;
         }
         if constexpr (kExperimental)
@@ -1911,6 +1911,27 @@ static void launch_pat_rr(sb_ctx c, const DevLevel &l, const DevLevel &lc, cudaS
 static void launch_jacobi(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *xin, const double *f,
                           double *xout, double omega) {
     launch_csr<M_JACOBI, 0>(c, l, s, xin, f, xout, omega, nullptr, Red{});
+}
+
+// A Jacobi sweep over the row pairs [q_lo, q_hi) of a k_crosspair level (the
+// partitioned path: interior while the halo is in flight, then the edges).
+static bool cross_range_ok(const DevLevel &l, const double *x, const double *f, const double *out) {
+    auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return l.pat && l.box_pair == 2 && (l.pat_w == 7 || l.pat_w == 5) && a16(x) && a16(f) && a16(out);
+}
+static void launch_jacobi_range(sb_ctx c, const DevLevel &l, cudaStream_t s, const double *xin, const double *f,
+                                double *xout, double omega, int64_t q_lo, int64_t q_hi) {
+    if (q_hi <= q_lo) return;
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>((q_hi - q_lo + kCrossThreads - 1) / kCrossThreads, static_cast<int64_t>(l.box_grid))));
+    if (l.pat_w == 7)
+        launch_k(c, k_crosspair<M_JACOBI, 0, 7, true>, dim3(grid), dim3(kCrossThreads), l.pat_tb, s, static_cast<int>(l.n),
+                 l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<7>(l), xin, f, xout, omega,
+                 static_cast<const int *>(nullptr), Red{}, static_cast<int>(q_lo), static_cast<int>(q_hi));
+    else
+        launch_k(c, k_crosspair<M_JACOBI, 0, 5, true>, dim3(grid), dim3(kCrossThreads), l.pat_tb, s, static_cast<int>(l.n),
+                 l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<5>(l), xin, f, xout, omega,
+                 static_cast<const int *>(nullptr), Red{}, static_cast<int>(q_lo), static_cast<int>(q_hi));
 }
 
 // TMA descriptor of an nx x ny x nz f64 grid at p with an (bx, by, 1) box,

@@ -190,3 +190,49 @@ def test_dist_p2p_two_processes_ipc(sp, tmp_path, graphs):
         assert m["it"] == ref.report.iterations
         x[m["lo"]:m["hi"]] = np.load(tmp_path / f"x{r}.npy")
     assert np.array_equal(x.view(np.uint64), ref.x.view(np.uint64))
+
+
+_OVERLAP_WORKER = r"""
+import os, sys, json, hashlib, numpy as np
+sys.path.insert(0, os.environ["SB_ROOT"])
+from paper_2007_00056_b200 import sparsh as sp
+from paper_2007_00056_b200.dist import DistSolver
+A = sp.poisson3d(48)
+h = sp.Hierarchy(A, sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40))
+cp = sp.CycleParams(6, 6, sp.SmootherKind.weighted_jacobi())
+b = sp.rhs_ones(A.nrows())
+out = {}
+for transport in ("local", "p2p"):
+    for graphs in (True, False):
+        ds = DistSolver(h, 2, 2048, transport=transport, graphs=graphs)
+        r = ds.pcg(b, cp, 1e-8 * np.sqrt(A.nrows()), 100)
+        out[f"{transport}-{int(graphs)}"] = [r.report.iterations, ds.last_launches(),
+                                             hashlib.sha1(r.x.tobytes()).hexdigest()]
+print(json.dumps(out))
+"""
+
+
+def test_dist_interior_overlap_bitwise():
+    """The halo/interior overlap (interior row pairs swept while the halo is in
+    flight, then the edge rows) changes the launch sequence, not one bit of the
+    solution: on vs off (SB_DIST_OVERLAP=0), both transports, graph and eager."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    res = {}
+    for ov in ("1", "0"):
+        env = dict(os.environ, SB_ROOT=ROOT, SB_DIST_OVERLAP=ov)
+        p = subprocess.run([sys.executable, "-c", _OVERLAP_WORKER], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert p.returncode == 0, p.stderr[-3000:]
+        res[ov] = json.loads(p.stdout.strip().splitlines()[-1])
+    hashes = {v[2] for r in res.values() for v in r.values()}
+    assert len(hashes) == 1, res
+    for key in res["1"]:
+        assert res["1"][key][0] == res["0"][key][0]
+    # overlap active on the P2P transport (publish / interior / wait / edges)
+    # and on the eager local transport (side stream)
+    assert res["1"]["p2p-1"][1] > res["0"]["p2p-1"][1], res
+    assert res["1"]["local-0"][1] > res["0"]["local-0"][1], res
