@@ -198,8 +198,9 @@ int64_t sb_last_solve_launches(sb_ctx ctx);
 /* Times `reps` back-to-back launches of one kernel on level `level` with CUDA
  * events on sb_stream; *avg_ms = mean per launch. kind: 0 Jacobi sweep,
  * 1 SpMV, 2 residual, 3 one V-cycle from x = 0 launched eagerly, 4 the same
- * V-cycle captured once as a CUDA graph and replayed (cp required for 0, 3, 4).
- * *launches = kernels launched per repetition. */
+ * V-cycle captured once as a CUDA graph and replayed, 5 a graph of 32 chained
+ * Jacobi sweeps (the in-graph cost of one sweep = *avg_ms / *launches; cp
+ * required for 0, 3, 4, 5). *launches = kernels launched per repetition. */
 int sb_time_kernel(sb_ctx ctx, int kind, int level, const sb_cycle *cp, int reps, double *avg_ms,
                    int *launches);
 /* Same, with a cold L2: before every launch a write of flush_bytes (> the

@@ -388,14 +388,27 @@ __global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
     const int npairs = n >> 1;
     const int stride = gridDim.x * kBoxThreads;
     const int lo = -mp.o[0] + 2, hi = n - (mp.o[26] + 3);  // pairs starting in [lo, hi) read inside [0, n)
-    auto emit = [&](int row, double o, double fi, double xi) {
-        out[row] = o;
+    // M_RESID_RESTRICT (coarse row q = fine rows 2q, 2q + 1; red.w0 = a_cc,
+    // red.w1 = the coarse first-sweep destination or null): f_c = (0 + r0) + r1
+    // (csr.hpp:267-274 then the unit-P spmv_transpose, csr.hpp:232-239) and
+    // x0_c = 0 + (w f_c) / a_cc, the operation order of k_pat_resid_restrict
+    auto restrict_pair = [&](int qc, double r0, double r1) {
+        const double s = __dadd_rn(__dadd_rn(0.0, r0), r1);
+        out[qc] = s;
+        if (red.w1)
+            const_cast<double *>(red.w1)[qc] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), __ldg(red.w0 + qc)));
+    };
+    auto accum = [&](int row, double o, double fi, double xi) {
         if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fi : red.w0 == x ? xi : red.w0[row]) : o);
         if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? (red.w1 == x ? xi : red.w1[row]) : o);
     };
+    auto emit = [&](int row, double o, double fi, double xi) {
+        out[row] = o;
+        accum(row, o, fi, xi);
+    };
     auto fin = [&](double xi, double fi, double sum, double dg, double ry) -> double {
         if constexpr (MODE == M_SPMV) return sum;
-        else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
+        else if constexpr (MODE == M_RESID || MODE == M_RESID_RESTRICT) return __dsub_rn(fi, sum);
         else return __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), dg, ry));
     };
     // the pattern bytes are constant: the first pair's before the dependency
@@ -503,9 +516,12 @@ __global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
 #ifndef SB_CROSS_MINB
 #define SB_CROSS_MINB 6  // measured (C2 / 256^3 L0 sweeps): 256 x 6 best of 256 x 4,5,6, 128 x 8,10,12, 512 x 2
 #endif
+#ifndef SB_CROSS_MINB_NV
+#define SB_CROSS_MINB_NV 4  // fused-dot variants (SpMV + dot, last sweep + dot): room for the reduction state
+#endif
 constexpr int kCrossThreads = SB_CROSS_THREADS;
 template <int MODE, int NV, int W, bool RG = false>
-__global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
+__global__ void __launch_bounds__(kCrossThreads, NV > 0 ? SB_CROSS_MINB_NV : SB_CROSS_MINB)
     k_crosspair(int n, const uint8_t *__restrict__ pid, int np, const unsigned char *__restrict__ table,
                 const uint32_t *__restrict__ rmask, const __grid_constant__ MainPat<W> mp,
                 const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out, double omega,
@@ -525,14 +541,27 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
     const int q_lo = RG ? q_lo_ : 0, q_hi = RG ? q_hi_ : npairs;
     const int stride = gridDim.x * kCrossThreads;
     const int lo = -mp.o[0] + 2, hi = n - (mp.o[W - 1] + 3);
-    auto emit = [&](int row, double o, double fi, double xi) {
-        out[row] = o;
+    // M_RESID_RESTRICT (coarse row q = fine rows 2q, 2q + 1; red.w0 = a_cc,
+    // red.w1 = the coarse first-sweep destination or null): f_c = (0 + r0) + r1
+    // (csr.hpp:267-274 then the unit-P spmv_transpose, csr.hpp:232-239) and
+    // x0_c = 0 + (w f_c) / a_cc, the operation order of k_pat_resid_restrict
+    auto restrict_pair = [&](int qc, double r0, double r1) {
+        const double s = __dadd_rn(__dadd_rn(0.0, r0), r1);
+        out[qc] = s;
+        if (red.w1)
+            const_cast<double *>(red.w1)[qc] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), __ldg(red.w0 + qc)));
+    };
+    auto accum = [&](int row, double o, double fi, double xi) {
         if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fi : red.w0 == x ? xi : red.w0[row]) : o);
         if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? (red.w1 == x ? xi : red.w1[row]) : o);
     };
+    auto emit = [&](int row, double o, double fi, double xi) {
+        out[row] = o;
+        accum(row, o, fi, xi);
+    };
     auto fin = [&](double xi, double fi, double sum, double dg, double ry) -> double {
         if constexpr (MODE == M_SPMV) return sum;
-        else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
+        else if constexpr (MODE == M_RESID || MODE == M_RESID_RESTRICT) return __dsub_rn(fi, sum);
         else return __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), dg, ry));
     };
     // the pattern bytes are constant: the first pair's before the dependency
@@ -541,7 +570,14 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
         return static_cast<uint32_t>(*reinterpret_cast<const uint16_t *>(pid + 2 * min(qq, npairs - 1)));
     };
     uint32_t ppn = q_hi > q_lo ? pair_of(q_lo + blockIdx.x * kCrossThreads + threadIdx.x) : 0u;
+#ifdef SB_XP_TRACE
+    const unsigned long long t_in = gtime();
+    unsigned long long t_ld = 0;
+#endif
     pdl_wait();
+#ifdef SB_XP_TRACE
+    const unsigned long long t_w = gtime();
+#endif
     if (!(skip && *skip)) {
         for (int q = q_lo + blockIdx.x * kCrossThreads + threadIdx.x, base = q_lo + blockIdx.x * kCrossThreads;
              base < q_hi; q += stride, base += stride) {
@@ -579,6 +615,15 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
                     b[k] = v2.y;
                 }
                 double s0 = 0.0, s1 = 0.0;
+#ifdef SB_XP_TRACE
+                {
+                    double chk = fv.x;
+#pragma unroll
+                    for (int k = 0; k < W; ++k) chk += a[k] + b[k];
+                    if (chk == 1.2345e300) t_ld = 1;
+                    t_ld = max(t_ld, gtime());
+                }
+#endif
                 if (__all_sync(0xffffffffu, (m0 & m1) == (1u << W) - 1u)) {
 #pragma unroll
                     for (int k = 0; k < W; ++k) {
@@ -594,14 +639,18 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
                 }
                 if (in) {
                     const double o0 = fin(a[C], fv.x, s0, mp.d, mp.r), o1 = fin(b[C], fv.y, s1, mp.d, mp.r);
-                    if constexpr (NV == 0) {
-                        *reinterpret_cast<double2 *>(out + r) = make_double2(o0, o1);
-                    } else {
-                        emit(r, o0, fv.x, a[C]);
-                        emit(r + 1, o1, fv.y, b[C]);
+                    if constexpr (MODE == M_RESID_RESTRICT) {
+                        restrict_pair(q, o0, o1);
+                        continue;
+                    }
+                    *reinterpret_cast<double2 *>(out + r) = make_double2(o0, o1);
+                    if constexpr (NV > 0) {
+                        accum(r, o0, fv.x, a[C]);
+                        accum(r + 1, o1, fv.y, b[C]);
                     }
                 }
             } else if (in) {  // the row-pattern per-row path for both rows
+                double o0r = 0.0, o1r = 0.0;
 #pragma unroll 1
                 for (int h = 0; h < 2; ++h) {
                     const int row = r + h, p = h ? p1 : p0;
@@ -611,12 +660,34 @@ __global__ void __launch_bounds__(kCrossThreads, SB_CROSS_MINB)
                     double sum = 0.0;
                     const int len = T.l(p);
                     for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(T.v(p, k), __ldg(xrow + T.o(p, k))));
-                    emit(row, fin(xi, fi, sum, T.d(p), T.r(p)), fi, xi);
+                    if constexpr (MODE == M_RESID_RESTRICT) (h ? o1r : o0r) = fin(xi, fi, sum, 0.0, 0.0);
+                    else emit(row, fin(xi, fi, sum, T.d(p), T.r(p)), fi, xi);
                 }
+                if constexpr (MODE == M_RESID_RESTRICT) restrict_pair(q, o0r, o1r);
             }
         }
     }
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);
+#ifdef SB_XP_TRACE
+    const unsigned long long t_end = gtime();
+    __shared__ unsigned long long s_ld, s_end;
+    if (threadIdx.x == 0) s_ld = s_end = 0;
+    __syncthreads();
+    atomicMax(&s_ld, t_ld);
+    atomicMax(&s_end, t_end);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned i = atomicAdd(&g_xp_n, 1u);
+        if (i < 65536u) {
+            g_xp_trace[6 * i] = t_in;
+            g_xp_trace[6 * i + 1] = t_w;
+            g_xp_trace[6 * i + 2] = s_end;
+            g_xp_trace[6 * i + 3] = blockIdx.x;
+            g_xp_trace[6 * i + 4] = s_ld;
+            g_xp_trace[6 * i + 5] = gtime();
+        }
+    }
+#endif
 }
 
 // Residual + restriction (k_pat_resid_restrict) on 7-point cross levels with

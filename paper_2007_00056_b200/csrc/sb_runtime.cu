@@ -100,6 +100,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
 // Programmatic dependent launch: wait for the predecessor grid's completion
 // (no-op when launched without the attribute) / allow the successor to launch.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifdef SB_XP_TRACE
+// diagnostics build only (tools/xp_trace.py): per-CTA globaltimer stamps of
+// k_crosspair (entry, after the dependency wait, exit)
+__device__ unsigned long long g_xp_trace[6 * 65536];
+__device__ unsigned g_xp_n;
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // grid-stride kernels: a CTA with at most one iteration over n items lets the
 // dependent grid launch now (it still waits for this grid's completion); CTAs
@@ -359,7 +370,9 @@ enum CsrMode {
     M_RESID = 1,         // r = f - A x                      (csr.hpp:267-274)
     M_JACOBI = 2,        // x' = x + w (f - A x) / a_ii      (smoother.hpp:113-120)
     // 3: retired (the first sweep from x = 0 is written by the parent's restriction)
-    M_JACOBI_PROLONG = 4 // prolongation + first post-sweep fused: x_j + (0 + x_c[agg_j])
+    M_JACOBI_PROLONG = 4, // prolongation + first post-sweep fused: x_j + (0 + x_c[agg_j])
+    M_RESID_RESTRICT = 5  // k_crosspair on a level whose aggregates are its row pairs: the pair's
+                          // residuals -> f_c = (0 + r_2c) + r_2c+1 and the coarse first sweep
 };
 
 // Operands of the fused modes.
@@ -1575,12 +1588,13 @@ struct DevLevel {
     size_t tb_smem = 0;
     const double *tb_tab = nullptr;
     // row pairs on 27-point box levels with even strides (k_boxpair)
-    int box_pair = 0, box_grid = 0;
+    int box_pair = 0, box_grid = 0, box_grid_nv = 0;  // box_grid_nv: the fused-dot variants
     const uint32_t *box_rmask = nullptr;
     const unsigned char *march_table = nullptr;
     const uint8_t *pat_id = nullptr;
     const unsigned char *pat_table = nullptr;
     int2 *mem = nullptr;
+    bool pair_aggs = false;  // mem[c] == (2c, 2c + 1) for every coarse row
     int ntiles = 0, cap = 0, grid = 0;
     size_t smem = 0;
     double *x = nullptr, *f = nullptr, *t = nullptr;
@@ -1712,6 +1726,10 @@ static CondSet conds(std::initializer_list<cudaGraphConditionalHandle> hs) {
 
 // ---- launchers (each counts the kernels it emits) -------------------------------
 
+static const bool c_pair_rr_off = [] {  // SB_PAIR_RR=0: k_pat_resid_restrict on pair levels too
+    const char *e = std::getenv("SB_PAIR_RR");
+    return e && std::atoi(e) == 0;
+}();
 static const bool c_cross_rr_off = [] {  // opt-in (SB_CROSS_RR=1): measured slower than k_pat_resid_restrict
     const char *e = std::getenv("SB_CROSS_RR");   // (C2 14.07 vs 13.70 ms, T256 98.0 vs 97.6 ms)
     return !(e && std::atoi(e) != 0);
@@ -1838,11 +1856,11 @@ static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double
                          static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<28>(l), x, f,
                          out, omega, skip, red);
             else if (l.pat_w == 7)
-                launch_k(c, k_crosspair<MODE, NV, 7>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
+                launch_k(c, k_crosspair<MODE, NV, 7>, dim3(NV > 0 ? l.box_grid_nv : l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
                          static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<7>(l), x, f,
                          out, omega, skip, red, 0, static_cast<int>(l.n / 2));
             else
-                launch_k(c, k_crosspair<MODE, NV, 5>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
+                launch_k(c, k_crosspair<MODE, NV, 5>, dim3(NV > 0 ? l.box_grid_nv : l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
                          static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<5>(l), x, f,
                          out, omega, skip, red, 0, static_cast<int>(l.n / 2));
             return;
@@ -1886,6 +1904,22 @@ static void launch_pat_rr_w(sb_ctx c, const DevLevel &l, const DevLevel &lc, cud
 static void launch_pat_rr(sb_ctx c, const DevLevel &l, const DevLevel &lc, cudaStream_t s, const double *x,
                           const double *f, double *x0, double omega) {
     auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (l.box_pair == 2 && l.pair_aggs && a16(x) && a16(f) && !c_pair_rr_off) {
+        // k_crosspair computes both rows of coarse row q; the coarse diagonal and
+        // the first-sweep destination travel in the (otherwise unused) Red slots
+        Red rr{};
+        rr.w0 = lc.diag;
+        rr.w1 = x0;
+        if (l.pat_w == 7)
+            launch_k(c, k_crosspair<M_RESID_RESTRICT, 0, 7>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
+                     static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<7>(l), x, f, lc.f,
+                     omega, static_cast<const int *>(nullptr), rr, 0, static_cast<int>(l.n / 2));
+        else
+            launch_k(c, k_crosspair<M_RESID_RESTRICT, 0, 5>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
+                     static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<5>(l), x, f, lc.f,
+                     omega, static_cast<const int *>(nullptr), rr, 0, static_cast<int>(l.n / 2));
+        return;
+    }
 #if SB_EXPERIMENTAL
     if (l.box_pair == 2 && l.pat_w == 7 && a16(x) && a16(f) && !c_cross_rr_off) {
         const int grid = static_cast<int>(std::max<int64_t>(
@@ -3038,6 +3072,10 @@ static void upload_level(sb_ctx c, const HostLevel &H, DevLevel &D, bool coarses
         }
         D.mem = dalloc<int2>(c, D.nc);
         CK(cudaMemcpy(D.mem, mem.data(), sizeof(int2) * mem.size(), cudaMemcpyHostToDevice));
+        // every aggregate the row pair (2c, 2c + 1) (node-HEM on a grid level)
+        D.pair_aggs = A.n % 2 == 0 && D.nc == A.n / 2;
+        for (int64_t q = 0; D.pair_aggs && q < D.nc; ++q)
+            D.pair_aggs = mem[static_cast<size_t>(q)].x == 2 * q && mem[static_cast<size_t>(q)].y == 2 * q + 1;
     }
     D.t = dalloc<double>(c, A.n);
     if (A.n != n0 || &D != &c->L[0]) {  // level 0 uses the caller's / Krylov vectors
@@ -3625,6 +3663,16 @@ static void ctx_finish(sb_ctx c, const Hier &h, const sb_device_opts &o, int64_t
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_crosspair<M_JACOBI, 0, 5>, th, l.pat_tb));
             const int64_t need = (l.n / 2 + th - 1) / th;
             l.box_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
+            l.box_grid_nv = l.box_grid;
+            if (l.box_pair == 2) {
+                occ = 0;
+                if (l.pat_w == 7)
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_crosspair<M_SPMV, 1, 7>, th, l.pat_tb));
+                else
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_crosspair<M_SPMV, 1, 5>, th, l.pat_tb));
+                l.box_grid_nv =
+                    static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, nsm * std::max(occ, 1))));
+            }
         }
         if (l.march_geo >= 0) {
             occ = 0;
@@ -3890,7 +3938,7 @@ static int time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int re
         const DevLevel &l = level_of(c, level);
         if (reps < 1) throw invalid_argument("sb_time_kernel: reps must be >= 1");
         Cyc y;
-        if (kind == 0 || kind == 3) y = check_cycle(c, cp, "sb_time_kernel");
+        if (kind == 0 || kind == 3 || kind == 4 || kind == 5) y = check_cycle(c, cp, "sb_time_kernel");
         CK(cudaSetDevice(c->device));
         cudaStream_t s = c->stream;
         double *x = c->kv[KX], *t = c->kv[KZ], *f = c->kv[KB];
@@ -3916,6 +3964,21 @@ static int time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int re
                     cudaGraph_t g = begin_capture(c);
                     c->launch_count = 0;
                     emit_vcycle(c, s, y, level, f, t, true);
+                    vlaunch = c->launch_count;
+                    end_capture(c, g);
+                    CK(cudaGraphInstantiate(&vgraph, g, 0));
+                    cudaGraphDestroy(g);
+                }
+                CK(cudaGraphLaunch(vgraph, s));
+                c->launch_count = vlaunch;
+            } else if (kind == 5) {  // 32 chained Jacobi sweeps captured as one graph
+                if (!vgraph) {
+                    cudaGraph_t g = begin_capture(c);
+                    c->launch_count = 0;
+                    for (int r = 0; r < 32; ++r) {
+                        launch_jacobi(c, l, s, x, f, t, y.omega);
+                        std::swap(x, t);
+                    }
                     vlaunch = c->launch_count;
                     end_capture(c, g);
                     CK(cudaGraphInstantiate(&vgraph, g, 0));
@@ -3962,6 +4025,20 @@ static int time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int re
     });
 }
 
+#ifdef SB_XP_TRACE
+extern "C" int sb_debug_xp_trace(unsigned long long *out, int cap, int reset) {
+    unsigned n = 0;
+    cudaMemcpyFromSymbol(&n, g_xp_n, sizeof(n));
+    n = std::min<unsigned>(n, 65536u);
+    const int m = std::min<int>(static_cast<int>(n), cap);
+    if (m > 0) cudaMemcpyFromSymbol(out, g_xp_trace, sizeof(unsigned long long) * 6 * m);
+    if (reset) {
+        unsigned z = 0;
+        cudaMemcpyToSymbol(g_xp_n, &z, sizeof(z));
+    }
+    return m;
+}
+#endif
 int sb_time_kernel(sb_ctx c, int kind, int level, const sb_cycle *cp, int reps, double *avg_ms, int *launches) {
     return time_kernel(c, kind, level, cp, reps, 0, avg_ms, launches);
 }
