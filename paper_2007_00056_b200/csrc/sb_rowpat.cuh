@@ -614,6 +614,27 @@ __global__ void __launch_bounds__(kCrossThreads, NV > 0 ? SB_CROSS_MINB_NV : SB_
                     a[k] = v2.x;
                     b[k] = v2.y;
                 }
+                if constexpr (MODE == M_JACOBI_PROLONG) {
+                    // x' = x + (0 + x_c[j / 2]) at every row read: rows r-1 | r, r+1 |
+                    // r+2 are pairs q-1 | q | q+1, the even offsets' rows pair q + o/2
+                    const int qq = r >> 1;
+                    const double *xc = red.w0;
+                    const double cm = __dadd_rn(0.0, __ldg(xc + qq - 1)), c0 = __dadd_rn(0.0, __ldg(xc + qq)),
+                                 cq = __dadd_rn(0.0, __ldg(xc + qq + 1));
+                    a[C - 1] = __dadd_rn(a[C - 1], cm);
+                    a[C] = __dadd_rn(a[C], c0);
+                    a[C + 1] = __dadd_rn(a[C + 1], c0);
+                    b[C - 1] = __dadd_rn(b[C - 1], c0);
+                    b[C] = __dadd_rn(b[C], c0);
+                    b[C + 1] = __dadd_rn(b[C + 1], cq);
+#pragma unroll
+                    for (int k = 0; k < W; ++k) {
+                        if (k >= C - 1 && k <= C + 1) continue;
+                        const double ck = __dadd_rn(0.0, __ldg(xc + qq + mp.o[k] / 2));
+                        a[k] = __dadd_rn(a[k], ck);
+                        b[k] = __dadd_rn(b[k], ck);
+                    }
+                }
                 double s0 = 0.0, s1 = 0.0;
 #ifdef SB_XP_TRACE
                 {
@@ -655,11 +676,17 @@ __global__ void __launch_bounds__(kCrossThreads, NV > 0 ? SB_CROSS_MINB_NV : SB_
                 for (int h = 0; h < 2; ++h) {
                     const int row = r + h, p = h ? p1 : p0;
                     const double *xrow = x + row;
-                    const double xi = __ldg(xrow);
+                    auto xv = [&](int o) {  // x' = x + (0 + x_c[j / 2]) for M_JACOBI_PROLONG
+                        if constexpr (MODE == M_JACOBI_PROLONG)
+                            return __dadd_rn(__ldg(xrow + o), __dadd_rn(0.0, __ldg(red.w0 + ((row + o) >> 1))));
+                        else
+                            return __ldg(xrow + o);
+                    };
+                    const double xi = xv(0);
                     const double fi = (MODE == M_SPMV) ? 0.0 : __ldg(f + row);
                     double sum = 0.0;
                     const int len = T.l(p);
-                    for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(T.v(p, k), __ldg(xrow + T.o(p, k))));
+                    for (int k = 0; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(T.v(p, k), xv(T.o(p, k))));
                     if constexpr (MODE == M_RESID_RESTRICT) (h ? o1r : o0r) = fin(xi, fi, sum, 0.0, 0.0);
                     else emit(row, fin(xi, fi, sum, T.d(p), T.r(p)), fi, xi);
                 }

@@ -1868,6 +1868,23 @@ static void launch_csr(sb_ctx c, const DevLevel &l, cudaStream_t s, const double
         if constexpr (kExperimental)
             if (l.pat && l.march_geo >= 0) return launch_march_g<MODE, NV, 0, 28>(c, l, s, x, f, out, omega, skip, red);
     }
+    if constexpr (MODE == M_JACOBI_PROLONG && NV == 0) {
+        // aggregates = row pairs: k_crosspair with x' = x + (0 + x_c[j / 2]) at its reads (x_c in red.w0)
+        auto a16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+        if (l.pat && l.box_pair == 2 && l.pair_aggs && a16(x) && a16(out) && a16(f)) {
+            Red rx{};
+            rx.w0 = aux.xc;
+            if (l.pat_w == 7)
+                launch_k(c, k_crosspair<MODE, 0, 7>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
+                         static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<7>(l), x, f,
+                         out, omega, skip, rx, 0, static_cast<int>(l.n / 2));
+            else
+                launch_k(c, k_crosspair<MODE, 0, 5>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
+                         static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<5>(l), x, f,
+                         out, omega, skip, rx, 0, static_cast<int>(l.n / 2));
+            return;
+        }
+    }
     if (l.pat) {
         switch (l.pat_w) {
         case 5: return launch_pat_w<MODE, NV, 5>(c, l, s, x, f, out, omega, skip, red, aux);
@@ -2159,7 +2176,16 @@ static void emit_vcycle(sb_ctx c, cudaStream_t s, const Cyc &cp, int k, const do
         const char *e = std::getenv("SB_PROLONG_SPLIT");
         return !(e && std::atoi(e) == 0);
     }();
-    const bool split = split_env && l.pat && l.box_pair == 2;
+    // aggregates = row pairs: the prolongation rides on k_crosspair's first
+    // post-sweep (SB_PAIR_PC=0: the split form)
+    static const bool pair_pc = [] {
+        const char *e = std::getenv("SB_PAIR_PC");
+        return !(e && std::atoi(e) == 0);
+    }();
+    auto a16p = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    const bool fused_pair = pair_pc && l.pat && l.box_pair == 2 && l.pair_aggs && a16p(cur) && a16p(post_first) &&
+                            a16p(f);
+    const bool split = split_env && l.pat && l.box_pair == 2 && !fused_pair;
     if (cp.post >= 1 && cur != post_first && !split) {
         // x' = cur + P x_c folded into the first post-sweep's gathers
         launch_csr<M_JACOBI_PROLONG, 0>(c, l, s, cur, f, post_first, cp.omega, nullptr, Red{},
