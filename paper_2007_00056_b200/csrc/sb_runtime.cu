@@ -1308,6 +1308,9 @@ struct X0 {
     const double *diag = nullptr;
     double *x0 = nullptr;
     double omega = 0.0;
+    // row-pattern level 0: a_ii = pdg[pid[i]] (1 B per row instead of the 8 B diagonal)
+    const uint8_t *pid = nullptr;
+    const double *pdg = nullptr;
     __device__ __forceinline__ void put(int64_t i, double v) const {
         if (x0) x0[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, v), diag[i]));
     }
@@ -1362,10 +1365,23 @@ template <typename Body> __device__ __forceinline__ void grid_rows(int64_t n, bo
         GRID_LOOP(i, n) body(std::integral_constant<int, 1>{}, i);
     }
 }
-__device__ __forceinline__ bool x0_ok(const X0 &z0) { return !z0.x0 || (al16(z0.x0) && al16(z0.diag)); }
+__device__ __forceinline__ bool x0_ok(const X0 &z0) {
+    return !z0.x0 || (al16(z0.x0) && (z0.pid || al16(z0.diag)));
+}
 template <int V> __device__ __forceinline__ void x0_put(const X0 &z0, int64_t i, const DV<V> &v) {
     if (!z0.x0) return;
-    const DV<V> d = ldv<V>(z0.diag, i);
+    DV<V> d;
+    if (z0.pid) {
+        if constexpr (V == 2) {
+            const uint32_t pp = *reinterpret_cast<const uint16_t *>(z0.pid + i);
+            d.v[0] = __ldg(z0.pdg + (pp & 0xff));
+            d.v[1] = __ldg(z0.pdg + (pp >> 8));
+        } else {
+            d.v[0] = __ldg(z0.pdg + z0.pid[i]);
+        }
+    } else {
+        d = ldv<V>(z0.diag, i);
+    }
     DV<V> o;
 #pragma unroll
     for (int k = 0; k < V; ++k) o.v[k] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z0.omega, v.v[k]), d.v[k]));
@@ -2280,6 +2296,17 @@ static cudaGraph_t end_capture(sb_ctx c, cudaGraph_t g) {
     return g;
 }
 
+// X0 of level 0 (the first zero-guess sweep written by a Krylov update kernel)
+static X0 level0_x0(sb_ctx c, double *x0, double omega) {
+    const DevLevel &l0 = c->L[0];
+    X0 z{static_cast<const double *>(l0.diag), x0, omega};
+    if (x0 && l0.pat && l0.pat_np > 0) {
+        z.pid = l0.pat_id;
+        z.pdg = reinterpret_cast<const double *>(l0.pat_table) + static_cast<size_t>(l0.pat_np) * ((l0.pat_w + 1) & ~1);
+    }
+    return z;
+}
+
 // PCG (krylov.hpp:65-119) as one graph: prologue IF (not converged at r0)
 // { z = M r; p = z, rz; WHILE (!done) { Ap, pAp -> alpha; x, r, ||r|| ->
 // tests; IF (!done) { z = M r; rz -> beta; p = z + beta p } } }; then the true
@@ -2321,7 +2348,7 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
             cudaGraphConditionalHandle h_vc = new_handle(s2);
             launch_k(c, k_pcg_update, dim3(vb), dim3(kVecThreads), 0, s2, 
                 n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})),
-                X0{static_cast<const double *>(l0.diag), x0, cp ? cp->omega : 0.0});
+                level0_x0(c, x0, cp ? cp->omega : 0.0));
             CK(cudaGetLastError());
             plan(c->plan.per_it);
             add_cond(c, s2, d2, h_vc, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
@@ -2358,8 +2385,8 @@ static cudaGraph_t build_bicg(sb_ctx c, const Cyc *cp, const double *b, double *
     // V-cycles that precondition them (X0)
     const int L = static_cast<int>(c->L.size());
     const bool fuse0 = cp && cp->pre >= 1 && L >= 2 && c->tail_from != 0;
-    const X0 x0p = fuse0 ? X0{static_cast<const double *>(l0.diag), zero_sweep_dest(c, *cp, 0, pt), cp->omega} : X0{};
-    const X0 x0s = fuse0 ? X0{static_cast<const double *>(l0.diag), zero_sweep_dest(c, *cp, 0, stv), cp->omega} : X0{};
+    const X0 x0p = fuse0 ? level0_x0(c, zero_sweep_dest(c, *cp, 0, pt), cp->omega) : X0{};
+    const X0 x0s = fuse0 ? level0_x0(c, zero_sweep_dest(c, *cp, 0, stv), cp->omega) : X0{};
     auto precond = [c, cp, n, fuse0](cudaStream_t ss, const double *in, double *out) {
         if (cp) emit_vcycle(c, ss, *cp, 0, in, out, true, fuse0);
         else CK(cudaMemcpyAsync(out, in, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToDevice, ss));
