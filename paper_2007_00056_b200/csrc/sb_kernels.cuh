@@ -69,6 +69,9 @@ struct Red {
     const double *w0;   // value 0 = sum out_i * w0_i (or custom, see kernels)
     const double *w1;   // value 1 = sum out_i * w1_i
     CondSet cs;
+    // k_crosspair M_RESID_RESTRICT on a row-pattern coarse level: a_cc = pdg[pid[c]]
+    const uint8_t *pid = nullptr;
+    const double *pdg = nullptr;
 };
 
 } // namespace sb

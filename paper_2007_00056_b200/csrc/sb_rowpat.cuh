@@ -388,16 +388,6 @@ __global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
     const int npairs = n >> 1;
     const int stride = gridDim.x * kBoxThreads;
     const int lo = -mp.o[0] + 2, hi = n - (mp.o[26] + 3);  // pairs starting in [lo, hi) read inside [0, n)
-    // M_RESID_RESTRICT (coarse row q = fine rows 2q, 2q + 1; red.w0 = a_cc,
-    // red.w1 = the coarse first-sweep destination or null): f_c = (0 + r0) + r1
-    // (csr.hpp:267-274 then the unit-P spmv_transpose, csr.hpp:232-239) and
-    // x0_c = 0 + (w f_c) / a_cc, the operation order of k_pat_resid_restrict
-    auto restrict_pair = [&](int qc, double r0, double r1) {
-        const double s = __dadd_rn(__dadd_rn(0.0, r0), r1);
-        out[qc] = s;
-        if (red.w1)
-            const_cast<double *>(red.w1)[qc] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), __ldg(red.w0 + qc)));
-    };
     auto accum = [&](int row, double o, double fi, double xi) {
         if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fi : red.w0 == x ? xi : red.w0[row]) : o);
         if (NV >= 2) acc[NV >= 2 ? 1 : 0] += o * (red.w1 ? (red.w1 == x ? xi : red.w1[row]) : o);
@@ -541,15 +531,18 @@ __global__ void __launch_bounds__(kCrossThreads, NV > 0 ? SB_CROSS_MINB_NV : SB_
     const int q_lo = RG ? q_lo_ : 0, q_hi = RG ? q_hi_ : npairs;
     const int stride = gridDim.x * kCrossThreads;
     const int lo = -mp.o[0] + 2, hi = n - (mp.o[W - 1] + 3);
-    // M_RESID_RESTRICT (coarse row q = fine rows 2q, 2q + 1; red.w0 = a_cc,
-    // red.w1 = the coarse first-sweep destination or null): f_c = (0 + r0) + r1
-    // (csr.hpp:267-274 then the unit-P spmv_transpose, csr.hpp:232-239) and
-    // x0_c = 0 + (w f_c) / a_cc, the operation order of k_pat_resid_restrict
+    // M_RESID_RESTRICT (coarse row q = fine rows 2q, 2q + 1; red.w0 = a_cc or
+    // red.pid / red.pdg the coarse pattern's, red.w1 = the coarse first-sweep
+    // destination or null): f_c = (0 + r0) + r1 (csr.hpp:267-274 then the
+    // unit-P spmv_transpose, csr.hpp:232-239) and x0_c = 0 + (w f_c) / a_cc,
+    // the operation order of k_pat_resid_restrict
     auto restrict_pair = [&](int qc, double r0, double r1) {
         const double s = __dadd_rn(__dadd_rn(0.0, r0), r1);
         out[qc] = s;
-        if (red.w1)
-            const_cast<double *>(red.w1)[qc] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), __ldg(red.w0 + qc)));
+        if (red.w1) {
+            const double d = red.pid ? __ldg(red.pdg + red.pid[qc]) : __ldg(red.w0 + qc);
+            const_cast<double *>(red.w1)[qc] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, s), d));
+        }
     };
     auto accum = [&](int row, double o, double fi, double xi) {
         if (NV >= 1) acc[0] += o * (red.w0 ? (red.w0 == f ? fi : red.w0 == x ? xi : red.w0[row]) : o);

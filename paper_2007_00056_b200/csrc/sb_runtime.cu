@@ -1943,6 +1943,10 @@ static void launch_pat_rr(sb_ctx c, const DevLevel &l, const DevLevel &lc, cudaS
         Red rr{};
         rr.w0 = lc.diag;
         rr.w1 = x0;
+        if (lc.pat && lc.pat_np > 0) {
+            rr.pid = lc.pat_id;
+            rr.pdg = reinterpret_cast<const double *>(lc.pat_table) + static_cast<size_t>(lc.pat_np) * ((lc.pat_w + 1) & ~1);
+        }
         if (l.pat_w == 7)
             launch_k(c, k_crosspair<M_RESID_RESTRICT, 0, 7>, dim3(l.box_grid), dim3(kCrossThreads), l.pat_tb, s,
                      static_cast<int>(l.n), l.pat_id, l.pat_np, l.pat_table, l.box_rmask, main_pat<7>(l), x, f, lc.f,
