@@ -121,11 +121,14 @@ def test_vcycle_27point_varied_bitexact(sp, port, tail_rows, monkeypatch):
         assert np.array_equal(sp.make_amg_preconditioner(h, _cp(sp)).apply(f), o.vcycle(f, np.zeros(A.nrows())))
 
 
-@pytest.mark.parametrize("which", ["p3", "p2", "cd"])
-def test_prolong_split_bitwise(sp, which):
-    """On row-pair levels the prolongation runs as its own vector pass
-    (k_prolong2) followed by k_crosspair sweeps; the V-cycle and the solve are
-    bit for bit the fused prolongation + first post-sweep (SB_PROLONG_SPLIT=0)."""
+@pytest.mark.parametrize("which", ["p3", "p2", "cd", "p3odd"])
+def test_pair_paths_bitwise(sp, which):
+    """Row-pair levels: residual + restriction through k_crosspair when the
+    aggregates are the row pairs (SB_PAIR_RR), the prolongation folded into
+    k_crosspair's first post-sweep (SB_PAIR_PC), the split prolongation
+    (k_prolong2 + sweeps, SB_PROLONG_SPLIT) and k_rowpat's fused prolongation:
+    every combination gives the V-cycle and the PCG solve bit for bit."""
+    import os
     import subprocess
     import sys
     from conftest import ROOT
@@ -136,12 +139,12 @@ def test_prolong_split_bitwise(sp, which):
             "r = sp.pcg(A, b, sp.make_amg_preconditioner(h, cp), 1e-8 * np.linalg.norm(b), 200); "
             "sys.stdout.write(v.tobytes().hex() + ' ' + r.x.tobytes().hex())")
     src = {"p3": "sp.poisson3d(32)", "p2": "sp.poisson2d(128, 96)",
-           "cd": "sp.convdiff3d(20, 18, 16, 1.0, 100.0, 1.0, 1.0)"}[which]
+           "cd": "sp.convdiff3d(20, 18, 16, 1.0, 100.0, 1.0, 1.0)", "p3odd": "sp.poisson3d(34, 22, 19)"}[which]
     outs = []
-    for on in ("1", "0"):
-        import os
-        out = subprocess.run([sys.executable, "-c", code % (ROOT, src)], env=dict(os.environ, SB_PROLONG_SPLIT=on),
-                             capture_output=True, text=True, timeout=600)
+    for rr, pc, split in (("1", "1", "1"), ("0", "0", "1"), ("1", "0", "0"), ("0", "1", "1")):
+        env = dict(os.environ, SB_PAIR_RR=rr, SB_PAIR_PC=pc, SB_PROLONG_SPLIT=split, SB_CROSS5="1")
+        out = subprocess.run([sys.executable, "-c", code % (ROOT, src)], env=env, capture_output=True, text=True,
+                             timeout=600)
         assert out.returncode == 0, out.stderr[-2000:]
         outs.append(out.stdout)
-    assert outs[0] and outs[0] == outs[1]
+    assert outs[0] and all(o == outs[0] for o in outs)
