@@ -7,8 +7,12 @@ import subprocess
 import sys
 
 rep, out_raw, out_json = sys.argv[1], sys.argv[2], sys.argv[3]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-open(out_raw, "w").write(raw)
+if rep.endswith(".csv"):  # a raw page exported on the GPU box
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep != out_raw:
+    open(out_raw, "w").write(raw)
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, r = rows[0], rows[1], rows[2]
 g = lambda k: r[hdr.index(k)] if k in hdr else None  # noqa: E731
