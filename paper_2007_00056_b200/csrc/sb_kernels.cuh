@@ -30,7 +30,8 @@ struct DevState {
     double rho, denom, omega, sn, true_res;
     double part[2];  // multi-rank: this rank's reduction totals
     double red[2];   // multi-rank: allreduced totals
-    int iter, max_iters, done, term, status, half, hist_cap, pad_;
+    int iter, max_iters, done, term, status, half, hist_cap;
+    int x_pending;  // PCG: x += alpha p of this iteration not applied yet (k_pcg_update_r -> k_xpay_x / k_x_final)
     unsigned long long t0;
     double *hist_r;
     double *hist_t;

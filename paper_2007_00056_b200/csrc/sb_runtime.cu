@@ -1446,6 +1446,70 @@ __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restri
     }
     finish_reduction<1>(red, a);
 }
+// PCG with the x update deferred (single-GPU graph): r += (-alpha) Ap; ||r||^2
+// (+ x0 of z = M r). x += alpha p is applied by the next k_xpay_x (which reads
+// p anyway) or, when the loop stops here, by k_x_final: the same operation on
+// the same values, so x is bit for bit krylov.hpp:96-97's; the update kernel
+// no longer streams x and p (16 B/row less per iteration, 8 B/row net).
+__global__ void k_pcg_update_r(int64_t n, double *__restrict__ r, const double *__restrict__ Ap, Red red, X0 z0) {
+    pdl_wait();
+    pdl_trigger_single(n);
+    double a[1] = {0.0};
+    DevState *st = red.st;
+    if (!st->done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->x_pending = 1;
+        const double nalpha = -st->alpha;
+        grid_rows(n, all16(r, Ap) && x0_ok(z0), [&](auto vc, int64_t i) {
+            constexpr int V = decltype(vc)::value;
+            DV<V> rv = ldv<V>(r, i);
+            const DV<V> av = ldv<V>(Ap, i);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                rv.v[k] = __dadd_rn(rv.v[k], __dmul_rn(nalpha, av.v[k]));
+                a[0] += rv.v[k] * rv.v[k];
+            }
+            stv<V>(r, i, rv);
+            x0_put<V>(z0, i, rv);
+        });
+    }
+    finish_reduction<1>(red, a);
+}
+// x += alpha p (the deferred update, krylov.hpp:96), then p = z + beta p (krylov.hpp:113)
+__global__ void k_xpay_x(int64_t n, const double *__restrict__ z, double *__restrict__ p, double *__restrict__ x,
+                         DevState *__restrict__ st) {
+    pdl_wait();
+    pdl_trigger_single(n);
+    const double beta = st->beta, alpha = st->alpha;
+    grid_rows(n, all16(z, p, x), [&](auto vc, int64_t i) {
+        constexpr int V = decltype(vc)::value;
+        const DV<V> zv = ldv<V>(z, i);
+        DV<V> pv = ldv<V>(p, i), xv = ldv<V>(x, i);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            xv.v[k] = __dadd_rn(xv.v[k], __dmul_rn(alpha, pv.v[k]));
+            pv.v[k] = __dadd_rn(zv.v[k], __dmul_rn(beta, pv.v[k]));
+        }
+        stv<V>(x, i, xv);
+        stv<V>(p, i, pv);
+    });
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->x_pending = 0;
+}
+// the last iteration's deferred x += alpha p (if its update kernel ran)
+__global__ void k_x_final(int64_t n, double *__restrict__ x, const double *__restrict__ p,
+                          DevState *__restrict__ st) {
+    pdl_wait();
+    pdl_trigger_single(n);
+    if (!st->x_pending) return;
+    const double alpha = st->alpha;
+    grid_rows(n, all16(x, p), [&](auto vc, int64_t i) {
+        constexpr int V = decltype(vc)::value;
+        DV<V> xv = ldv<V>(x, i);
+        const DV<V> pv = ldv<V>(p, i);
+#pragma unroll
+        for (int k = 0; k < V; ++k) xv.v[k] = __dadd_rn(xv.v[k], __dmul_rn(alpha, pv.v[k]));
+        stv<V>(x, i, xv);
+    });
+}
 // p = z + beta p (krylov.hpp:113)
 __global__ void k_xpay(int64_t n, const double *__restrict__ z, double *__restrict__ p,
                        const DevState *__restrict__ st) {
@@ -2316,6 +2380,11 @@ static X0 level0_x0(sb_ctx c, double *x0, double omega) {
 // tests; IF (!done) { z = M r; rz -> beta; p = z + beta p } } }; then the true
 // residual. cp == nullptr: identity preconditioner (z = r).
 static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x) {
+    // x += alpha p deferred into the p update (SB_DEFER_X=0: in the r update)
+    static const bool defer_x = [] {
+        const char *e = std::getenv("SB_DEFER_X");
+        return !(e && std::atoi(e) == 0);
+    }();
     const DevLevel &l0 = c->L[0];
     const int64_t n = l0.n;
     const int vb = vec_grid(n);
@@ -2350,9 +2419,14 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
         add_cond(c, s1, d1, h_loop, cudaGraphCondTypeWhile, [&](cudaStream_t s2, int d2) {
             launch_csr<M_SPMV, 1>(c, l0, s2, p, nullptr, Ap, 0.0, &c->st->done, make_red(c, EP_PCG_PAP, 1, p));
             cudaGraphConditionalHandle h_vc = new_handle(s2);
-            launch_k(c, k_pcg_update, dim3(vb), dim3(kVecThreads), 0, s2, 
-                n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})),
-                level0_x0(c, x0, cp ? cp->omega : 0.0));
+            if (defer_x)
+                launch_k(c, k_pcg_update_r, dim3(vb), dim3(kVecThreads), 0, s2, n, r, static_cast<const double *>(Ap),
+                         make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})),
+                         level0_x0(c, x0, cp ? cp->omega : 0.0));
+            else
+                launch_k(c, k_pcg_update, dim3(vb), dim3(kVecThreads), 0, s2,
+                         n, x, r, p, Ap, make_red(c, EP_PCG_RN, 1, nullptr, nullptr, conds({h_vc, h_loop})),
+                         level0_x0(c, x0, cp ? cp->omega : 0.0));
             CK(cudaGetLastError());
             plan(c->plan.per_it);
             add_cond(c, s2, d2, h_vc, cudaGraphCondTypeIf, [&](cudaStream_t s3, int) {
@@ -2365,12 +2439,18 @@ static cudaGraph_t build_pcg(sb_ctx c, const Cyc *cp, const double *b, double *x
                     launch_k(c, k_dot, dim3(vb), dim3(kVecThreads), 0, s3, n, r, z, nullptr, rz);
                     CK(cudaGetLastError());
                 }
-                launch_k(c, k_xpay, dim3(vb), dim3(kVecThreads), 0, s3, n, z, p, c->st);
+                if (defer_x)
+                    launch_k(c, k_xpay_x, dim3(vb), dim3(kVecThreads), 0, s3, n, static_cast<const double *>(z), p, x,
+                             c->st);
+                else
+                    launch_k(c, k_xpay, dim3(vb), dim3(kVecThreads), 0, s3, n, z, p, c->st);
                 CK(cudaGetLastError());
                 plan(c->plan.per_it_cond);
             });
         });
     });
+    if (defer_x)  // the last iteration's x += alpha p
+        launch_k(c, k_x_final, dim3(vb), dim3(kVecThreads), 0, s, n, x, static_cast<const double *>(p), c->st);
     // true residual ||b - A x|| (krylov.hpp:116)
     launch_csr<M_RESID, 1>(c, l0, s, x, b, c->rs, 0.0, nullptr, make_red(c, EP_STORE, 1));
     plan(c->plan.post);
