@@ -504,7 +504,8 @@ __global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
 #define SB_CROSS_THREADS 256
 #endif
 #ifndef SB_CROSS_MINB
-#define SB_CROSS_MINB 6  // measured (C2 / 256^3 L0 sweeps): 256 x 6 best of 256 x 4,5,6, 128 x 8,10,12, 512 x 2
+#define SB_CROSS_MINB 6  // measured (C2 / 256^3 L0 sweeps): 256 x 6 best of 256 x 4,5,6,8, 128 x 8,10,12, 512 x 2
+                         // (256 x 8 = 32 registers spills: 256^3 L0 110 vs 79 us cold)
 #endif
 #ifndef SB_CROSS_MINB_NV
 #define SB_CROSS_MINB_NV 4  // fused-dot variants (SpMV + dot, last sweep + dot): room for the reduction state
