@@ -185,3 +185,35 @@ def test_c2_shape_64cubed(sp, port):
     o = port.hierarchy(A, 500, 40).pcg(b, 1e-300, 16)
     r2 = sp.pcg(A, b, sp.make_amg_preconditioner(h, _cp(sp)), 1e-300, 16)
     assert rel(r2.x, o.x) < 1e-10
+
+
+@pytest.mark.parametrize("graphs", ["1", "0"])
+def test_deferred_x_update_bitwise(graphs):
+    """PCG with x += alpha p moved into the p update (k_xpay_x) or the post-loop
+    k_x_final: the same operation on the same values, so the solution, the
+    iteration count and the residual history equal the in-place update
+    (SB_DEFER_X=0) bit for bit -- also for a solve that stops at max_iters and
+    for plain CG (no preconditioner)."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from paper_2007_00056_b200 import sparsh as sp; "
+            "A = sp.poisson3d(40, 36, 30); "
+            "cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40); "
+            "h = sp.Hierarchy(A, cfg, graphs=%s); cp = sp.CycleParams.from_config(cfg); "
+            "b = sp.rhs_random(A.nrows(), 11); M = sp.make_amg_preconditioner(h, cp); "
+            "out = []\n"
+            "for tol, k in ((1e-8 * np.linalg.norm(b), 200), (1e-14 * np.linalg.norm(b), 5)):\n"
+            "    r = sp.pcg(A, b, M, tol, k)\n"
+            "    out += [r.x.tobytes().hex(), str(r.report.iterations), np.asarray(r.report.residual_history).tobytes().hex()]\n"
+            "r = sp.cg(A, b, 1e-8 * np.linalg.norm(b), 300)\n"
+            "out += [r.x.tobytes().hex(), str(r.report.iterations)]\n"
+            "sys.stdout.write(' '.join(out))")
+    outs = []
+    for on in ("1", "0"):
+        p = subprocess.run([sys.executable, "-c", code % (ROOT, "True" if graphs == "1" else "False")],
+                           env=dict(os.environ, SB_DEFER_X=on), capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(p.stdout.split())
+    assert outs[0] and outs[0] == outs[1]
