@@ -451,6 +451,17 @@ __device__ __forceinline__ double row_eval(int row, int rs, int re, const E &e, 
 
 // Rows longer than this are evaluated by a whole warp (k_csr_tile).
 constexpr int kLongRow = 32;
+// Rows longer than this (up to kHubMax per CTA; e.g. the hub row a stalled
+// coarsening leaves: ~560 entries on G128's deep levels) are deferred to the
+// end of k_csr_tile and evaluated by the whole CTA: every product at once into
+// shared memory, then one thread per row adds them in CSR order (~8 cycles per
+// entry). With a warp they paid a gather round trip per 32 entries: ~10 us
+// per sweep on those levels.
+#ifndef SB_HUB_ROW
+#define SB_HUB_ROW 32  // measured on G128: 32 (every warp-path row) 70.3 ms, 96: 71.5, 256: 74.0, warp path only: 83.9
+#endif
+constexpr int kHubRow = SB_HUB_ROW;
+constexpr int kHubMax = 16;  // deferred hub rows per CTA (more: the warp path)
 
 // row_eval of one long row by a warp: lane l multiplies entries k0 + l (the
 // products are the reference's, __dmul_rn), then every lane adds the 32
@@ -537,6 +548,10 @@ __global__ void __launch_bounds__(kTileRows, 3)
     __shared__ __align__(8) uint64_t empty[kStages];
     __shared__ int4 hdr[kStages];
     __shared__ double sdict[VF ? 256 : 1];
+    __shared__ int hub_rows[kHubMax];
+    __shared__ int hub_off[kHubMax + 1];
+    __shared__ int nhub;
+    __shared__ double hub_d[kHubMax];
     double acc[NV > 0 ? NV : 1];
 #pragma unroll
     for (int v = 0; v < (NV > 0 ? NV : 1); ++v) acc[v] = 0.0;
@@ -588,6 +603,7 @@ __global__ void __launch_bounds__(kTileRows, 3)
     }
     if constexpr (VF == 1)
         for (int i = threadIdx.x; i < ndict; i += blockDim.x) sdict[i] = dict[i];
+    if (threadIdx.x == 0) nhub = 0;
     __syncthreads();
     const int G = static_cast<int>(gridDim.x);
     const int b = static_cast<int>(blockIdx.x);
@@ -641,11 +657,103 @@ __global__ void __launch_bounds__(kTileRows, 3)
             for (unsigned m = lm; m; m &= m - 1) {  // gathers 32 entries at a time, sum in CSR order
                 const int src = __ffs(m) - 1;
                 const int lr = row - lane + src;
+                if (srp[lr + 1] - srp[lr] > kHubRow) {  // deferred to the CTA (below), if there is room
+                    int slot = 0;
+                    if (lane == 0) slot = atomicAdd(&nhub, 1);
+                    slot = __shfl_sync(0xffffffffu, slot, 0);
+                    if (slot < kHubMax) {
+                        if (lane == 0) hub_rows[slot] = lr;
+                        continue;
+                    }
+                }
                 const double o = warp_row_eval<MODE>(lr, srp[lr], srp[lr + 1], e, x, f, rhs_of(lr), aux, omega, lane);
                 if (lane == src) emit_row(lr, o);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+        }
+        // deferred hub rows: the whole CTA forms the products (every gather in
+        // flight at once) into the drained stage buffers, then thread q adds row
+        // q's products in CSR order. Every issued stage was consumed above, so
+        // no copy is in flight.
+        __syncthreads();
+        const int nh = min(nhub, kHubMax);
+        if (nh > 0) {
+            double *buf = reinterpret_cast<double *>(smem);
+            const int seg = static_cast<int>(kStages * sb / 8 < 8192 ? kStages * sb / 8 : 8192);
+            Ent<VF, CF> eg;
+            eg.vals = vals;
+            eg.cols = cols;
+            eg.dict = sdict;
+            if (threadIdx.x == 0) {
+                int o = 0;
+                for (int q = 0; q < nh; ++q) {
+                    hub_off[q] = o;
+                    o += rp[hub_rows[q] + 1] - rp[hub_rows[q]];
+                    hub_d[q] = 0.0;
+                }
+                hub_off[nh] = o;
+            }
+            __syncthreads();
+            auto finish = [&](int q, double sum) {
+                const int hr = hub_rows[q];
+                const double fi = (MODE == M_SPMV) ? 0.0 : f[hr];
+                double o;
+                if constexpr (MODE == M_SPMV) o = sum;
+                else if constexpr (MODE == M_RESID) o = __dsub_rn(fi, sum);
+                else
+                    o = __dadd_rn(xval<MODE, false>(hr, x, f, aux, omega),
+                                  __ddiv_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), hub_d[q]));
+                emit_row(hr, o);
+            };
+            auto add_chain = [&](const double *b, int len, double sum) {
+                int k = 0;
+                for (; k + 8 <= len; k += 8) {
+                    double t[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) t[j] = b[k + j];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) sum = __dadd_rn(sum, t[j]);
+                }
+                for (; k < len; ++k) sum = __dadd_rn(sum, b[k]);
+                return sum;
+            };
+            if (hub_off[nh] <= seg) {  // all rows at once: products, then one thread per row adds
+                for (int k = threadIdx.x; k < hub_off[nh]; k += blockDim.x) {
+                    int q = 0;
+                    while (hub_off[q + 1] <= k) ++q;
+                    const int hr = hub_rows[q];
+                    const int ke = rp[hr] + (k - hub_off[q]);
+                    const int c = eg.col(ke, hr);
+                    const double a = eg.val(ke);
+                    buf[k] = __dmul_rn(a, xval<MODE, false>(c, x, f, aux, omega));
+                    if (MODE >= M_JACOBI && c == hr) hub_d[q] = a;
+                }
+                __syncthreads();
+                if (static_cast<int>(threadIdx.x) < nh) {
+                    const int q = threadIdx.x;
+                    finish(q, add_chain(buf + hub_off[q], hub_off[q + 1] - hub_off[q], 0.0));
+                }
+            } else {  // row by row in segments of the buffer
+                for (int q = 0; q < nh; ++q) {
+                    const int hr = hub_rows[q];
+                    const int rs = rp[hr], re = rp[hr + 1];
+                    double sum = 0.0;
+                    for (int s0 = rs; s0 < re; s0 += seg) {
+                        const int s1 = min(re, s0 + seg);
+                        __syncthreads();  // the previous segment's adds are done with buf
+                        for (int k = s0 + static_cast<int>(threadIdx.x); k < s1; k += blockDim.x) {
+                            const int c = eg.col(k, hr);
+                            const double a = eg.val(k);
+                            buf[k - s0] = __dmul_rn(a, xval<MODE, false>(c, x, f, aux, omega));
+                            if (MODE >= M_JACOBI && c == hr) hub_d[q] = a;
+                        }
+                        __syncthreads();
+                        if (threadIdx.x == 0) sum = add_chain(buf, s1 - s0, sum);
+                    }
+                    if (threadIdx.x == 0) finish(q, sum);
+                }
+            }
         }
     }
     if constexpr (NV > 0) finish_reduction<NV>(red, acc);

@@ -11,7 +11,7 @@ from paper_2007_00056_b200 import sparsh as sp, _lib  # noqa
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "C2"
 A = {"C2": lambda: sp.poisson3d(128), "T256": lambda: sp.poisson3d(256), "C1": lambda: sp.poisson2d(1024, 1024),
-     "P27": lambda: sp.poisson3d_27(128), "P27_256": lambda: sp.poisson3d_27(256)}[wl]()
+     "P27": lambda: sp.poisson3d_27(128), "P27_256": lambda: sp.poisson3d_27(256), "G128": lambda: sp.graph_laplacian3d(128, seed=7)}[wl]()
 cfg = sp.SolverConfig(smoother=sp.SmootherKind.weighted_jacobi(), max_levels=40)
 h = sp.Hierarchy(A, cfg)
 ctx = h.ctx()
