@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kBoxThreads, SB_BOX_MINB)
     };
     auto fin = [&](double xi, double fi, double sum, double dg, double ry) -> double {
         if constexpr (MODE == M_SPMV) return sum;
-        else if constexpr (MODE == M_RESID || MODE == M_RESID_RESTRICT) return __dsub_rn(fi, sum);
+        else if constexpr (MODE == M_RESID) return __dsub_rn(fi, sum);
         else return __dadd_rn(xi, div_rn(__dmul_rn(omega, __dsub_rn(fi, sum)), dg, ry));
     };
     // the pattern bytes are constant: the first pair's before the dependency
