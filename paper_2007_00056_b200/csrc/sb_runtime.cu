@@ -451,6 +451,9 @@ __device__ __forceinline__ double row_eval(int row, int rs, int re, const E &e, 
 
 // Rows longer than this are evaluated by a whole warp (k_csr_tile).
 constexpr int kLongRow = 32;
+#ifndef SB_TILE_U
+#define SB_TILE_U 4  // gathers in flight per row step in k_csr_tile (G128: 4 -> 67.0 ms, 6 -> 67.5, 8 -> 70.3 with spills, 2 -> 70.9, 16 -> 93.3)
+#endif
 // Rows longer than this (up to kHubMax per CTA; e.g. the hub row a stalled
 // coarsening leaves: ~560 entries on G128's deep levels) are deferred to the
 // end of k_csr_tile and evaluated by the whole CTA: every product at once into
@@ -537,8 +540,11 @@ __host__ __device__ __forceinline__ size_t stage_bytes_of(int cap, int vf, int c
            static_cast<size_t>(kFWin) * 8;
 }
 
+#ifndef SB_TILE_MINB
+#define SB_TILE_MINB 3
+#endif
 template <int MODE, int NV, int VF, int CF>
-__global__ void __launch_bounds__(kTileRows, 3)
+__global__ void __launch_bounds__(kTileRows, SB_TILE_MINB)
     k_csr_tile(const int32_t *__restrict__ rp, const void *__restrict__ cols, const void *__restrict__ vals,
                const double *__restrict__ dict, int ndict, const int32_t *__restrict__ tile_ptr, int ntiles,
                const double *__restrict__ x, const double *__restrict__ f, double *__restrict__ out,
@@ -653,7 +659,7 @@ __global__ void __launch_bounds__(kTileRows, 3)
             // rows longer than kLongRow go to the whole warp (below)
             const unsigned lm = __ballot_sync(0xffffffffu, row < r1 && srp[row + 1] - srp[row] > kLongRow);
             if (row < r1 && !((lm >> lane) & 1u))
-                emit_row(row, row_eval<MODE, false>(row, srp[row], srp[row + 1], e, x, f, rhs_of(row), aux, omega));
+                emit_row(row, row_eval<MODE, false, SB_TILE_U>(row, srp[row], srp[row + 1], e, x, f, rhs_of(row), aux, omega));
             for (unsigned m = lm; m; m &= m - 1) {  // gathers 32 entries at a time, sum in CSR order
                 const int src = __ffs(m) - 1;
                 const int lr = row - lane + src;
