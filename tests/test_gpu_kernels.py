@@ -156,3 +156,39 @@ def test_27point_varied_bitexact(sp, oracle_best, dims):
     assert np.array_equal(sp.smooth(jac, A, x, f, 3), oracle_best.jacobi(A, 2.0 / 3.0, x, f, 3))
     x[[40, 41, 200]] = [np.inf, np.nan, -np.inf]  # non-finite values inside interior rows
     assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x), equal_nan=True)
+
+
+@pytest.mark.parametrize("case", ["many-in-one-tile", "spread", "longer-than-buffer"])
+def test_csr_tile_long_rows_cta_path(sp, oracle_best, case, monkeypatch):
+    """k_csr_tile defers rows of > 32 entries (up to 16 per CTA) to the end of
+    the kernel, where the whole CTA forms their products and one thread per row
+    adds them in CSR order; more rows per CTA take the warp path, and a row
+    longer than the drained stage buffers is added segment by segment. SpMV,
+    residual and Jacobi must stay the reference's bits in every case."""
+    monkeypatch.setenv("SB_SELL", "0")
+    monkeypatch.setenv("SB_RPAT", "0")
+    rng = np.random.default_rng({"many-in-one-tile": 1, "spread": 2, "longer-than-buffer": 3}[case])
+    n = {"many-in-one-tile": 600, "spread": 3000, "longer-than-buffer": 9000}[case]
+    hubs = {"many-in-one-tile": list(range(10, 240, 10)),            # 23 long rows in the first tile
+            "spread": list(rng.choice(n, 40, replace=False)),         # long rows across many tiles
+            "longer-than-buffer": [5, 4000]}[case]                    # rows with ~n entries
+    ent = {}
+    for i in range(n):
+        ent[(i, i)] = 4.0
+        for j in (i - 1, i + 1):
+            if 0 <= j < n:
+                ent[(i, j)] = -1.0
+    for h in hubs:
+        cols = np.arange(n) if case == "longer-than-buffer" else rng.choice(n, int(rng.integers(33, 400)),
+                                                                              replace=False)
+        for j in cols:
+            if j != h:
+                ent[(int(h), int(j))] = -float(rng.uniform(0.001, 0.01))
+        ent[(int(h), int(h))] = 4.0 + float(len(cols)) * 0.01
+    A = sp.CsrMatrix.from_triplets(n, n, [(r, c, v) for (r, c), v in ent.items()])
+    x = rng.uniform(-1, 1, n)
+    f = rng.uniform(-1, 1, n)
+    assert np.array_equal(sp.spmv(A, x), oracle_best.spmv(A, x))
+    assert np.array_equal(sp.residual(A, x, f), oracle_best.residual(A, x, f))
+    jac = sp.SmootherKind.weighted_jacobi()
+    assert np.array_equal(sp.smooth(jac, A, x, f, 3), oracle_best.jacobi(A, 2.0 / 3.0, x, f, 3))
