@@ -1422,9 +1422,10 @@ struct X0 {
     const double *diag = nullptr;
     double *x0 = nullptr;
     double omega = 0.0;
-    // row-pattern level 0: a_ii = pdg[pid[i]] (1 B per row instead of the 8 B diagonal)
+    // row-pattern level 0: a_ii = pdg[pid[i]] (1 B per row instead of the 8 B
+    // diagonal) and RN(1/a_ii) = pry[pid[i]] for the Markstein quotient
     const uint8_t *pid = nullptr;
-    const double *pdg = nullptr;
+    const double *pdg = nullptr, *pry = nullptr;
     __device__ __forceinline__ void put(int64_t i, double v) const {
         if (x0) x0[i] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(omega, v), diag[i]));
     }
@@ -1484,21 +1485,24 @@ __device__ __forceinline__ bool x0_ok(const X0 &z0) {
 }
 template <int V> __device__ __forceinline__ void x0_put(const X0 &z0, int64_t i, const DV<V> &v) {
     if (!z0.x0) return;
-    DV<V> d;
-    if (z0.pid) {
+    DV<V> o;
+    if (z0.pid) {  // table a_ii and its reciprocal: div_rn is the IEEE quotient (its range checks fall back)
+        int p[V];
         if constexpr (V == 2) {
             const uint32_t pp = *reinterpret_cast<const uint16_t *>(z0.pid + i);
-            d.v[0] = __ldg(z0.pdg + (pp & 0xff));
-            d.v[1] = __ldg(z0.pdg + (pp >> 8));
+            p[0] = pp & 0xff;
+            p[V - 1] = pp >> 8;
         } else {
-            d.v[0] = __ldg(z0.pdg + z0.pid[i]);
+            p[0] = z0.pid[i];
         }
-    } else {
-        d = ldv<V>(z0.diag, i);
-    }
-    DV<V> o;
 #pragma unroll
-    for (int k = 0; k < V; ++k) o.v[k] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z0.omega, v.v[k]), d.v[k]));
+        for (int k = 0; k < V; ++k)
+            o.v[k] = __dadd_rn(0.0, div_rn(__dmul_rn(z0.omega, v.v[k]), __ldg(z0.pdg + p[k]), __ldg(z0.pry + p[k])));
+    } else {
+        const DV<V> d = ldv<V>(z0.diag, i);
+#pragma unroll
+        for (int k = 0; k < V; ++k) o.v[k] = __dadd_rn(0.0, __ddiv_rn(__dmul_rn(z0.omega, v.v[k]), d.v[k]));
+    }
     stv<V>(z0.x0, i, o);
 }
 
@@ -2485,6 +2489,7 @@ static X0 level0_x0(sb_ctx c, double *x0, double omega) {
     if (x0 && l0.pat && l0.pat_np > 0) {
         z.pid = l0.pat_id;
         z.pdg = reinterpret_cast<const double *>(l0.pat_table) + static_cast<size_t>(l0.pat_np) * ((l0.pat_w + 1) & ~1);
+        z.pry = z.pdg + l0.pat_np;
     }
     return z;
 }
